@@ -1,0 +1,196 @@
+/*
+ * microadam_cuda.h — C ABI of libmicroadam_cuda: the B200 (sm_100a) MicroAdam
+ * optimizer step behind plain pointers and sizes (no C++ / torch types).
+ *
+ * It replaces, for the blockwise practical engine, the reference's
+ *   microadam::MicroAdamOptimizer            (proj/include/microadam/optim.hpp:98-128,
+ *                                             proj/src/optim.cpp:127-190)
+ *   microadam::HyperParams / validate        (optim.hpp:15-30, optim.cpp:7-30)
+ *   microadam::StepReport                    (optim.hpp:32-38)
+ *   microadam::GradientWindow, QuantizedErrorBuffer state inspection
+ *                                            (window.hpp:10-33, quantize.hpp:54-70)
+ * Paths are relative to the reference root /root/reference. Each entry point
+ * names the reference symbol it stands in for. INTEGRATION.md shows the
+ * reference-side binding (a C++ Optimizer adapter and a ctypes stub).
+ *
+ * Error model: every call returns ma_status; the reference's throw sites map
+ * to codes (std::invalid_argument -> MA_ERR_INVALID_ARG / MA_ERR_DIM /
+ * MA_ERR_NONFINITE, std::logic_error -> MA_ERR_STATE). ma_last_error() gives
+ * the message for the calling thread. No exception crosses the ABI.
+ *
+ * Threading: one handle is bound to one device; calls on one handle must be
+ * serialized (the reference optimizer is not thread-safe either).
+ */
+#ifndef MICROADAM_CUDA_H
+#define MICROADAM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MA_API __attribute__((visibility("default")))
+#else
+#define MA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MA_ABI_VERSION 1
+
+typedef enum ma_status {
+    MA_OK = 0,
+    MA_ERR_INVALID_ARG = 1, /* HyperParams::validate / BlockLayout ctor throws (optim.cpp:7-21, compress.cpp:19-26) */
+    MA_ERR_DIM = 2,         /* "step: gradient dim mismatch" (optim.cpp:34-35) */
+    MA_ERR_NONFINITE = 3,   /* check_finite on the gradient (optim.cpp:36, vec.hpp:41-45) */
+    MA_ERR_CUDA = 4,        /* CUDA runtime failure */
+    MA_ERR_NCCL = 5,        /* collective failure (multi-GPU helpers) */
+    MA_ERR_UNSUPPORTED = 6, /* legal reference config this build does not run on device */
+    MA_ERR_STATE = 7        /* e.g. error_buffer() on a lossless engine (optim.cpp:155-158) */
+} ma_status;
+
+typedef enum ma_dtype { MA_F64 = 0, MA_F32 = 1, MA_BF16 = 2 } ma_dtype;
+
+/* Non-finite gradient handling (reference: check_grad throws before any
+ * mutation, optim.cpp:34-37). */
+typedef enum ma_finite_mode {
+    MA_FINITE_FLAG = 0,   /* fused check; flag read at ma_sync(); state undefined after a hit */
+    MA_FINITE_STRICT = 1, /* pre-scan + host sync; rejects before mutation (reference-exact) */
+    MA_FINITE_OFF = 2     /* no check */
+} ma_finite_mode;
+
+/* Mirrors microadam::HyperParams (optim.hpp:15-30). k <= 0 means "unset". */
+typedef struct ma_hyperparams {
+    double beta1;        /* 0.9 */
+    double beta2;        /* 0.999 */
+    double eps;          /* 1e-8 */
+    double lr;           /* 1e-3 (used by ma_step_host; ma_step takes lr per call) */
+    double weight_decay; /* 0; unused by the practical engine, as in the reference */
+    int64_t window;      /* m = 10 */
+    double density;      /* 0.01 */
+    int64_t k;           /* explicit selection count, overrides density; <= 0 unset */
+    int32_t bits;        /* 4 */
+    int32_t reserved0;
+    int64_t block;       /* B_d = 4096 */
+    int64_t bucket;      /* B_q = 64 */
+} ma_hyperparams;
+
+typedef struct ma_config {
+    ma_hyperparams hp;
+    int32_t blockwise;      /* 1 (the device path); 0 = global Top-K, run as one block when d <= 8192 */
+    int32_t lossless_error; /* 0 (quantized EF); 1 unsupported on device */
+    int32_t param_dtype;    /* ma_dtype of θ in device memory */
+    int32_t grad_dtype;     /* ma_dtype of the gradient */
+    int32_t value_dtype;    /* ma_dtype of window values (bf16 = the paper's layout) */
+    int32_t finite_mode;    /* ma_finite_mode */
+} ma_config;
+
+/* Mirrors microadam::StepReport (optim.hpp:32-38). Norms are reduced in a
+ * fixed tree order (≠ the reference's sequential sum: within 1e-12 relative);
+ * update_nnz is exact. loss is left 0 (filled by run() in the reference). */
+typedef struct ma_step_report {
+    double grad_norm;
+    double error_norm;
+    double empirical_q;
+    int64_t update_nnz;
+    double loss;
+} ma_step_report;
+
+/* Derived layout (optim.cpp:137-144, compress.cpp:28-33, quantize.hpp:67). */
+typedef struct ma_layout_info {
+    int64_t dim;          /* parameters covered by this layout (shard length for shards) */
+    int64_t block;        /* min(hp.block, global dim) */
+    int64_t per_block_k;  /* min(ceil(density*block), block) */
+    int64_t num_blocks;   /* blocks covered */
+    int64_t row_width;    /* Σ_b min(per_block_k, len_b) = window row width k_ */
+    int64_t num_buckets;  /* EF buckets covered */
+    int64_t code_bytes;   /* packed EF bytes covered */
+    int64_t kb_stride;    /* device window entries reserved per (block, slot) */
+    int64_t state_bytes;  /* device optimizer-state bytes (EF codes + meta + window) */
+} ma_layout_info;
+
+typedef struct ma_handle ma_handle;
+
+/* Defaults of HyperParams (optim.hpp:15-30) + device dtypes f32/f32/bf16, flag mode. */
+MA_API void ma_config_default(ma_config* cfg);
+
+/* HyperParams::validate (optim.cpp:7-21) + resolve_k (:23-30) + BlockLayout
+ * checks + device support checks, without allocating anything. */
+MA_API ma_status ma_validate(const ma_config* cfg, int64_t dim);
+
+/* Layout for the whole vector (block_begin=0, block_end=-1) or a block range. */
+MA_API ma_status ma_layout(const ma_config* cfg, int64_t dim, int64_t block_begin, int64_t block_end,
+                    ma_layout_info* out);
+
+/* MicroAdamOptimizer ctor (optim.cpp:127-153): zero EF buffer (quantize.cpp:130-140),
+ * empty window (window.cpp:5-12). θ stays caller-owned (see ma_step). */
+MA_API ma_status ma_create(const ma_config* cfg, int64_t dim, int device, ma_handle** out);
+
+/* Same, owning only blocks [block_begin, block_end) of a dim-length vector
+ * (block-aligned data-parallel shard). Pointers passed to
+ * ma_step then address the shard's slice (element block_begin*block). */
+MA_API ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin,
+                          int64_t block_end, int device, ma_handle** out);
+
+MA_API ma_status ma_destroy(ma_handle* h);
+
+/* MicroAdamOptimizer::step (optim.cpp:164-190) on device memory:
+ * d_params (param_dtype, updated in place) and d_grads (grad_dtype), both
+ * covering the handle's range; lr replaces hp.lr; stream is a cudaStream_t
+ * (NULL = legacy default). Asynchronous unless report != NULL or
+ * finite_mode == MA_FINITE_STRICT. */
+MA_API ma_status ma_step(ma_handle* h, void* d_params, const void* d_grads, double lr, void* stream,
+                  ma_step_report* report);
+
+/* Drop-in host path for Optimizer::step(const Vec&) + params(): h_grads and
+ * h_params are HOST buffers (pinned or pageable, grad/param dtype). The handle
+ * keeps a device copy of θ (uploaded from h_params on the first call or after
+ * ma_set_params), streams the gradient up and the updated θ back in chunks
+ * that overlap the step, and returns when h_params holds the new θ. */
+MA_API ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double lr,
+                       ma_step_report* report);
+
+/* Wait for outstanding work; returns MA_ERR_NONFINITE if the fused check hit. */
+MA_API ma_status ma_sync(ma_handle* h);
+
+/* window().step / head / filled and the m row stamps (window.hpp:10-33). */
+MA_API ma_status ma_get_counters(const ma_handle* h, int64_t* step, int64_t* head, int64_t* filled,
+                          int64_t* stamps /* m entries, may be NULL */);
+
+/* error_buffer() (optim.cpp:155-158): packed codes (code_bytes) and per-bucket
+ * (lo, hi) as fp64 (num_buckets each), host buffers, for the handle's range. */
+MA_API ma_status ma_read_error_buffer(ma_handle* h, uint8_t* codes, double* lo, double* hi);
+
+/* window().rows[slot] in the reference layout: row_width global int64 indices
+ * (ascending) and values widened to fp64. Returns MA_ERR_INVALID_ARG for slot
+ * out of range. An unwritten row reads back as zeros. */
+MA_API ma_status ma_read_window_row(ma_handle* h, int64_t slot, int64_t* indices, double* values);
+
+/* Restore state (checkpoint resume; inverse of the three readers above). */
+MA_API ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, const double* hi,
+                         int64_t step, int64_t head, const int64_t* stamps,
+                         const int64_t* win_indices /* m*row_width */,
+                         const double* win_values /* m*row_width */);
+
+/* For ma_step_host: replace the device copy of θ from a host buffer. */
+MA_API ma_status ma_set_params(ma_handle* h, const void* h_params);
+
+MA_API ma_status ma_get_layout(const ma_handle* h, ma_layout_info* out);
+
+/* Number of step-kernel launches issued so far by this handle (all kernels). */
+MA_API int64_t ma_kernel_launches(const ma_handle* h);
+
+MA_API const char* ma_last_error(void);
+MA_API const char* ma_version(void);
+
+/* Synthetic gradient generator on device (include/ma_synth.h stream rounded
+ * to dtype), for benches: out[i] = round(value(seed, step, offset + i)). */
+MA_API ma_status ma_fill_synthetic(void* d_out, int32_t dtype, int64_t n, uint64_t seed, uint64_t step,
+                            int64_t offset, int32_t levels, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MICROADAM_CUDA_H */

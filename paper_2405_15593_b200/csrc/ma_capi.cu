@@ -1,0 +1,639 @@
+// ma_capi.cu — host side of libmicroadam_cuda: the C ABI declared in
+// include/microadam_cuda.h. Owns the per-handle device state (EF codes,
+// bucket grids, window ring), the host counters of the reference's
+// GradientWindow (step/head/filled/stamps, window.hpp:10-33), the glibc
+// pow() weights (window.cpp:37,43 — computed here, on the host, exactly as the
+// reference does) and kernel launches. No exception crosses the ABI.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/microadam_cuda.h"
+#include "ma_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ma_status fail(ma_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+ma_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(MA_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define MA_CUDA(call)                                      \
+    do {                                                   \
+        cudaError_t _e = (call);                           \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+size_t dtype_size(int dt) { return dt == MA_F64 ? 8 : (dt == MA_F32 ? 4 : 2); }
+
+// Resolved shape of a (possibly sharded) configuration.
+struct Shape {
+    int64_t dim_global = 0;
+    int64_t block = 0;       // min(hp.block, dim) (optim.cpp:140)
+    int64_t per_block_k = 0; // compress.cpp:28-33
+    int64_t nblocks_global = 0;
+    int64_t b0 = 0, b1 = 0;  // owned block range
+    int64_t elem0 = 0, dim = 0;
+    int64_t row_width = 0;   // Σ_b∈[b0,b1) min(per_block_k, len_b)
+    int64_t bucket = 0, nbuckets = 0, bucket0 = 0;
+    int64_t code_bytes = 0;
+    int64_t kb_stride = 0;
+};
+
+// HyperParams::validate (optim.cpp:7-21) — same checks, same order.
+ma_status validate_hp(const ma_hyperparams& hp) {
+    if (!(hp.beta1 > 0.0 && hp.beta1 < 1.0))
+        return fail(MA_ERR_INVALID_ARG, "HyperParams: beta1 must be in (0,1)");
+    if (!(hp.beta2 > 0.0 && hp.beta2 < 1.0))
+        return fail(MA_ERR_INVALID_ARG, "HyperParams: beta2 must be in (0,1)");
+    if (!(hp.eps > 0.0)) return fail(MA_ERR_INVALID_ARG, "HyperParams: eps must be > 0");
+    if (!(hp.lr > 0.0)) return fail(MA_ERR_INVALID_ARG, "HyperParams: lr must be > 0");
+    if (!(hp.weight_decay >= 0.0))
+        return fail(MA_ERR_INVALID_ARG, "HyperParams: weight_decay must be >= 0");
+    if (hp.window < 1) return fail(MA_ERR_INVALID_ARG, "HyperParams: window must be >= 1");
+    if (!(hp.density > 0.0) || hp.density > 1.0)
+        return fail(MA_ERR_INVALID_ARG, "HyperParams: density must be in (0,1]");
+    if (hp.bits < 1 || hp.bits > 24)
+        return fail(MA_ERR_INVALID_ARG, "HyperParams: bits must be in [1,24]");
+    if (hp.block < 1 || hp.block > 32767)
+        return fail(MA_ERR_INVALID_ARG, "HyperParams: block must be in [1, 32767]");
+    if (hp.bucket < 1) return fail(MA_ERR_INVALID_ARG, "HyperParams: bucket must be >= 1");
+    return MA_OK;
+}
+
+ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b1, Shape* out) {
+    if (!cfg || !out) return fail(MA_ERR_INVALID_ARG, "null argument");
+    ma_status st = validate_hp(cfg->hp);
+    if (st != MA_OK) return st;
+    const ma_hyperparams& hp = cfg->hp;
+    if (dim < 1) return fail(MA_ERR_INVALID_ARG, "MicroAdamOptimizer: empty parameter vector");
+    if (hp.k > dim) return fail(MA_ERR_INVALID_ARG, "HyperParams: k exceeds dimension");
+    for (int dt : {cfg->param_dtype, cfg->grad_dtype, cfg->value_dtype})
+        if (dt < MA_F64 || dt > MA_BF16) return fail(MA_ERR_INVALID_ARG, "unknown dtype");
+    if (cfg->finite_mode < MA_FINITE_FLAG || cfg->finite_mode > MA_FINITE_OFF)
+        return fail(MA_ERR_INVALID_ARG, "unknown finite_mode");
+    if (cfg->lossless_error)
+        return fail(MA_ERR_UNSUPPORTED, "lossless_error (dense EF test hook) is not on the device path");
+    if (hp.bits != 4) return fail(MA_ERR_UNSUPPORTED, "device path implements bits = 4");
+    if (hp.window > ma::kMaxWindow) return fail(MA_ERR_UNSUPPORTED, "window > 256 not supported on device");
+
+    Shape s;
+    s.dim_global = dim;
+    if (cfg->blockwise) {
+        // optim.cpp:137-144: density = k/d when k is set; block = min(block, d).
+        const double density = hp.k > 0 ? static_cast<double>(hp.k) / static_cast<double>(dim)
+                                        : hp.density;
+        if (!(density > 0.0) || density > 1.0)
+            return fail(MA_ERR_INVALID_ARG, "BlockLayout: density must be in (0, 1]");
+        s.block = hp.block < dim ? hp.block : dim;
+        int64_t k = static_cast<int64_t>(std::ceil(density * static_cast<double>(s.block)));
+        s.per_block_k = k < s.block ? k : s.block;
+        if (s.per_block_k < 1)
+            return fail(MA_ERR_INVALID_ARG, "BlockLayout: per_block_k must be in [1, block]");
+    } else {
+        // Global Top-K (compress.cpp:66-71) == one block spanning d.
+        s.block = dim;
+        int64_t k = hp.k > 0 ? hp.k
+                             : static_cast<int64_t>(std::ceil(hp.density * static_cast<double>(dim)));
+        s.per_block_k = k < 1 ? 1 : (k > dim ? dim : k);
+    }
+    if (s.block > ma::kMaxBlock)
+        return fail(MA_ERR_UNSUPPORTED, "block (or global-mode dim) > 8192 not supported on device");
+    s.nblocks_global = (dim + s.block - 1) / s.block;
+    if (s.nblocks_global > 1 && (s.block % hp.bucket != 0 || s.block % 2 != 0))
+        return fail(MA_ERR_UNSUPPORTED,
+                    "device path needs bucket | block and an even block when d > block");
+    if (b1 < 0) b1 = s.nblocks_global;
+    if (b0 < 0 || b0 >= b1 || b1 > s.nblocks_global)
+        return fail(MA_ERR_INVALID_ARG, "shard block range out of bounds");
+    s.b0 = b0;
+    s.b1 = b1;
+    s.elem0 = b0 * s.block;
+    const int64_t elem1 = b1 * s.block < dim ? b1 * s.block : dim;
+    s.dim = elem1 - s.elem0;
+    s.row_width = 0;
+    for (int64_t b = b0; b < b1; ++b) {
+        const int64_t len = (b + 1) * s.block <= dim ? s.block : dim - b * s.block;
+        s.row_width += s.per_block_k < len ? s.per_block_k : len;
+    }
+    s.bucket = hp.bucket;
+    s.bucket0 = s.elem0 / hp.bucket;
+    s.nbuckets = (s.dim + hp.bucket - 1) / hp.bucket;
+    s.code_bytes = (s.dim * 4 + 7) / 8;
+    s.kb_stride = (s.per_block_k + 7) / 8 * 8;
+    *out = s;
+    return MA_OK;
+}
+
+void fill_layout(const Shape& s, const ma_config& cfg, ma_layout_info* o) {
+    o->dim = s.dim;
+    o->block = s.block;
+    o->per_block_k = s.per_block_k;
+    o->num_blocks = s.b1 - s.b0;
+    o->row_width = s.row_width;
+    o->num_buckets = s.nbuckets;
+    o->code_bytes = s.code_bytes;
+    o->kb_stride = s.kb_stride;
+    const int64_t went = o->num_blocks * cfg.hp.window * s.kb_stride;
+    o->state_bytes = s.code_bytes + s.nbuckets * 16 + went * (2 + int64_t(dtype_size(cfg.value_dtype)));
+}
+
+}  // namespace
+
+struct ma_handle {
+    ma_config cfg{};
+    Shape shape;
+    ma::Variant variant{};
+    int device = 0;
+    uint8_t* d_codes = nullptr;
+    double2* d_meta = nullptr;
+    int16_t* d_win_idx = nullptr;
+    void* d_win_val = nullptr;
+    unsigned int* d_flag = nullptr;
+    double* d_partials = nullptr;
+    double* d_report = nullptr;
+    // host counters (window.hpp:10-33)
+    int64_t step = 0, head = 0, filled = 0;
+    std::vector<int64_t> stamps;
+    // host path (ma_step_host)
+    void* d_theta = nullptr;
+    void* d_gstage = nullptr;
+    bool theta_valid = false;
+    cudaStream_t host_stream = nullptr;
+    cudaStream_t last_stream = nullptr;
+    int64_t launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void free_handle(ma_handle* h) {
+    if (!h) return;
+    DeviceGuard g(h->device);
+    cudaFree(h->d_codes);
+    cudaFree(h->d_meta);
+    cudaFree(h->d_win_idx);
+    cudaFree(h->d_win_val);
+    cudaFree(h->d_flag);
+    cudaFree(h->d_partials);
+    cudaFree(h->d_report);
+    cudaFree(h->d_theta);
+    cudaFree(h->d_gstage);
+    if (h->host_stream) cudaStreamDestroy(h->host_stream);
+    delete h;
+}
+
+// Advance the host counters exactly like GradientWindow::push (window.cpp:14-26)
+// and build the kernel weights like adam_stats (window.cpp:28-46).
+int64_t push_and_weights(ma_handle* h, ma::StepArgs* a) {
+    const ma_hyperparams& hp = h->cfg.hp;
+    const int64_t slot = h->head;
+    ++h->step;
+    h->stamps[size_t(slot)] = h->step;
+    h->head = (h->head + 1) % hp.window;
+    h->filled = h->step < hp.window ? h->step : hp.window;
+    for (int64_t r = 0; r < h->filled; ++r) {
+        // Rows with stamp 0 are skipped by the reference (window.cpp:33); with
+        // rows written in slot order every r < filled has a stamp.
+        a->w1[r] = std::pow(hp.beta1, static_cast<double>(h->step - h->stamps[size_t(r)]));
+        a->w2[r] = std::pow(hp.beta2, static_cast<double>(h->step - h->stamps[size_t(r)]));
+    }
+    a->scale1 = (1.0 - hp.beta1) / (1.0 - std::pow(hp.beta1, static_cast<double>(h->step)));
+    a->scale2 = (1.0 - hp.beta2) / (1.0 - std::pow(hp.beta2, static_cast<double>(h->step)));
+    a->filled = static_cast<int32_t>(h->filled);
+    a->slot = static_cast<int32_t>(slot);
+    return slot;
+}
+
+void base_args(ma_handle* h, ma::StepArgs* a) {
+    std::memset(a, 0, sizeof(*a));
+    const Shape& s = h->shape;
+    a->codes = h->d_codes;
+    a->meta = h->d_meta;
+    a->win_idx = h->d_win_idx;
+    a->win_val = h->d_win_val;
+    a->flag = h->d_flag;
+    a->dim = s.dim;
+    a->num_blocks = s.b1 - s.b0;
+    a->block = static_cast<int32_t>(s.block);
+    a->per_block_k = static_cast<int32_t>(s.per_block_k);
+    a->kb_stride = static_cast<int32_t>(s.kb_stride);
+    a->bucket = static_cast<int32_t>(s.bucket);
+    a->m = static_cast<int32_t>(h->cfg.hp.window);
+    a->check_finite = h->cfg.finite_mode == MA_FINITE_FLAG ? 1 : 0;
+    a->g_dtype = h->cfg.grad_dtype;
+    a->p_dtype = h->cfg.param_dtype;
+    a->v_dtype = h->cfg.value_dtype;
+    a->eps = h->cfg.hp.eps;
+}
+
+ma_status finish_report(ma_handle* h, cudaStream_t st, ma_step_report* report) {
+    MA_CUDA(ma::launch_report_reduce(h->d_partials, h->shape.b1 - h->shape.b0, h->d_report, st));
+    ++h->launches;
+    double r[ma::kReportFields];
+    MA_CUDA(cudaMemcpyAsync(r, h->d_report, sizeof(r), cudaMemcpyDeviceToHost, st));
+    MA_CUDA(cudaStreamSynchronize(st));
+    const double na = std::sqrt(r[1]);
+    report->grad_norm = std::sqrt(r[0]);
+    report->empirical_q = na > 0.0 ? std::sqrt(r[2]) / na : 0.0;
+    report->error_norm = std::sqrt(r[3]);
+    report->update_nnz = static_cast<int64_t>(r[4]);
+    report->loss = 0.0;
+    return MA_OK;
+}
+
+ma_status strict_prescan(ma_handle* h, const void* d_grads, cudaStream_t st) {
+    MA_CUDA(cudaMemsetAsync(h->d_flag, 0, sizeof(unsigned), st));
+    MA_CUDA(ma::launch_finite_scan(d_grads, h->cfg.grad_dtype, h->shape.dim, h->d_flag, st));
+    ++h->launches;
+    unsigned flag = 0;
+    MA_CUDA(cudaMemcpyAsync(&flag, h->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, st));
+    MA_CUDA(cudaStreamSynchronize(st));
+    if (flag) return fail(MA_ERR_NONFINITE, "step gradient: non-finite entry");
+    return MA_OK;
+}
+
+ma_status run_step(ma_handle* h, void* d_params, const void* d_grads, double lr, cudaStream_t st,
+                   ma_step_report* report) {
+    if (!(lr > 0.0)) return fail(MA_ERR_INVALID_ARG, "step: lr must be > 0");
+    if (!d_params || !d_grads) return fail(MA_ERR_INVALID_ARG, "step: null buffer");
+    if (h->cfg.finite_mode == MA_FINITE_STRICT) {
+        ma_status s = strict_prescan(h, d_grads, st);
+        if (s != MA_OK) return s;
+    }
+    ma::StepArgs a;
+    base_args(h, &a);
+    a.grads = d_grads;
+    a.params = d_params;
+    a.lr = lr;
+    a.partials = report ? h->d_partials : nullptr;
+    push_and_weights(h, &a);
+    MA_CUDA(ma::launch_step(a, h->variant, h->shape.b1 - h->shape.b0, st));
+    ++h->launches;
+    h->last_stream = st;
+    if (report) return finish_report(h, st, report);
+    return MA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ma_config_default(ma_config* cfg) {
+    if (!cfg) return;
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->hp.beta1 = 0.9;
+    cfg->hp.beta2 = 0.999;
+    cfg->hp.eps = 1e-8;
+    cfg->hp.lr = 1e-3;
+    cfg->hp.weight_decay = 0.0;
+    cfg->hp.window = 10;
+    cfg->hp.density = 0.01;
+    cfg->hp.k = 0;
+    cfg->hp.bits = 4;
+    cfg->hp.block = 4096;
+    cfg->hp.bucket = 64;
+    cfg->blockwise = 1;
+    cfg->lossless_error = 0;
+    cfg->param_dtype = MA_F32;
+    cfg->grad_dtype = MA_F32;
+    cfg->value_dtype = MA_BF16;
+    cfg->finite_mode = MA_FINITE_FLAG;
+}
+
+ma_status ma_validate(const ma_config* cfg, int64_t dim) {
+    Shape s;
+    return resolve_shape(cfg, dim, 0, -1, &s);
+}
+
+ma_status ma_layout(const ma_config* cfg, int64_t dim, int64_t block_begin, int64_t block_end,
+                    ma_layout_info* out) {
+    Shape s;
+    ma_status st = resolve_shape(cfg, dim, block_begin, block_end, &s);
+    if (st != MA_OK) return st;
+    if (!out) return fail(MA_ERR_INVALID_ARG, "null out");
+    fill_layout(s, *cfg, out);
+    return MA_OK;
+}
+
+ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin,
+                          int64_t block_end, int device, ma_handle** out) {
+    if (!out) return fail(MA_ERR_INVALID_ARG, "null out");
+    *out = nullptr;
+    Shape s;
+    ma_status st = resolve_shape(cfg, dim, block_begin, block_end, &s);
+    if (st != MA_OK) return st;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MA_ERR_CUDA, "no CUDA device visible (the device path has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(MA_ERR_INVALID_ARG, "device out of range");
+    DeviceGuard g(device);
+    ma_handle* h = new (std::nothrow) ma_handle();
+    if (!h) return fail(MA_ERR_INVALID_ARG, "out of host memory");
+    h->cfg = *cfg;
+    h->shape = s;
+    h->device = device;
+    h->variant = ma::pick_variant(static_cast<int>(s.block));
+    h->stamps.assign(size_t(cfg->hp.window), 0);
+    const int64_t nb = s.b1 - s.b0;
+    const size_t went = size_t(nb) * size_t(cfg->hp.window) * size_t(s.kb_stride);
+    const size_t smem = ma::step_smem_bytes(h->variant.nt, h->variant.ept, int(s.block),
+                                            int(s.bucket), int(cfg->hp.window), int(s.kb_stride));
+    int smem_max = 0;
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (smem > size_t(smem_max)) {
+        delete h;
+        return fail(MA_ERR_UNSUPPORTED, "block/window shape needs more shared memory than one SM has");
+    }
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](void** p, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(p, bytes ? bytes : 16);
+        if (e == cudaSuccess) e = cudaMemset(*p, 0, bytes ? bytes : 16);
+    };
+    alloc(reinterpret_cast<void**>(&h->d_codes), size_t(s.code_bytes));
+    alloc(reinterpret_cast<void**>(&h->d_meta), size_t(s.nbuckets) * sizeof(double2));
+    alloc(reinterpret_cast<void**>(&h->d_win_idx), went * sizeof(int16_t));
+    alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));
+    alloc(reinterpret_cast<void**>(&h->d_flag), sizeof(unsigned));
+    alloc(reinterpret_cast<void**>(&h->d_partials), size_t(nb) * ma::kReportFields * sizeof(double));
+    alloc(reinterpret_cast<void**>(&h->d_report), ma::kReportFields * sizeof(double));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        free_handle(h);
+        return cuda_fail(e, "ma_create");
+    }
+    *out = h;
+    return MA_OK;
+}
+
+ma_status ma_create(const ma_config* cfg, int64_t dim, int device, ma_handle** out) {
+    return ma_create_shard(cfg, dim, 0, -1, device, out);
+}
+
+ma_status ma_destroy(ma_handle* h) {
+    free_handle(h);
+    return MA_OK;
+}
+
+ma_status ma_step(ma_handle* h, void* d_params, const void* d_grads, double lr, void* stream,
+                  ma_step_report* report) {
+    if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
+    DeviceGuard g(h->device);
+    return run_step(h, d_params, d_grads, lr, static_cast<cudaStream_t>(stream), report);
+}
+
+ma_status ma_set_params(ma_handle* h, const void* h_params) {
+    if (!h || !h_params) return fail(MA_ERR_INVALID_ARG, "null argument");
+    DeviceGuard g(h->device);
+    const size_t pbytes = size_t(h->shape.dim) * dtype_size(h->cfg.param_dtype);
+    if (!h->d_theta) MA_CUDA(cudaMalloc(&h->d_theta, pbytes));
+    MA_CUDA(cudaMemcpy(h->d_theta, h_params, pbytes, cudaMemcpyHostToDevice));
+    h->theta_valid = true;
+    return MA_OK;
+}
+
+ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double lr,
+                       ma_step_report* report) {
+    if (!h || !h_params || !h_grads) return fail(MA_ERR_INVALID_ARG, "null argument");
+    DeviceGuard g(h->device);
+    const Shape& s = h->shape;
+    const size_t gsz = dtype_size(h->cfg.grad_dtype), psz = dtype_size(h->cfg.param_dtype);
+    if (!h->host_stream) MA_CUDA(cudaStreamCreateWithFlags(&h->host_stream, cudaStreamNonBlocking));
+    if (!h->d_gstage) MA_CUDA(cudaMalloc(&h->d_gstage, size_t(s.dim) * gsz));
+    if (!h->theta_valid) {
+        ma_status st = ma_set_params(h, h_params);
+        if (st != MA_OK) return st;
+    }
+    cudaStream_t st = h->host_stream;
+    if (h->cfg.finite_mode == MA_FINITE_STRICT || report) {
+        // Whole-vector path: strict pre-scan / report need the full gradient.
+        MA_CUDA(cudaMemcpyAsync(h->d_gstage, h_grads, size_t(s.dim) * gsz, cudaMemcpyHostToDevice, st));
+        ma_status r = run_step(h, h->d_theta, h->d_gstage, lr, st, report);
+        if (r != MA_OK) return r;
+        MA_CUDA(cudaMemcpyAsync(h_params, h->d_theta, size_t(s.dim) * psz, cudaMemcpyDeviceToHost, st));
+        MA_CUDA(cudaStreamSynchronize(st));
+        return ma_sync(h);
+    }
+    // Chunked pipeline: H2D grads of chunk c+1 overlaps the step of chunk c
+    // and the D2H of θ for chunk c-1 (two copy engines + SMs busy at once).
+    ma::StepArgs a;
+    base_args(h, &a);
+    a.grads = h->d_gstage;
+    a.params = h->d_theta;
+    a.lr = lr;
+    push_and_weights(h, &a);
+    const int64_t nb = s.b1 - s.b0;
+    const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(64) << 20) / (s.block * int64_t(gsz)));
+    const int64_t nchunks = (nb + chunk_blocks - 1) / chunk_blocks;
+    std::vector<cudaEvent_t> up(static_cast<size_t>(nchunks)), done(static_cast<size_t>(nchunks));
+    static thread_local cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    if (!s_h2d) MA_CUDA(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
+    if (!s_d2h) MA_CUDA(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
+    for (int64_t c = 0; c < nchunks; ++c) {
+        MA_CUDA(cudaEventCreateWithFlags(&up[size_t(c)], cudaEventDisableTiming));
+        MA_CUDA(cudaEventCreateWithFlags(&done[size_t(c)], cudaEventDisableTiming));
+    }
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t cb0 = c * chunk_blocks, cb1 = std::min(nb, cb0 + chunk_blocks);
+        const int64_t e0 = cb0 * s.block, e1 = std::min(s.dim, cb1 * s.block);
+        MA_CUDA(cudaMemcpyAsync(static_cast<char*>(h->d_gstage) + e0 * gsz,
+                                static_cast<const char*>(h_grads) + e0 * gsz, size_t(e1 - e0) * gsz,
+                                cudaMemcpyHostToDevice, s_h2d));
+        MA_CUDA(cudaEventRecord(up[size_t(c)], s_h2d));
+        MA_CUDA(cudaStreamWaitEvent(st, up[size_t(c)], 0));
+        a.block_offset = cb0;
+        MA_CUDA(ma::launch_step(a, h->variant, cb1 - cb0, st));
+        ++h->launches;
+        MA_CUDA(cudaEventRecord(done[size_t(c)], st));
+        MA_CUDA(cudaStreamWaitEvent(s_d2h, done[size_t(c)], 0));
+        MA_CUDA(cudaMemcpyAsync(static_cast<char*>(h_params) + e0 * psz,
+                                static_cast<const char*>(h->d_theta) + e0 * psz,
+                                size_t(e1 - e0) * psz, cudaMemcpyDeviceToHost, s_d2h));
+    }
+    MA_CUDA(cudaStreamSynchronize(s_d2h));
+    MA_CUDA(cudaStreamSynchronize(st));
+    for (int64_t c = 0; c < nchunks; ++c) {
+        cudaEventDestroy(up[size_t(c)]);
+        cudaEventDestroy(done[size_t(c)]);
+    }
+    h->last_stream = st;
+    return ma_sync(h);
+}
+
+ma_status ma_sync(ma_handle* h) {
+    if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
+    DeviceGuard g(h->device);
+    MA_CUDA(cudaDeviceSynchronize());
+    unsigned flag = 0;
+    MA_CUDA(cudaMemcpy(&flag, h->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
+    if (flag) {
+        MA_CUDA(cudaMemset(h->d_flag, 0, sizeof(unsigned)));
+        return fail(MA_ERR_NONFINITE, "step gradient: non-finite entry (state of that step is undefined)");
+    }
+    return MA_OK;
+}
+
+ma_status ma_get_counters(const ma_handle* h, int64_t* step, int64_t* head, int64_t* filled,
+                          int64_t* stamps) {
+    if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
+    if (step) *step = h->step;
+    if (head) *head = h->head;
+    if (filled) *filled = h->filled;
+    if (stamps) std::memcpy(stamps, h->stamps.data(), h->stamps.size() * sizeof(int64_t));
+    return MA_OK;
+}
+
+ma_status ma_read_error_buffer(ma_handle* h, uint8_t* codes, double* lo, double* hi) {
+    if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
+    DeviceGuard g(h->device);
+    MA_CUDA(cudaDeviceSynchronize());
+    if (codes) MA_CUDA(cudaMemcpy(codes, h->d_codes, size_t(h->shape.code_bytes), cudaMemcpyDeviceToHost));
+    if (lo || hi) {
+        std::vector<double2> meta(size_t(h->shape.nbuckets));
+        MA_CUDA(cudaMemcpy(meta.data(), h->d_meta, meta.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < meta.size(); ++i) {
+            if (lo) lo[i] = meta[i].x;
+            if (hi) hi[i] = meta[i].y;
+        }
+    }
+    return MA_OK;
+}
+
+namespace {
+double widen(const void* p, int dt, size_t i) {
+    if (dt == MA_F64) return static_cast<const double*>(p)[i];
+    if (dt == MA_F32) return double(static_cast<const float*>(p)[i]);
+    uint32_t u = uint32_t(static_cast<const uint16_t*>(p)[i]) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return double(f);
+}
+}  // namespace
+
+ma_status ma_read_window_row(ma_handle* h, int64_t slot, int64_t* indices, double* values) {
+    if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
+    if (slot < 0 || slot >= h->cfg.hp.window) return fail(MA_ERR_INVALID_ARG, "slot out of range");
+    DeviceGuard g(h->device);
+    MA_CUDA(cudaDeviceSynchronize());
+    const Shape& s = h->shape;
+    const int64_t nb = s.b1 - s.b0, m = h->cfg.hp.window, kbs = s.kb_stride;
+    const size_t vsz = dtype_size(h->cfg.value_dtype);
+    // Strided 2-D copy of just this slot: one row of kb_stride per block.
+    std::vector<int16_t> idx(size_t(nb * kbs));
+    std::vector<unsigned char> val(size_t(nb * kbs) * vsz);
+    MA_CUDA(cudaMemcpy2D(idx.data(), size_t(kbs) * 2, h->d_win_idx + slot * kbs, size_t(m * kbs) * 2,
+                         size_t(kbs) * 2, size_t(nb), cudaMemcpyDeviceToHost));
+    MA_CUDA(cudaMemcpy2D(val.data(), size_t(kbs) * vsz,
+                         static_cast<char*>(h->d_win_val) + size_t(slot * kbs) * vsz,
+                         size_t(m * kbs) * vsz, size_t(kbs) * vsz, size_t(nb), cudaMemcpyDeviceToHost));
+    int64_t n = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t start = b * s.block;
+        const int64_t len = std::min(s.block, s.dim - start);
+        const int64_t kb = std::min(s.per_block_k, len);
+        for (int64_t j = 0; j < kb; ++j, ++n) {
+            if (indices) indices[n] = s.elem0 + start + idx[size_t(b * kbs + j)];
+            if (values) values[n] = widen(val.data(), h->cfg.value_dtype, size_t(b * kbs + j));
+        }
+    }
+    return MA_OK;
+}
+
+ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, const double* hi,
+                         int64_t step, int64_t head, const int64_t* stamps,
+                         const int64_t* win_indices, const double* win_values) {
+    if (!h || !codes || !lo || !hi || !stamps || !win_indices || !win_values)
+        return fail(MA_ERR_INVALID_ARG, "null argument");
+    const Shape& s = h->shape;
+    const int64_t m = h->cfg.hp.window;
+    if (step < 0 || head < 0 || head >= m) return fail(MA_ERR_INVALID_ARG, "bad counters");
+    DeviceGuard g(h->device);
+    MA_CUDA(cudaDeviceSynchronize());
+    MA_CUDA(cudaMemcpy(h->d_codes, codes, size_t(s.code_bytes), cudaMemcpyHostToDevice));
+    std::vector<double2> meta(size_t(s.nbuckets));
+    for (size_t i = 0; i < meta.size(); ++i) meta[i] = make_double2(lo[i], hi[i]);
+    MA_CUDA(cudaMemcpy(h->d_meta, meta.data(), meta.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    const int64_t nb = s.b1 - s.b0, kbs = s.kb_stride;
+    const int vdt = h->cfg.value_dtype;
+    const size_t vsz = dtype_size(vdt);
+    std::vector<int16_t> idx(size_t(nb * m * kbs), 0);
+    std::vector<unsigned char> val(size_t(nb * m * kbs) * vsz, 0);
+    for (int64_t r = 0; r < m; ++r) {
+        int64_t n = r * s.row_width;
+        for (int64_t b = 0; b < nb; ++b) {
+            const int64_t start = b * s.block;
+            const int64_t len = std::min(s.block, s.dim - start);
+            const int64_t kb = std::min(s.per_block_k, len);
+            for (int64_t j = 0; j < kb; ++j, ++n) {
+                const int64_t rel = win_indices[n] - s.elem0 - start;
+                if (stamps[r] != 0 && (rel < 0 || rel >= len))
+                    return fail(MA_ERR_INVALID_ARG, "window index outside its block");
+                const size_t q = size_t((b * m + r) * kbs + j);
+                idx[q] = int16_t(rel < 0 ? 0 : rel);
+                const double v = win_values[n];
+                if (vdt == MA_F64) {
+                    std::memcpy(&val[q * 8], &v, 8);
+                } else if (vdt == MA_F32) {
+                    const float f = float(v);
+                    std::memcpy(&val[q * 4], &f, 4);
+                } else {
+                    const float f = float(v);  // caller passes bf16-representable values
+                    uint32_t u;
+                    std::memcpy(&u, &f, 4);
+                    const uint16_t hb = uint16_t(u >> 16);
+                    std::memcpy(&val[q * 2], &hb, 2);
+                }
+            }
+        }
+    }
+    MA_CUDA(cudaMemcpy(h->d_win_idx, idx.data(), idx.size() * 2, cudaMemcpyHostToDevice));
+    MA_CUDA(cudaMemcpy(h->d_win_val, val.data(), val.size(), cudaMemcpyHostToDevice));
+    h->step = step;
+    h->head = head;
+    h->filled = step < m ? step : m;
+    std::memcpy(h->stamps.data(), stamps, size_t(m) * sizeof(int64_t));
+    return MA_OK;
+}
+
+ma_status ma_get_layout(const ma_handle* h, ma_layout_info* out) {
+    if (!h || !out) return fail(MA_ERR_INVALID_ARG, "null argument");
+    fill_layout(h->shape, h->cfg, out);
+    return MA_OK;
+}
+
+int64_t ma_kernel_launches(const ma_handle* h) { return h ? h->launches : 0; }
+
+const char* ma_last_error(void) { return g_last_error.c_str(); }
+
+const char* ma_version(void) { return "microadam_cuda 0.1 (sm_100a, ABI 1)"; }
+
+ma_status ma_fill_synthetic(void* d_out, int32_t dtype, int64_t n, uint64_t seed, uint64_t step,
+                            int64_t offset, int32_t levels, void* stream) {
+    if (!d_out || dtype < MA_F64 || dtype > MA_BF16) return fail(MA_ERR_INVALID_ARG, "bad argument");
+    MA_CUDA(ma::launch_fill_synthetic(d_out, dtype, n, seed, step, offset, levels,
+                                      static_cast<cudaStream_t>(stream)));
+    return MA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// ma_internal.h — shared between the C-ABI host code (ma_capi.cu) and the
+// sm_100a kernels (ma_kernels.cu). Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ma {
+
+constexpr int kMaxWindow = 256;  // m supported on device (params carry m weights)
+constexpr int kMaxBlock = 8192;  // B_d supported on device (fp64 block held on chip)
+constexpr int kCandCap = 128;    // exact-rank stage capacity of the Top-K select
+constexpr int kReportFields = 5; // Σg², Σa², Σr², Σe_new², nnz per block
+
+enum Dtype : int32_t { F64 = 0, F32 = 1, BF16 = 2 };
+
+// One step over blocks [block_offset, block_offset + gridDim-covered) of the
+// handle's shard. All pointers are shard-local (element 0 = first element of
+// the shard); block b covers elements [b*block, min((b+1)*block, dim)).
+struct StepArgs {
+    const void* grads;
+    void* params;
+    uint8_t* codes;   // packed 4-bit EF codes, low nibble first (quantize.cpp:102-114)
+    double2* meta;    // per-bucket (lo, hi) fp64
+    int16_t* win_idx; // [num_blocks][m][kb_stride] block-relative indices
+    void* win_val;    // [num_blocks][m][kb_stride] values (value dtype)
+    unsigned int* flag;
+    double* partials; // nullable: [num_blocks][kReportFields]
+    int64_t dim;
+    int64_t num_blocks;
+    int64_t block_offset;
+    int32_t block, per_block_k, kb_stride, bucket;
+    int32_t m, filled, slot, check_finite;
+    int32_t g_dtype, p_dtype, v_dtype, pad0;
+    double eps, lr, scale1, scale2;
+    double w1[kMaxWindow];
+    double w2[kMaxWindow];
+};
+
+struct Variant {
+    int nt;   // threads per CTA
+    int ept;  // elements per thread (even)
+};
+
+// Dynamic shared memory bytes needed by the step kernel for this shape.
+size_t step_smem_bytes(int nt, int ept, int block, int bucket, int m, int kb_stride);
+// Smallest variant that holds `block` elements on chip; nt == 0 if none.
+Variant pick_variant(int block);
+
+cudaError_t launch_step(const StepArgs& a, Variant v, int64_t nblocks, cudaStream_t s);
+cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int* flag,
+                               cudaStream_t s);
+cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double* out5,
+                                 cudaStream_t s);
+cudaError_t launch_fill_synthetic(void* out, int dtype, int64_t n, uint64_t seed, uint64_t step,
+                                  int64_t offset, int levels, cudaStream_t s);
+
+}  // namespace ma

@@ -1,0 +1,695 @@
+// ma_kernels.cu — sm_100a kernels of the MicroAdam optimizer step.
+//
+// One fused kernel runs the whole reference step (optim.cpp:164-190) for one
+// Top-K block per CTA, reading every input once from HBM and writing every
+// output once:
+//
+//   P1  EF decode + accumulate   a = g + (code·level + lo)       quantize.cpp:164-178, optim.cpp:166-168
+//   P2  block Top-K select        (|a| desc, idx asc), radix      compress.cpp:39-53, 73-85
+//   P3  window write + residual   slot `head` ← (rel idx, V(a))   window.cpp:14-26, compress.cpp:95-102
+//   P4  4-bit re-quantization     per-bucket min/max, nearest     quantize.cpp:7-24, 42-55, 142-162
+//   P5  nibble pack               low nibble first                quantize.cpp:102-114
+//   P6  ADAM_STATS + update       window rows in slot order       window.cpp:28-46, optim.cpp:183-187
+//
+// Arithmetic on the EF/Top-K/stats path is fp64 with explicit round-to-nearest
+// intrinsics (__dmul_rn/__dadd_rn/__ddiv_rn/__dsqrt_rn) and the library is
+// built with -fmad=false: the reference build has no FMA and a
+// contracted decode changes ~37% of accumulator bits.
+#include <cuda_bf16.h>
+
+#include "../../include/ma_synth.h"
+#include "ma_internal.h"
+
+namespace ma {
+namespace {
+
+constexpr uint64_t kAbsMask = 0x7FFFFFFFFFFFFFFFull;
+
+__device__ __forceinline__ uint64_t key_of(double x) {
+    return static_cast<uint64_t>(__double_as_longlong(x)) & kAbsMask;
+}
+
+// Round-to-nearest-even of a double to bfloat16, returned as the (exactly
+// representable) double. Same rule as oracle/microadam_oracle.c:mo_bf16_round.
+__device__ __forceinline__ double bf16_round(double x) {
+    if (!isfinite(x) || x == 0.0) return x;
+    if (fabs(x) < 0x1p-126) return __dmul_rn(rint(__dmul_rn(x, 0x1p133)), 0x1p-133);
+    uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
+    const uint64_t lsb = (u >> 45) & 1u;
+    u += ((uint64_t(1) << 44) - 1u) + lsb;
+    u &= ~((uint64_t(1) << 45) - 1u);
+    const double y = __longlong_as_double(static_cast<long long>(u));
+    if (fabs(y) >= 0x1p128) return copysign(__longlong_as_double(0x7FF0000000000000ll), x);
+    return y;
+}
+
+__device__ __forceinline__ double round_to(double x, int dt) {
+    if (dt == F64) return x;
+    if (dt == F32) return static_cast<double>(__double2float_rn(x));
+    return bf16_round(x);
+}
+
+__device__ __forceinline__ double ld_val(const void* p, int dt, int64_t i) {
+    if (dt == F64) return static_cast<const double*>(p)[i];
+    if (dt == F32) return static_cast<double>(static_cast<const float*>(p)[i]);
+    const uint32_t u = static_cast<const uint16_t*>(p)[i];
+    return static_cast<double>(__uint_as_float(u << 16));
+}
+
+// Two consecutive elements starting at an even index (aligned vector load).
+__device__ __forceinline__ void ld_pair(const void* p, int dt, int64_t i, double& x0, double& x1) {
+    if (dt == F64) {
+        const double2 v = static_cast<const double2*>(p)[i >> 1];
+        x0 = v.x;
+        x1 = v.y;
+    } else if (dt == F32) {
+        const float2 v = static_cast<const float2*>(p)[i >> 1];
+        x0 = v.x;
+        x1 = v.y;
+    } else {
+        const uint32_t v = static_cast<const uint32_t*>(p)[i >> 1];
+        x0 = static_cast<double>(__uint_as_float(v << 16));
+        x1 = static_cast<double>(__uint_as_float(v & 0xFFFF0000u));
+    }
+}
+
+__device__ __forceinline__ void st_val(void* p, int dt, int64_t i, double x) {
+    if (dt == F64) {
+        static_cast<double*>(p)[i] = x;
+    } else if (dt == F32) {
+        static_cast<float*>(p)[i] = __double2float_rn(x);
+    } else {
+        const float f = static_cast<float>(bf16_round(x));  // exact
+        static_cast<uint16_t*>(p)[i] = static_cast<uint16_t>(__float_as_uint(f) >> 16);
+    }
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory carve-up (identical on host and device).
+// ---------------------------------------------------------------------------
+struct SmemLayout {
+    size_t lo, lvl, a, z1, z2, eval, ckey, red, owner, hist, cidx, scan, misc, eidx, code, selm;
+    size_t total;
+
+    __host__ __device__ static size_t take(size_t& off, size_t bytes) {
+        off = (off + 15) & ~size_t(15);
+        const size_t r = off;
+        off += bytes;
+        return r;
+    }
+    __host__ __device__ SmemLayout(int nt, int ept, int block, int bucket, int m, int kbs) {
+        const size_t nbk = size_t((block + bucket - 1) / bucket);
+        const size_t ent = size_t(m) * size_t(kbs);
+        size_t off = 0;
+        lo = take(off, nbk * 8);
+        lvl = take(off, nbk * 8);
+        a = take(off, size_t(block) * 8);
+        z1 = take(off, ent * 8);
+        z2 = take(off, ent * 8);
+        eval = take(off, ent * 8);
+        ckey = take(off, size_t(kCandCap) * 8);
+        red = take(off, size_t(nt / 32) * kReportFields * 8);
+        owner = take(off, size_t(block) * 4);
+        hist = take(off, 256 * 4);
+        cidx = take(off, size_t(kCandCap) * 4);
+        scan = take(off, (size_t(ept / 2) * size_t(nt / 32) + 1) * 4);
+        misc = take(off, 32 * 4);
+        eidx = take(off, ent * 2);
+        code = take(off, size_t(block));
+        selm = take(off, size_t(block));
+        total = (off + 15) & ~size_t(15);
+    }
+};
+
+// Warp 0: locate the bin holding the need-th largest element of a 256-bin
+// histogram. out = {bin, count above bin, count in bin}; bin = -1 if the
+// histogram holds fewer than `need` elements.
+__device__ __forceinline__ void find_bin(const uint32_t* hist, uint32_t need, int* out) {
+    const int lane = threadIdx.x & 31;
+    uint32_t h[8];
+    uint32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        h[q] = hist[lane * 8 + q];
+        s += h[q];
+    }
+    uint32_t incl = s;  // Σ over lanes >= lane
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_down_sync(0xFFFFFFFFu, incl, off);
+        if (lane + off < 32) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 0);
+    if (total < need) {
+        if (lane == 0) {
+            out[0] = -1;
+            out[1] = 0;
+            out[2] = static_cast<int>(total);
+        }
+        return;
+    }
+    uint32_t cum = incl - s;
+#pragma unroll
+    for (int q = 7; q >= 0; --q) {
+        if (cum < need && cum + h[q] >= need) {
+            out[0] = lane * 8 + q;
+            out[1] = static_cast<int>(cum);
+            out[2] = static_cast<int>(h[q]);
+        }
+        cum += h[q];
+    }
+}
+
+// Exclusive rank, in element order, of the flagged elements of the block.
+// Thread `tid` holds elements e = 2*(j*NT + tid) + p at register slot 2j+p, so
+// element order is (j, warp, lane, p). Returns the flagged total.
+template <int NT, int EPT>
+__device__ __forceinline__ int block_rank(uint32_t flags, int (&rank)[EPT], int* scan) {
+    constexpr int NW = NT / 32;
+    constexpr int NP = EPT / 2;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = lanemask_lt();
+    __syncthreads();  // previous users of scan[] are done
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        const uint32_t f0 = (flags >> (2 * j)) & 1u, f1 = (flags >> (2 * j + 1)) & 1u;
+        const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, f0), b1 = __ballot_sync(0xFFFFFFFFu, f1);
+        const int pre = __popc(b0 & lt) + __popc(b1 & lt);
+        rank[2 * j] = pre;
+        rank[2 * j + 1] = pre + static_cast<int>(f0);
+        if (lane == 0) scan[j * NW + warp] = __popc(b0) + __popc(b1);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        constexpr int n = NP * NW;
+        int carry = 0;
+        for (int base = 0; base < n; base += 32) {
+            const int i = base + lane;
+            const int v = i < n ? scan[i] : 0;
+            int incl = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+                if (lane >= off) incl += t;
+            }
+            if (i < n) scan[i] = carry + incl - v;
+            carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+        if (lane == 0) scan[n] = carry;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        const int off = scan[j * NW + warp];
+        rank[2 * j] += off;
+        rank[2 * j + 1] += off;
+    }
+    return scan[NP * NW];
+}
+
+template <int NT>
+__device__ __forceinline__ void block_zero_hist(uint32_t* hist) {
+    for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
+}
+
+// Block Top-K (compress.cpp:39-53 semantics): select exactly `kb` of the
+// valid elements, the first under (|a| desc, index asc). Returns the
+// selection bitmask over the thread's register slots.
+//
+// Keys are the fp64 bit patterns with the sign cleared (monotone in |a|,
+// -0.0 == +0.0). Pass 1 is a 256-bin histogram of key>>45 (1/128 binade per
+// bin) over the top 256 bins below the block maximum, which usually leaves a
+// handful of candidates; a general 8-bit-digit radix select from bit 62
+// covers the rest. Once the candidates fit kCandCap they are ranked exactly
+// by (key desc, index asc); if all 63 bits tie, the lowest indices win.
+template <int NT, int EPT>
+__device__ uint32_t block_topk(const double (&a)[EPT], uint32_t valid, int kb, uint32_t* hist,
+                               int* misc, uint64_t* ckey, int* cidx, uint8_t* selm, int* scan) {
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto elem = [&](int i) { return 2 * ((i >> 1) * NT + tid) + (i & 1); };
+
+    uint32_t sel = 0;
+    uint32_t tmax = 0;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i)
+        if ((valid >> i) & 1u) tmax = max(tmax, static_cast<uint32_t>(key_of(a[i]) >> 45));
+    tmax = __reduce_max_sync(0xFFFFFFFFu, tmax);
+    if (lane == 0) misc[warp] = static_cast<int>(tmax);
+    block_zero_hist<NT>(hist);
+    __syncthreads();
+    uint32_t top = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) top = max(top, static_cast<uint32_t>(misc[w]));
+    const uint32_t tbase = top >= 255u ? top - 255u : 0u;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+        if ((valid >> i) & 1u) {
+            const uint32_t t = static_cast<uint32_t>(key_of(a[i]) >> 45);
+            if (t >= tbase) atomicAdd(&hist[t - tbase], 1u);
+        }
+    }
+    __syncthreads();
+    if (warp == 0) find_bin(hist, static_cast<uint32_t>(kb), misc + 16);
+    __syncthreads();
+
+    int need = kb;
+    int fs;
+    uint64_t prefix;
+    int cnt;
+    if (misc[16] >= 0) {
+        prefix = tbase + static_cast<uint32_t>(misc[16]);
+        need -= misc[17];
+        cnt = misc[18];
+        fs = 45;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if (((valid >> i) & 1u) && (key_of(a[i]) >> 45) > prefix) sel |= 1u << i;
+    } else {
+        fs = 63;
+        prefix = 0;
+        cnt = 0x7FFFFFFF;  // unknown; forces a radix pass
+    }
+
+    for (;;) {
+        // Candidates: valid, unselected, key >> fs == prefix.
+        uint32_t cand = 0;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if (((valid >> i) & 1u) && !((sel >> i) & 1u) && (key_of(a[i]) >> fs) == prefix)
+                cand |= 1u << i;
+        if (cnt == need) {
+            sel |= cand;
+            break;
+        }
+        if (cnt <= kCandCap) {
+            __syncthreads();  // misc[20] / ckey reuse
+            if (tid == 0) misc[20] = 0;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                if ((cand >> i) & 1u) {
+                    const int s = atomicAdd(&misc[20], 1);
+                    ckey[s] = key_of(a[i]);
+                    cidx[s] = elem(i);
+                }
+            }
+            __syncthreads();
+            const int n = misc[20];
+            for (int c = tid; c < n; c += NT) {
+                const uint64_t kc = ckey[c];
+                const int ic = cidx[c];
+                int r = 0;
+                for (int q = 0; q < n; ++q) {
+                    const uint64_t kq = ckey[q];
+                    r += (kq > kc) || (kq == kc && cidx[q] < ic);
+                }
+                if (r < need) selm[ic] = 1;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < EPT; ++i)
+                if (((cand >> i) & 1u) && selm[elem(i)]) sel |= 1u << i;
+            break;
+        }
+        if (fs == 0) {
+            // Exact 63-bit ties beyond the cap: lowest indices win.
+            int rank[EPT];
+            block_rank<NT, EPT>(cand, rank, scan);
+#pragma unroll
+            for (int i = 0; i < EPT; ++i)
+                if (((cand >> i) & 1u) && rank[i] < need) sel |= 1u << i;
+            break;
+        }
+        const int ns = fs > 8 ? fs - 8 : 0;
+        const int width = fs - ns;
+        const uint32_t mask = (1u << width) - 1u;
+        __syncthreads();  // hist / misc reuse
+        block_zero_hist<NT>(hist);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if ((cand >> i) & 1u)
+                atomicAdd(&hist[static_cast<uint32_t>(key_of(a[i]) >> ns) & mask], 1u);
+        __syncthreads();
+        if (warp == 0) find_bin(hist, static_cast<uint32_t>(need), misc + 16);
+        __syncthreads();
+        const uint32_t bin = static_cast<uint32_t>(misc[16]);
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if (((cand >> i) & 1u) && (static_cast<uint32_t>(key_of(a[i]) >> ns) & mask) > bin)
+                sel |= 1u << i;
+        need -= misc[17];
+        cnt = misc[18];
+        prefix = (prefix << width) | bin;
+        fs = ns;
+    }
+    return sel;
+}
+
+template <int NT>
+__device__ __forceinline__ void block_sum5(double (&v)[kReportFields], double* red, double* out) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int f = 0; f < kReportFields; ++f) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[f] += __shfl_xor_sync(0xFFFFFFFFu, v[f], off);
+        if (lane == 0) red[warp * kReportFields + f] = v[f];
+    }
+    __syncthreads();
+    if (threadIdx.x < kReportFields) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += red[w * kReportFields + threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The fused step kernel: one CTA per Top-K block.
+// ---------------------------------------------------------------------------
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constant__ StepArgs p) {
+    constexpr int NP = EPT / 2;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const SmemLayout L(NT, EPT, p.block, p.bucket, p.m, p.kb_stride);
+    double* s_lo = reinterpret_cast<double*>(smem + L.lo);
+    double* s_lvl = reinterpret_cast<double*>(smem + L.lvl);
+    double* s_a = reinterpret_cast<double*>(smem + L.a);
+    double* s_z1 = reinterpret_cast<double*>(smem + L.z1);
+    double* s_z2 = reinterpret_cast<double*>(smem + L.z2);
+    double* s_eval = reinterpret_cast<double*>(smem + L.eval);
+    uint64_t* s_ckey = reinterpret_cast<uint64_t*>(smem + L.ckey);
+    double* s_red = reinterpret_cast<double*>(smem + L.red);
+    int* s_owner = reinterpret_cast<int*>(smem + L.owner);
+    uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + L.hist);
+    int* s_cidx = reinterpret_cast<int*>(smem + L.cidx);
+    int* s_scan = reinterpret_cast<int*>(smem + L.scan);
+    int* s_misc = reinterpret_cast<int*>(smem + L.misc);
+    int16_t* s_eidx = reinterpret_cast<int16_t*>(smem + L.eidx);
+    uint8_t* s_code = reinterpret_cast<uint8_t*>(smem + L.code);
+    uint8_t* s_selm = reinterpret_cast<uint8_t*>(smem + L.selm);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = NT / 32;
+    const int block = p.block, bucket = p.bucket, kbs = p.kb_stride;
+    const int64_t b = p.block_offset + blockIdx.x;
+    const int64_t base = b * static_cast<int64_t>(block);
+    const int len = static_cast<int>(min(static_cast<int64_t>(block), p.dim - base));
+    const int kb = min(p.per_block_k, len);
+    const int nbk = (len + bucket - 1) / bucket;
+    const int64_t bk0 = base / bucket;
+    const bool want_report = p.partials != nullptr;
+    auto elem = [&](int i) { return 2 * ((i >> 1) * NT + tid) + (i & 1); };
+
+    // ---- P0: old bucket grids (QuantParams ctor, quantize.cpp:7-13) ----
+    for (int i = tid; i < nbk; i += NT) {
+        const double2 mt = p.meta[bk0 + i];
+        s_lo[i] = mt.x;
+        s_lvl[i] = (mt.x == mt.y) ? 0.0 : __ddiv_rn(__dsub_rn(mt.y, mt.x), 15.0);
+    }
+    for (int i = tid; i < len; i += NT) s_selm[i] = 0;
+    __syncthreads();
+
+    // ---- P1: decode + accumulate (quantize.cpp:164-178, optim.cpp:166-168) ----
+    double a[EPT];
+    uint32_t valid = 0;
+    bool bad = false;
+    double rep[kReportFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        const int e = 2 * (j * NT + tid);
+        a[2 * j] = 0.0;
+        a[2 * j + 1] = 0.0;
+        if (e < len) {
+            double g0, g1 = 0.0;
+            const bool two = e + 1 < len;
+            if (two)
+                ld_pair(p.grads, p.g_dtype, base + e, g0, g1);
+            else
+                g0 = ld_val(p.grads, p.g_dtype, base + e);
+            const uint32_t byte = p.codes[(base + e) >> 1];
+            const int bA = e / bucket;
+            const double e0 =
+                __dadd_rn(__dmul_rn(static_cast<double>(byte & 15u), s_lvl[bA]), s_lo[bA]);
+            a[2 * j] = __dadd_rn(g0, e0);
+            valid |= 1u << (2 * j);
+            bad |= !isfinite(g0) || !isfinite(a[2 * j]);
+            if (want_report) {
+                rep[0] += g0 * g0;
+                rep[1] += a[2 * j] * a[2 * j];
+            }
+            if (two) {
+                const int bB = (e + 1) / bucket;
+                const double e1 =
+                    __dadd_rn(__dmul_rn(static_cast<double>(byte >> 4), s_lvl[bB]), s_lo[bB]);
+                a[2 * j + 1] = __dadd_rn(g1, e1);
+                valid |= 1u << (2 * j + 1);
+                bad |= !isfinite(g1) || !isfinite(a[2 * j + 1]);
+                if (want_report) {
+                    rep[0] += g1 * g1;
+                    rep[1] += a[2 * j + 1] * a[2 * j + 1];
+                }
+            }
+        }
+    }
+    if (p.check_finite && bad) atomicOr(p.flag, 1u);
+
+    // ---- P2: block Top-K (compress.cpp:73-85) ----
+    uint32_t sel = valid;
+    if (kb < len)
+        sel = block_topk<NT, EPT>(a, valid, kb, s_hist, s_misc, s_ckey, s_cidx, s_selm, s_scan);
+
+    // ---- P3: window row `slot` (window.cpp:14-26) + residual (compress.cpp:95-102) ----
+    int rank[EPT];
+    block_rank<NT, EPT>(sel, rank, s_scan);
+    const int slot = p.slot;
+    const int64_t wrow = (b * p.m + slot) * static_cast<int64_t>(kbs);
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+        if (!((valid >> i) & 1u)) continue;
+        const int e = elem(i);
+        if ((sel >> i) & 1u) {
+            const int pos = rank[i];
+            p.win_idx[wrow + pos] = static_cast<int16_t>(e);
+            st_val(p.win_val, p.v_dtype, wrow + pos, a[i]);
+            s_eidx[slot * kbs + pos] = static_cast<int16_t>(e);
+            s_eval[slot * kbs + pos] = round_to(a[i], p.v_dtype);
+            s_a[e] = 0.0;
+        } else {
+            s_a[e] = a[i];
+            if (want_report) rep[2] += a[i] * a[i];
+        }
+    }
+    // Older rows of this block's window (any order; consumed in slot order in P6).
+    const int filled = p.filled;
+    for (int t = tid; t < filled * kb; t += NT) {
+        const int r = t / kb;
+        if (r == slot) continue;
+        const int j = t - r * kb;
+        const int64_t g = (b * p.m + r) * static_cast<int64_t>(kbs) + j;
+        s_eidx[r * kbs + j] = p.win_idx[g];
+        s_eval[r * kbs + j] = ld_val(p.win_val, p.v_dtype, g);
+    }
+    __syncthreads();
+
+    // ---- P4: re-quantize the residual (quantize.cpp:15-24, 42-55, 142-162) ----
+    for (int bk = warp; bk < nbk; bk += NW) {
+        const int s = bk * bucket;
+        const int n = min(bucket, len - s);
+        double lo = s_a[s], hi = s_a[s];
+        for (int i = lane; i < n; i += 32) {
+            const double x = s_a[s + i];
+            lo = fmin(lo, x);
+            hi = fmax(hi, x);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, off));
+            hi = fmax(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, off));
+        }
+        const double level = (lo == hi) ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+        if (lane == 0) p.meta[bk0 + bk] = make_double2(lo, hi);
+        // Guarded reciprocal: floor((x-lo)*(1/level)+0.5) equals the exact
+        // quotient's unless t lands within 7e-15 of an integer; such t take
+        // the IEEE division.
+        const bool fast = level >= 0x1p-1000;
+        const double rinv = fast ? __drcp_rn(level) : 0.0;
+        for (int i = lane; i < n; i += 32) {
+            const double x = s_a[s + i];
+            uint32_t c = 0;
+            if (level != 0.0) {
+                const double d = __dsub_rn(x, lo);
+                double t = __dadd_rn(__dmul_rn(d, rinv), 0.5);
+                double f = floor(t);
+                const double fr = __dsub_rn(t, f);
+                if (!fast || fr < 1e-12 || fr > 1.0 - 1e-12) f = floor(__dadd_rn(__ddiv_rn(d, level), 0.5));
+                f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+                c = static_cast<uint32_t>(f);
+            }
+            s_code[s + i] = static_cast<uint8_t>(c);
+            if (want_report) {
+                const double en = __dadd_rn(__dmul_rn(static_cast<double>(c), level), lo);
+                rep[3] += en * en;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- P5: nibble pack (quantize.cpp:102-114) ----
+    for (int i = tid; i < (len + 1) / 2; i += NT) {
+        const uint32_t lo4 = s_code[2 * i];
+        const uint32_t hi4 = (2 * i + 1 < len) ? s_code[2 * i + 1] : 0u;
+        p.codes[(base >> 1) + i] = static_cast<uint8_t>(lo4 | (hi4 << 4));
+    }
+
+    // ---- P6: ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) ----
+    // Each coordinate gets one owner entry; the owner accumulates every row's
+    // contribution in physical slot order (rows hold unique indices, so a row
+    // pass is race-free), matching the reference's summation order exactly.
+    const int nent = filled * kb;
+    for (int t = tid; t < nent; t += NT) {
+        const int r = t / kb;
+        const int e = r * kbs + (t - r * kb);
+        s_owner[s_eidx[e]] = e;
+    }
+    __syncthreads();
+    for (int t = tid; t < nent; t += NT) {
+        const int r = t / kb;
+        const int e = r * kbs + (t - r * kb);
+        if (s_owner[s_eidx[e]] == e) {
+            s_z1[e] = 0.0;
+            s_z2[e] = 0.0;
+        }
+    }
+    __syncthreads();
+    for (int r = 0; r < filled; ++r) {
+        const double w1 = p.w1[r], w2 = p.w2[r];
+        for (int j = tid; j < kb; j += NT) {
+            const int e = r * kbs + j;
+            const int o = s_owner[s_eidx[e]];
+            const double v = s_eval[e];
+            s_z1[o] = __dadd_rn(s_z1[o], __dmul_rn(w1, v));
+            s_z2[o] = __dadd_rn(s_z2[o], __dmul_rn(w2, __dmul_rn(v, v)));
+        }
+        __syncthreads();
+    }
+    for (int t = tid; t < nent; t += NT) {
+        const int r = t / kb;
+        const int e = r * kbs + (t - r * kb);
+        const int idx = s_eidx[e];
+        if (s_owner[idx] != e) continue;
+        const double mhat = __dmul_rn(s_z1[e], p.scale1);
+        const double vhat = __dmul_rn(s_z2[e], p.scale2);
+        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+        const double th = ld_val(p.params, p.p_dtype, base + idx);
+        st_val(p.params, p.p_dtype, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
+        if (want_report && u != 0.0) rep[4] += 1.0;
+    }
+    if (want_report) block_sum5<NT>(rep, s_red, p.partials + b * kReportFields);
+}
+
+__global__ void finite_scan_kernel(const void* g, int dt, int64_t n, unsigned int* flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        bad |= !isfinite(ld_val(g, dt, i));
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+__global__ void report_reduce_kernel(const double* partials, int64_t nblocks, double* out) {
+    __shared__ double red[1024 / 32][kReportFields];
+    double v[kReportFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t b = threadIdx.x; b < nblocks; b += blockDim.x)
+        for (int f = 0; f < kReportFields; ++f) v[f] += partials[b * kReportFields + f];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int f = 0; f < kReportFields; ++f) {
+        for (int off = 16; off > 0; off >>= 1) v[f] += __shfl_xor_sync(0xFFFFFFFFu, v[f], off);
+        if (lane == 0) red[warp][f] = v[f];
+    }
+    __syncthreads();
+    if (threadIdx.x < kReportFields) {
+        double s = 0.0;
+        for (int w = 0; w < int(blockDim.x / 32); ++w) s += red[w][threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+}
+
+__global__ void fill_synthetic_kernel(void* out, int dt, int64_t n, uint64_t seed, uint64_t step,
+                                      int64_t offset, int levels) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t gi = static_cast<uint64_t>(offset + i);
+        const double v = levels ? ma_synth_levels(seed, step, gi) : ma_synth_normal(seed, step, gi);
+        st_val(out, dt, i, v);
+    }
+}
+
+template <int NT, int EPT>
+cudaError_t launch_variant(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
+    const size_t smem = SmemLayout(NT, EPT, a.block, a.bucket, a.m, a.kb_stride).total;
+    auto k = microadam_step_kernel<NT, EPT>;
+    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+    if (err != cudaSuccess) return err;
+    k<<<static_cast<unsigned>(nblocks), NT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t step_smem_bytes(int nt, int ept, int block, int bucket, int m, int kb_stride) {
+    return SmemLayout(nt, ept, block, bucket, m, kb_stride).total;
+}
+
+Variant pick_variant(int block) {
+    if (block <= 128) return {64, 2};
+    if (block <= 1024) return {128, 8};
+    if (block <= 4096) return {256, 16};
+    if (block <= 8192) return {512, 16};
+    return {0, 0};
+}
+
+cudaError_t launch_step(const StepArgs& a, Variant v, int64_t nblocks, cudaStream_t s) {
+    if (nblocks <= 0) return cudaSuccess;
+    if (nblocks > 0x7FFFFFFFll) return cudaErrorInvalidConfiguration;
+    switch (v.nt) {
+        case 64: return launch_variant<64, 2>(a, nblocks, s);
+        case 128: return launch_variant<128, 8>(a, nblocks, s);
+        case 256: return launch_variant<256, 16>(a, nblocks, s);
+        case 512: return launch_variant<512, 16>(a, nblocks, s);
+        default: return cudaErrorInvalidConfiguration;
+    }
+}
+
+cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int* flag,
+                               cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t want = (n + 255) / 256;
+    const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
+    finite_scan_kernel<<<grid, 256, 0, s>>>(g, dtype, n, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double* out5,
+                                 cudaStream_t s) {
+    report_reduce_kernel<<<1, 1024, 0, s>>>(partials, nblocks, out5);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_synthetic(void* out, int dtype, int64_t n, uint64_t seed, uint64_t step,
+                                  int64_t offset, int levels, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t want = (n + 255) / 256;
+    const unsigned grid = static_cast<unsigned>(want < 148 * 32 ? want : 148 * 32);
+    fill_synthetic_kernel<<<grid, 256, 0, s>>>(out, dtype, n, seed, step, offset, levels);
+    return cudaGetLastError();
+}
+
+}  // namespace ma
