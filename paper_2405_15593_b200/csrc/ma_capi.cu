@@ -4,8 +4,10 @@
 // GradientWindow (step/head/filled/stamps, window.hpp:10-33), the glibc
 // pow() weights (window.cpp:37,43 — computed here, on the host, exactly as the
 // reference does) and kernel launches. No exception crosses the ABI.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -153,6 +155,7 @@ struct ma_handle {
     ma_config cfg{};
     Shape shape;
     ma::Variant variant{};
+    bool fast = false;  // ma_fast.cu kernel (else the generic ma_kernels.cu kernel)
     int device = 0;
     uint8_t* d_codes = nullptr;
     double2* d_meta = nullptr;
@@ -161,6 +164,7 @@ struct ma_handle {
     unsigned int* d_flag = nullptr;
     double* d_partials = nullptr;
     double* d_report = nullptr;
+    uint32_t* d_thresh = nullptr;
     // host counters (window.hpp:10-33)
     int64_t step = 0, head = 0, filled = 0;
     std::vector<int64_t> stamps;
@@ -198,6 +202,7 @@ void free_handle(ma_handle* h) {
     cudaFree(h->d_flag);
     cudaFree(h->d_partials);
     cudaFree(h->d_report);
+    cudaFree(h->d_thresh);
     cudaFree(h->d_theta);
     cudaFree(h->d_gstage);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
@@ -234,6 +239,7 @@ void base_args(ma_handle* h, ma::StepArgs* a) {
     a->win_idx = h->d_win_idx;
     a->win_val = h->d_win_val;
     a->flag = h->d_flag;
+    a->thresh = h->d_thresh;
     a->dim = s.dim;
     a->num_blocks = s.b1 - s.b0;
     a->block = static_cast<int32_t>(s.block);
@@ -246,6 +252,11 @@ void base_args(ma_handle* h, ma::StepArgs* a) {
     a->p_dtype = h->cfg.param_dtype;
     a->v_dtype = h->cfg.value_dtype;
     a->eps = h->cfg.hp.eps;
+}
+
+cudaError_t launch(ma_handle* h, const ma::StepArgs& a, int64_t nblocks, cudaStream_t st) {
+    return h->fast ? ma::launch_step_fast(a, h->variant, nblocks, st)
+                   : ma::launch_step(a, h->variant, nblocks, st);
 }
 
 ma_status finish_report(ma_handle* h, cudaStream_t st, ma_step_report* report) {
@@ -289,7 +300,7 @@ ma_status run_step(ma_handle* h, void* d_params, const void* d_grads, double lr,
     a.lr = lr;
     a.partials = report ? h->d_partials : nullptr;
     push_and_weights(h, &a);
-    MA_CUDA(ma::launch_step(a, h->variant, h->shape.b1 - h->shape.b0, st));
+    MA_CUDA(launch(h, a, h->shape.b1 - h->shape.b0, st));
     ++h->launches;
     h->last_stream = st;
     if (report) return finish_report(h, st, report);
@@ -354,14 +365,27 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     h->cfg = *cfg;
     h->shape = s;
     h->device = device;
-    h->variant = ma::pick_variant(static_cast<int>(s.block));
     h->stamps.assign(size_t(cfg->hp.window), 0);
     const int64_t nb = s.b1 - s.b0;
     const size_t went = size_t(nb) * size_t(cfg->hp.window) * size_t(s.kb_stride);
-    const size_t smem = ma::step_smem_bytes(h->variant.nt, h->variant.ept, int(s.block),
-                                            int(s.bucket), int(cfg->hp.window), int(s.kb_stride));
     int smem_max = 0;
     cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    const char* force_generic = std::getenv("MA_FORCE_GENERIC");
+    const ma::Variant fv = ma::pick_fast_variant(int(s.block), int(s.bucket), int(cfg->hp.window),
+                                                 int(s.kb_stride));
+    if (fv.nt && !(force_generic && force_generic[0] == '1') &&
+        ma::fast_smem_bytes(fv, int(s.block), int(cfg->hp.window), int(s.kb_stride),
+                            cfg->param_dtype) <= size_t(smem_max)) {
+        h->variant = fv;
+        h->fast = true;
+    } else {
+        h->variant = ma::pick_variant(static_cast<int>(s.block));
+    }
+    const size_t smem = h->fast ? ma::fast_smem_bytes(h->variant, int(s.block), int(cfg->hp.window),
+                                                      int(s.kb_stride), cfg->param_dtype)
+                                : ma::step_smem_bytes(h->variant.nt, h->variant.ept, int(s.block),
+                                                      int(s.bucket), int(cfg->hp.window),
+                                                      int(s.kb_stride));
     if (smem > size_t(smem_max)) {
         delete h;
         return fail(MA_ERR_UNSUPPORTED, "block/window shape needs more shared memory than one SM has");
@@ -378,6 +402,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     alloc(reinterpret_cast<void**>(&h->d_flag), sizeof(unsigned));
     alloc(reinterpret_cast<void**>(&h->d_partials), size_t(nb) * ma::kReportFields * sizeof(double));
     alloc(reinterpret_cast<void**>(&h->d_report), ma::kReportFields * sizeof(double));
+    alloc(reinterpret_cast<void**>(&h->d_thresh), size_t(nb) * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         free_handle(h);
@@ -463,7 +488,7 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
         MA_CUDA(cudaEventRecord(up[size_t(c)], s_h2d));
         MA_CUDA(cudaStreamWaitEvent(st, up[size_t(c)], 0));
         a.block_offset = cb0;
-        MA_CUDA(ma::launch_step(a, h->variant, cb1 - cb0, st));
+        MA_CUDA(launch(h, a, cb1 - cb0, st));
         ++h->launches;
         MA_CUDA(cudaEventRecord(done[size_t(c)], st));
         MA_CUDA(cudaStreamWaitEvent(s_d2h, done[size_t(c)], 0));
@@ -608,6 +633,7 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
         }
     }
     MA_CUDA(cudaMemcpy(h->d_win_idx, idx.data(), idx.size() * 2, cudaMemcpyHostToDevice));
+    MA_CUDA(cudaMemset(h->d_thresh, 0, size_t(nb) * sizeof(uint32_t)));
     MA_CUDA(cudaMemcpy(h->d_win_val, val.data(), val.size(), cudaMemcpyHostToDevice));
     h->step = step;
     h->head = head;

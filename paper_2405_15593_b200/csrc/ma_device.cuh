@@ -1,0 +1,264 @@
+// ma_device.cuh — device helpers shared by the step kernels (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "ma_internal.h"
+
+namespace ma {
+namespace dev {
+
+constexpr uint64_t kAbsMask = 0x7FFFFFFFFFFFFFFFull;
+
+__device__ __forceinline__ uint64_t key_of(double x) {
+    return static_cast<uint64_t>(__double_as_longlong(x)) & kAbsMask;
+}
+
+// Round-to-nearest-even of a double to bfloat16, returned as the (exactly
+// representable) double. Same rule as oracle/microadam_oracle.c:mo_bf16_round.
+__device__ __forceinline__ double bf16_round(double x) {
+    if (!isfinite(x) || x == 0.0) return x;
+    if (fabs(x) < 0x1p-126) return __dmul_rn(rint(__dmul_rn(x, 0x1p133)), 0x1p-133);
+    uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
+    const uint64_t lsb = (u >> 45) & 1u;
+    u += ((uint64_t(1) << 44) - 1u) + lsb;
+    u &= ~((uint64_t(1) << 45) - 1u);
+    const double y = __longlong_as_double(static_cast<long long>(u));
+    if (fabs(y) >= 0x1p128) return copysign(__longlong_as_double(0x7FF0000000000000ll), x);
+    return y;
+}
+
+__device__ __forceinline__ double round_to(double x, int dt) {
+    if (dt == F64) return x;
+    if (dt == F32) return static_cast<double>(__double2float_rn(x));
+    return bf16_round(x);
+}
+
+__device__ __forceinline__ double ld_val(const void* p, int dt, int64_t i) {
+    if (dt == F64) return static_cast<const double*>(p)[i];
+    if (dt == F32) return static_cast<double>(static_cast<const float*>(p)[i]);
+    const uint32_t u = static_cast<const uint16_t*>(p)[i];
+    return static_cast<double>(__uint_as_float(u << 16));
+}
+
+// Two consecutive elements starting at an even index (aligned vector load).
+__device__ __forceinline__ void ld_pair(const void* p, int dt, int64_t i, double& x0, double& x1) {
+    if (dt == F64) {
+        const double2 v = static_cast<const double2*>(p)[i >> 1];
+        x0 = v.x;
+        x1 = v.y;
+    } else if (dt == F32) {
+        const float2 v = static_cast<const float2*>(p)[i >> 1];
+        x0 = v.x;
+        x1 = v.y;
+    } else {
+        const uint32_t v = static_cast<const uint32_t*>(p)[i >> 1];
+        x0 = static_cast<double>(__uint_as_float(v << 16));
+        x1 = static_cast<double>(__uint_as_float(v & 0xFFFF0000u));
+    }
+}
+
+__device__ __forceinline__ void st_val(void* p, int dt, int64_t i, double x) {
+    if (dt == F64) {
+        static_cast<double*>(p)[i] = x;
+    } else if (dt == F32) {
+        static_cast<float*>(p)[i] = __double2float_rn(x);
+    } else {
+        const float f = static_cast<float>(bf16_round(x));  // exact
+        static_cast<uint16_t*>(p)[i] = static_cast<uint16_t>(__float_as_uint(f) >> 16);
+    }
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+
+// Warp 0: locate the bin holding the need-th largest element of a 256-bin
+// histogram. out = {bin, count above bin, count in bin}; bin = -1 if the
+// histogram holds fewer than `need` elements.
+__device__ __forceinline__ void find_bin(const uint32_t* hist, uint32_t need, int* out) {
+    const int lane = threadIdx.x & 31;
+    uint32_t h[8];
+    uint32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        h[q] = hist[lane * 8 + q];
+        s += h[q];
+    }
+    uint32_t incl = s;  // Σ over lanes >= lane
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_down_sync(0xFFFFFFFFu, incl, off);
+        if (lane + off < 32) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 0);
+    if (total < need) {
+        if (lane == 0) {
+            out[0] = -1;
+            out[1] = 0;
+            out[2] = static_cast<int>(total);
+        }
+        return;
+    }
+    uint32_t cum = incl - s;
+#pragma unroll
+    for (int q = 7; q >= 0; --q) {
+        if (cum < need && cum + h[q] >= need) {
+            out[0] = lane * 8 + q;
+            out[1] = static_cast<int>(cum);
+            out[2] = static_cast<int>(h[q]);
+        }
+        cum += h[q];
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ void block_zero_hist(uint32_t* hist) {
+    for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
+}
+
+// Block Top-K (compress.cpp:39-53 semantics): select exactly `kb` of the
+// valid elements, the first under (|a| desc, index asc). Returns the
+// selection bitmask over the thread's register slots.
+//
+// Keys are the fp64 bit patterns with the sign cleared (monotone in |a|,
+// -0.0 == +0.0). Pass 1 is a 256-bin histogram of key>>45 (1/128 binade per
+// bin) over the top 256 bins below the block maximum, which usually leaves a
+// handful of candidates; a general 8-bit-digit radix select from bit 62
+// covers the rest. Once the candidates fit kCandCap they are ranked exactly
+// by (key desc, index asc); if all 63 bits tie, the lowest indices win.
+//
+// `elem(i)` maps register slot i to its block-relative element index;
+// `tie_rank(mask, rank)` returns, for the flagged slots, their exclusive rank
+// in element-index order across the block (all threads must call it).
+template <int NT, int EPT, class Elem, class TieRank>
+__device__ uint32_t block_topk(const double (&a)[EPT], uint32_t valid, int kb, uint32_t* hist,
+                               int* misc, uint64_t* ckey, int* cidx, uint8_t* selm, Elem elem,
+                               TieRank tie_rank) {
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    uint32_t sel = 0;
+    uint32_t tmax = 0;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i)
+        if ((valid >> i) & 1u) tmax = max(tmax, static_cast<uint32_t>(key_of(a[i]) >> 45));
+    tmax = __reduce_max_sync(0xFFFFFFFFu, tmax);
+    if (lane == 0) misc[warp] = static_cast<int>(tmax);
+    block_zero_hist<NT>(hist);
+    __syncthreads();
+    uint32_t top = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) top = max(top, static_cast<uint32_t>(misc[w]));
+    const uint32_t tbase = top >= 255u ? top - 255u : 0u;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+        if ((valid >> i) & 1u) {
+            const uint32_t t = static_cast<uint32_t>(key_of(a[i]) >> 45);
+            if (t >= tbase) atomicAdd(&hist[t - tbase], 1u);
+        }
+    }
+    __syncthreads();
+    if (warp == 0) find_bin(hist, static_cast<uint32_t>(kb), misc + 16);
+    __syncthreads();
+
+    int need = kb;
+    int fs;
+    uint64_t prefix;
+    int cnt;
+    if (misc[16] >= 0) {
+        prefix = tbase + static_cast<uint32_t>(misc[16]);
+        need -= misc[17];
+        cnt = misc[18];
+        fs = 45;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if (((valid >> i) & 1u) && (key_of(a[i]) >> 45) > prefix) sel |= 1u << i;
+    } else {
+        fs = 63;
+        prefix = 0;
+        cnt = 0x7FFFFFFF;  // unknown; forces a radix pass
+    }
+
+    for (;;) {
+        // Candidates: valid, unselected, key >> fs == prefix.
+        uint32_t cand = 0;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if (((valid >> i) & 1u) && !((sel >> i) & 1u) && (key_of(a[i]) >> fs) == prefix)
+                cand |= 1u << i;
+        if (cnt == need) {
+            sel |= cand;
+            break;
+        }
+        if (cnt <= kCandCap) {
+            __syncthreads();  // misc[20] / ckey reuse
+            if (tid == 0) misc[20] = 0;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                if ((cand >> i) & 1u) {
+                    const int s = atomicAdd(&misc[20], 1);
+                    ckey[s] = key_of(a[i]);
+                    cidx[s] = elem(i);
+                }
+            }
+            __syncthreads();
+            const int n = misc[20];
+            for (int c = tid; c < n; c += NT) {
+                const uint64_t kc = ckey[c];
+                const int ic = cidx[c];
+                int r = 0;
+                for (int q = 0; q < n; ++q) {
+                    const uint64_t kq = ckey[q];
+                    r += (kq > kc) || (kq == kc && cidx[q] < ic);
+                }
+                if (r < need) selm[ic] = 1;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < EPT; ++i)
+                if (((cand >> i) & 1u) && selm[elem(i)]) sel |= 1u << i;
+            break;
+        }
+        if (fs == 0) {
+            // Exact 63-bit ties beyond the cap: lowest indices win.
+            int rank[EPT];
+            tie_rank(cand, rank);
+#pragma unroll
+            for (int i = 0; i < EPT; ++i)
+                if (((cand >> i) & 1u) && rank[i] < need) sel |= 1u << i;
+            break;
+        }
+        const int ns = fs > 8 ? fs - 8 : 0;
+        const int width = fs - ns;
+        const uint32_t mask = (1u << width) - 1u;
+        __syncthreads();  // hist / misc reuse
+        block_zero_hist<NT>(hist);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if ((cand >> i) & 1u)
+                atomicAdd(&hist[static_cast<uint32_t>(key_of(a[i]) >> ns) & mask], 1u);
+        __syncthreads();
+        if (warp == 0) find_bin(hist, static_cast<uint32_t>(need), misc + 16);
+        __syncthreads();
+        const uint32_t bin = static_cast<uint32_t>(misc[16]);
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if (((cand >> i) & 1u) && (static_cast<uint32_t>(key_of(a[i]) >> ns) & mask) > bin)
+                sel |= 1u << i;
+        need -= misc[17];
+        cnt = misc[18];
+        prefix = (prefix << width) | bin;
+        fs = ns;
+    }
+    return sel;
+}
+
+}  // namespace dev
+}  // namespace ma

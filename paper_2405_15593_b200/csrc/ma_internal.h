@@ -26,6 +26,7 @@ struct StepArgs {
     void* win_val;    // [num_blocks][m][kb_stride] values (value dtype)
     unsigned int* flag;
     double* partials; // nullable: [num_blocks][kReportFields]
+    uint32_t* thresh; // [num_blocks] Top-K fast-path threshold carried across steps (fast kernel)
     int64_t dim;
     int64_t num_blocks;
     int64_t block_offset;
@@ -48,6 +49,11 @@ size_t step_smem_bytes(int nt, int ept, int block, int bucket, int m, int kb_str
 Variant pick_variant(int block);
 
 cudaError_t launch_step(const StepArgs& a, Variant v, int64_t nblocks, cudaStream_t s);
+
+// Fast kernel (ma_fast.cu): B_q in {16, 32, 64}, B_d % 8 == 0, m*kb_stride <= 65535.
+Variant pick_fast_variant(int block, int bucket, int m, int kb_stride);
+size_t fast_smem_bytes(Variant v, int block, int m, int kb_stride, int p_dtype);
+cudaError_t launch_step_fast(const StepArgs& a, Variant v, int64_t nblocks, cudaStream_t s);
 cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int* flag,
                                cudaStream_t s);
 cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double* out5,

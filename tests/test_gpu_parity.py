@@ -39,9 +39,29 @@ def _host(t):
     return t.detach().to(torch.float64).cpu().numpy()
 
 
-def run_parity(d, hp, *, gdt="f32", pdt="f32", vdt="bf16", steps=12, levels=False, seed=42,
-               grad_fn=None, check_reference=None, lr=None, report_every=0):
+KERNELS = {"fast": {}, "fast_g2": {"MA_FAST_G2": "1"}, "generic": {"MA_FORCE_GENERIC": "1"}}
+
+
+def make_engine(kernel, *args, **kw):
+    """Create a MicroAdam engine with the kernel family selected at ma_create time."""
+    import os
     from paper_2405_15593_b200 import MicroAdam
+    saved = {k: os.environ.get(k) for k in ("MA_FAST_G2", "MA_FORCE_GENERIC")}
+    for k in saved:
+        os.environ.pop(k, None)
+    os.environ.update(KERNELS[kernel])
+    try:
+        return MicroAdam(*args, **kw)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def run_parity(d, hp, *, gdt="f32", pdt="f32", vdt="bf16", steps=12, levels=False, seed=42,
+               grad_fn=None, check_reference=None, lr=None, report_every=0, kernel="fast"):
     torch = _torch()
     oracle.build()
     lr = hp.get("lr", 1e-3) if lr is None else lr
@@ -52,7 +72,7 @@ def run_parity(d, hp, *, gdt="f32", pdt="f32", vdt="bf16", steps=12, levels=Fals
         check_reference = pdt == "f64" and vdt == "f64" and oracle.reference_available()
     if check_reference:
         ref = oracle.Reference(theta0, hp)
-    eng = MicroAdam(d, hp, param_dtype=pdt, grad_dtype=gdt, value_dtype=vdt)
+    eng = make_engine(kernel, d, hp, param_dtype=pdt, grad_dtype=gdt, value_dtype=vdt)
     params = _dev(theta0, pdt)
     for s in range(1, steps + 1):
         g = grad_fn(s) if grad_fn else oracle.synth(seed, s, 0, d, gdt, levels=levels)
@@ -93,15 +113,17 @@ def run_parity(d, hp, *, gdt="f32", pdt="f32", vdt="bf16", steps=12, levels=Fals
     return eng, orc
 
 
-def test_default_config_1m_fp32_bf16_window():
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
+def test_default_config_1m_fp32_bf16_window(kernel):
     # SURVEY config 1 shape (1M params, density 1%, m=10, 4-bit EF, B_d 4096, B_q 64).
     run_parity(1_000_000, dict(lr=1e-3), gdt="f32", pdt="f32", vdt="bf16", steps=20,
-               report_every=5)
+               report_every=5, kernel=kernel)
 
 
-def test_fp64_mode_bit_exact_vs_unmodified_reference():
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
+def test_fp64_mode_bit_exact_vs_unmodified_reference(kernel):
     run_parity(200_000, dict(lr=1e-3), gdt="f64", pdt="f64", vdt="f64", steps=15,
-               check_reference=oracle.reference_available())
+               check_reference=oracle.reference_available(), kernel=kernel)
 
 
 def test_bf16_params_and_grads():
@@ -126,20 +148,37 @@ def test_fp32_window_values():
     (130, 128, 64, 0.5, 1),        # m = 1
     (8, 4, 2, 0.25, 10),           # test_optim.cpp:265-274 shape
 ])
-def test_shapes(d, block, bucket, density, m):
+@pytest.mark.parametrize("kernel", ["fast", "generic"])
+def test_shapes(d, block, bucket, density, m, kernel):
     hp = dict(block=block, bucket=bucket, density=density, window=m, lr=1e-2)
-    run_parity(d, hp, gdt="f64", pdt="f64", vdt="f64", steps=m + 4)
+    run_parity(d, hp, gdt="f64", pdt="f64", vdt="f64", steps=m + 4, kernel=kernel)
 
 
-def test_tie_heavy_levels():
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
+def test_tie_heavy_levels(kernel):
     # 16 grad levels: many exact |a| ties; index order must decide.
-    run_parity(40_000, dict(lr=1e-2), gdt="f32", pdt="f32", vdt="bf16", steps=10, levels=True)
+    run_parity(40_000, dict(lr=1e-2), gdt="f32", pdt="f32", vdt="bf16", steps=10, levels=True,
+               kernel=kernel)
 
 
-def test_zero_gradient_degenerate_buckets():
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
+def test_zero_gradient_degenerate_buckets(kernel):
     # all-zero gradients: every |a| ties, every bucket lo == hi (level 0).
     run_parity(20_000, dict(lr=1e-2), gdt="f32", pdt="f32", vdt="bf16", steps=6,
-               grad_fn=lambda s: np.zeros(20_000))
+               grad_fn=lambda s: np.zeros(20_000), kernel=kernel)
+
+
+@pytest.mark.parametrize("bucket", [16, 32])
+def test_fast_kernel_small_buckets(bucket):
+    run_parity(70_000, dict(lr=1e-2, bucket=bucket), gdt="bf16", pdt="bf16", vdt="bf16", steps=8)
+
+
+def test_distribution_shift_and_threshold_recovery():
+    # scale jumps by 2^20 between steps: the carried Top-K threshold is wrong
+    # in both directions and the exact fallback must take over.
+    scales = [1.0, 2.0 ** 20, 2.0 ** 20, 2.0 ** -20, 1.0, 1.0, 3.0, 1.0]
+    run_parity(60_000, dict(lr=1e-2), gdt="f64", pdt="f64", vdt="f64", steps=len(scales),
+               grad_fn=lambda s: oracle.synth(9, s, 0, 60_000) * scales[s - 1])
 
 
 def test_sparse_spiky_gradients():
