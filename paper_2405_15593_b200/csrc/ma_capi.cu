@@ -155,7 +155,9 @@ struct ma_handle {
     ma_config cfg{};
     Shape shape;
     ma::Variant variant{};
+    ma::Variant tail_variant{};  // generic kernel for the partial tail block (fast path)
     bool fast = false;  // ma_fast.cu kernel (else the generic ma_kernels.cu kernel)
+    int persist_grid = 0;
     int device = 0;
     uint8_t* d_codes = nullptr;
     double2* d_meta = nullptr;
@@ -254,9 +256,28 @@ void base_args(ma_handle* h, ma::StepArgs* a) {
     a->eps = h->cfg.hp.eps;
 }
 
-cudaError_t launch(ma_handle* h, const ma::StepArgs& a, int64_t nblocks, cudaStream_t st) {
-    return h->fast ? ma::launch_step_fast(a, h->variant, nblocks, st)
-                   : ma::launch_step(a, h->variant, nblocks, st);
+// Fast path: the persistent kernel takes the range's full blocks and the
+// generic kernel the shard's partial tail block (if it is in the range).
+cudaError_t launch(ma_handle* h, ma::StepArgs& a, int64_t nblocks, cudaStream_t st) {
+    if (!h->fast) return ma::launch_step(a, h->variant, nblocks, st);
+    const Shape& s = h->shape;
+    const int64_t nb_shard = s.b1 - s.b0;
+    const bool tail_partial = (s.dim % s.block) != 0 && a.block_offset + nblocks == nb_shard;
+    const int64_t nfull = nblocks - (tail_partial ? 1 : 0);
+    if (nfull > 0) {
+        a.block_count = nfull;
+        const int64_t grid = std::min<int64_t>(nfull, h->persist_grid);
+        cudaError_t e = ma::launch_step_fast(a, h->variant, int(grid), st);
+        if (e != cudaSuccess) return e;
+    }
+    if (tail_partial) {
+        ma::StepArgs t = a;
+        t.block_offset = a.block_offset + nfull;
+        t.block_count = 1;
+        ++h->launches;
+        return ma::launch_step(t, h->tail_variant, 1, st);
+    }
+    return cudaSuccess;
 }
 
 ma_status finish_report(ma_handle* h, cudaStream_t st, ma_step_report* report) {
@@ -373,19 +394,24 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     const char* force_generic = std::getenv("MA_FORCE_GENERIC");
     const ma::Variant fv = ma::pick_fast_variant(int(s.block), int(s.bucket), int(cfg->hp.window),
                                                  int(s.kb_stride));
-    if (fv.nt && !(force_generic && force_generic[0] == '1') &&
-        ma::fast_smem_bytes(fv, int(s.block), int(cfg->hp.window), int(s.kb_stride),
-                            cfg->param_dtype) <= size_t(smem_max)) {
-        h->variant = fv;
-        h->fast = true;
-    } else {
-        h->variant = ma::pick_variant(static_cast<int>(s.block));
+    h->tail_variant = ma::pick_variant(static_cast<int>(s.block));
+    size_t smem = ma::step_smem_bytes(h->tail_variant.nt, h->tail_variant.ept, int(s.block),
+                                      int(s.bucket), int(cfg->hp.window), int(s.kb_stride));
+    if (fv.nt && !(force_generic && force_generic[0] == '1')) {
+        const size_t fs = ma::fast_smem_bytes(fv, int(s.block), int(s.bucket), int(cfg->hp.window),
+                                              int(s.kb_stride), cfg->grad_dtype, cfg->param_dtype,
+                                              cfg->value_dtype);
+        const int per_sm = fs <= size_t(smem_max) ? ma::fast_blocks_per_sm(fv, int(s.bucket), fs) : 0;
+        if (per_sm > 0) {
+            int nsm = 0;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+            h->variant = fv;
+            h->fast = true;
+            h->persist_grid = per_sm * nsm;
+            smem = std::max(smem, fs);
+        }
     }
-    const size_t smem = h->fast ? ma::fast_smem_bytes(h->variant, int(s.block), int(cfg->hp.window),
-                                                      int(s.kb_stride), cfg->param_dtype)
-                                : ma::step_smem_bytes(h->variant.nt, h->variant.ept, int(s.block),
-                                                      int(s.bucket), int(cfg->hp.window),
-                                                      int(s.kb_stride));
+    if (!h->fast) h->variant = h->tail_variant;
     if (smem > size_t(smem_max)) {
         delete h;
         return fail(MA_ERR_UNSUPPORTED, "block/window shape needs more shared memory than one SM has");

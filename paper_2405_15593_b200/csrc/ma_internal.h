@@ -30,6 +30,7 @@ struct StepArgs {
     int64_t dim;
     int64_t num_blocks;
     int64_t block_offset;
+    int64_t block_count;  // blocks [block_offset, block_offset + block_count) (persistent kernel)
     int32_t block, per_block_k, kb_stride, bucket;
     int32_t m, filled, slot, check_finite;
     int32_t g_dtype, p_dtype, v_dtype, pad0;
@@ -50,10 +51,13 @@ Variant pick_variant(int block);
 
 cudaError_t launch_step(const StepArgs& a, Variant v, int64_t nblocks, cudaStream_t s);
 
-// Fast kernel (ma_fast.cu): B_q in {16, 32, 64}, B_d % 8 == 0, m*kb_stride <= 65535.
+// Fast persistent kernel (ma_fast.cu): full blocks only; B_q in {16, 32, 64},
+// B_d in {1024, 2048, 4096, 8192}, m*kb_stride <= 65535. ept = 8 * groups per thread.
 Variant pick_fast_variant(int block, int bucket, int m, int kb_stride);
-size_t fast_smem_bytes(Variant v, int block, int m, int kb_stride, int p_dtype);
-cudaError_t launch_step_fast(const StepArgs& a, Variant v, int64_t nblocks, cudaStream_t s);
+size_t fast_smem_bytes(Variant v, int block, int bucket, int m, int kb_stride, int g_dtype,
+                       int p_dtype, int v_dtype);
+int fast_blocks_per_sm(Variant v, int bucket, size_t smem);
+cudaError_t launch_step_fast(const StepArgs& a, Variant v, int grid, cudaStream_t s);
 cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int* flag,
                                cudaStream_t s);
 cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double* out5,
