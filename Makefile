@@ -13,7 +13,7 @@ NVFLAGS  := -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
             -fmad=false -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
             -Xcompiler -fvisibility=hidden -Xptxas -warn-spills
 SRCS     := $(CSRC)/ma_kernels.cu $(CSRC)/ma_fast.cu $(CSRC)/ma_capi.cu $(CSRC)/microadam_b200.cpp
-HDRS     := include/microadam_cuda.h include/ma_synth.h $(CSRC)/ma_internal.h $(CSRC)/ma_device.cuh $(CSRC)/microadam_b200.hpp
+HDRS     := include/microadam_cuda.h include/ma_synth.h $(CSRC)/ma_internal.h $(CSRC)/ma_device.cuh $(CSRC)/ma_async.cuh $(CSRC)/microadam_b200.hpp
 
 .PHONY: all lib oracle clean sass
 all: lib oracle

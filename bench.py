@@ -377,7 +377,9 @@ def run_ours(args):
                          "traffic": (traffic_total if traffic_total is None else traffic_total),
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "bytes_per_param": bytes_launch / n,
-                         "kernel_ms": kern * 1e3, "peak_source": peak_src,
+                         "kernel_ms": kern * 1e3,
+                         "kernel_ms_per_step": [round(a.elapsed_time(b_), 3) for a, b_ in kev],
+                         "peak_source": peak_src,
                          "traffic_source": traffic_src,
                          "kernel": "microadam_step_kernel (fused P1-P6)"},
             "e2e": e2e,

@@ -323,7 +323,7 @@ def test_block_sharding_matches_unsharded():
 def test_kernel_counts_and_library_is_native():
     """The step runs through libmicroadam_cuda.so (no fallback path exists)."""
     import paper_2405_15593_b200 as pkg
-    d = 50_000
+    d = 12 * 4096  # whole blocks: one fused launch per step (a partial tail adds one)
     eng = pkg.MicroAdam(d, dict(lr=1e-3))
     params = _dev(oracle.synth(1, 0, 0, d, "f32"), "f32")
     g = _dev(oracle.synth(42, 1, 0, d, "f32"), "f32")
