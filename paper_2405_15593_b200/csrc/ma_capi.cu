@@ -393,7 +393,8 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     const char* force_generic = std::getenv("MA_FORCE_GENERIC");
     const ma::Variant fv = ma::pick_fast_variant(int(s.block), int(s.bucket), int(cfg->hp.window),
-                                                 int(s.kb_stride));
+                                                 int(s.kb_stride), cfg->grad_dtype,
+                                                 cfg->param_dtype, cfg->value_dtype);
     h->tail_variant = ma::pick_variant(static_cast<int>(s.block));
     size_t smem = ma::step_smem_bytes(h->tail_variant.nt, h->tail_variant.ept, int(s.block),
                                       int(s.bucket), int(cfg->hp.window), int(s.kb_stride));

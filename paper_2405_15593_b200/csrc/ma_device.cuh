@@ -70,6 +70,27 @@ __device__ __forceinline__ void st_val(void* p, int dt, int64_t i, double x) {
     }
 }
 
+// Compile-time-dtype variants (the fast kernel instantiates per dtype combo).
+template <int DT>
+__device__ __forceinline__ double ld_t(const void* p, int64_t i) {
+    if constexpr (DT == F64) return static_cast<const double*>(p)[i];
+    else if constexpr (DT == F32) return static_cast<double>(static_cast<const float*>(p)[i]);
+    else return static_cast<double>(__uint_as_float(uint32_t(static_cast<const uint16_t*>(p)[i]) << 16));
+}
+template <int DT>
+__device__ __forceinline__ void st_t(void* p, int64_t i, double x) {
+    if constexpr (DT == F64) static_cast<double*>(p)[i] = x;
+    else if constexpr (DT == F32) static_cast<float*>(p)[i] = __double2float_rn(x);
+    else static_cast<uint16_t*>(p)[i] =
+        static_cast<uint16_t>(__float_as_uint(static_cast<float>(bf16_round(x))) >> 16);
+}
+template <int DT>
+__device__ __forceinline__ double round_t(double x) {
+    if constexpr (DT == F64) return x;
+    else if constexpr (DT == F32) return static_cast<double>(__double2float_rn(x));
+    else return bf16_round(x);
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));

@@ -82,6 +82,14 @@ struct Layout4 {
     }
 };
 
+// Compile-time shape of one fast-kernel instantiation.
+template <int G_, int LPB_, int GDT_, int PDT_, int VDT_, bool REP_>
+struct K {
+    static constexpr int G = G_, LPB = LPB_, GDT = GDT_, PDT = PDT_, VDT = VDT_;
+    static constexpr bool REPORT = REP_;
+    static constexpr int BUCKET = 8 * LPB_, BLOCK = 8 * kNT * G_;
+};
+
 struct Ctx {
     const StepArgs* p;
     unsigned char* smem;
@@ -91,8 +99,9 @@ struct Ctx {
 };
 
 // 8 consecutive g values (element e0, 8-aligned) as doubles.
-__device__ __forceinline__ void load_g8(const void* g, int dt, int64_t e0, double (&x)[8]) {
-    if (dt == BF16) {
+template <int DT>
+__device__ __forceinline__ void load_g8(const void* g, int64_t e0, double (&x)[8]) {
+    if constexpr (DT == BF16) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + e0));
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -100,7 +109,7 @@ __device__ __forceinline__ void load_g8(const void* g, int dt, int64_t e0, doubl
             x[2 * k] = static_cast<double>(__uint_as_float(w[k] << 16));
             x[2 * k + 1] = static_cast<double>(__uint_as_float(w[k] & 0xFFFF0000u));
         }
-    } else if (dt == F32) {
+    } else if constexpr (DT == F32) {
         const float4* q = reinterpret_cast<const float4*>(static_cast<const float*>(g) + e0);
         const float4 v0 = __ldg(q), v1 = __ldg(q + 1);
         x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
@@ -118,11 +127,12 @@ __device__ __forceinline__ void load_g8(const void* g, int dt, int64_t e0, doubl
 
 // a = g + (code·level + lo) for the 8 elements at e0 (quantize.cpp:164-178,
 // optim.cpp:166-168): separate multiply and add, fp64, no FMA.
+template <class KT>
 __device__ __forceinline__ void decode8(const Ctx& c, int e0, double (&a)[8]) {
     const StepArgs& p = *c.p;
-    load_g8(p.grads, p.g_dtype, c.base + e0, a);
+    load_g8<KT::GDT>(p.grads, c.base + e0, a);
     const uint32_t cw = __ldg(reinterpret_cast<const uint32_t*>(p.codes + ((c.base + e0) >> 1)));
-    const int bk = e0 / c.bucket;
+    const int bk = e0 / KT::BUCKET;
     const double lo = reinterpret_cast<const double*>(c.smem + c.L.lo)[bk];
     const double level = reinterpret_cast<const double*>(c.smem + c.L.lvl)[bk];
 #pragma unroll
@@ -130,14 +140,54 @@ __device__ __forceinline__ void decode8(const Ctx& c, int e0, double (&a)[8]) {
         a[i] = __dadd_rn(a[i], __dadd_rn(__dmul_rn(static_cast<double>((cw >> (4 * i)) & 15u), level), lo));
 }
 
+template <class KT>
 __device__ __forceinline__ double recompute_a(const Ctx& c, int e) {
     const StepArgs& p = *c.p;
     const uint32_t byte = p.codes[(c.base + e) >> 1];
-    const int bk = e / c.bucket;
+    const int bk = e / KT::BUCKET;
     const double lo = reinterpret_cast<const double*>(c.smem + c.L.lo)[bk];
     const double level = reinterpret_cast<const double*>(c.smem + c.L.lvl)[bk];
     const double ev = __dadd_rn(__dmul_rn(static_cast<double>((byte >> ((e & 1) * 4)) & 15u), level), lo);
-    return __dadd_rn(ld_val(p.grads, p.g_dtype, c.base + e), ev);
+    return __dadd_rn(ld_t<KT::GDT>(p.grads, c.base + e), ev);
+}
+
+// t / kb for t < 2^16 without an integer division (float reciprocal + fix-up).
+__device__ __forceinline__ int row_of(int t, int kb, float inv_kb) {
+    int r = __float2int_rz(static_cast<float>(t) * inv_kb);
+    r -= (r * kb > t);
+    r += ((r + 1) * kb <= t);
+    return r;
+}
+
+// Rank correction among candidates whose high words tie (compress.cpp:43-48:
+// full |a| key first, then the lower index). Out of line: rare.
+__device__ __noinline__ int tie_rank_hi(const double* cval, const uint32_t* ckhi, const int* cidx,
+                                        int ncand, int t) {
+    const uint32_t kh = ckhi[t];
+    const uint64_t kt = key_of(cval[t]);
+    const int it = cidx[t];
+    int extra = 0;
+    for (int q = 0; q < ncand; ++q) {
+        if (q == t || ckhi[q] != kh) continue;
+        const uint64_t kq = key_of(cval[q]);
+        extra += (kq > kt) || (kq == kt && cidx[q] < it);
+    }
+    return extra;
+}
+
+// The IEEE path of quantize_nearest (quantize.cpp:51-53) for the elements
+// whose fast fixed-point code fell in the guard band. Out of line: rare.
+__device__ __noinline__ uint32_t exact_codes(const double (&a)[8], double lo, double rng,
+                                             uint32_t bad, uint32_t word) {
+    const double level = __ddiv_rn(rng, 15.0);
+#pragma unroll 1
+    for (int i = 0; i < 8; ++i) {
+        if (!((bad >> i) & 1u)) continue;
+        double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(a[i], lo), level), 0.5));
+        f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+        word = (word & ~(15u << (4 * i))) | (static_cast<uint32_t>(f) << (4 * i));
+    }
+    return word;
 }
 
 __device__ __forceinline__ void word_prefix(const uint32_t* bits, int nwords, int* pref) {
@@ -165,6 +215,7 @@ __device__ __forceinline__ void wait_stage(uint64_t* bar) {
 
 // Selected element e (value a) -> window row `slot` at its ascending position
 // (window.cpp:14-26): global ring, the staged rows, and its owner mark.
+template <class KT>
 __device__ __forceinline__ void emit_selected(const Ctx& c, int e, double a) {
     const StepArgs& p = *c.p;
     const uint32_t* s_sel = reinterpret_cast<const uint32_t*>(c.smem + c.L.sel);
@@ -172,10 +223,10 @@ __device__ __forceinline__ void emit_selected(const Ctx& c, int e, double a) {
     const int pos = s_wpref[e >> 5] + __popc(s_sel[e >> 5] & ((1u << (e & 31)) - 1u));
     const int64_t g = (c.b * c.m + c.slot) * static_cast<int64_t>(c.kbs) + pos;
     p.win_idx[g] = static_cast<int16_t>(e);
-    st_val(p.win_val, p.v_dtype, g, a);
+    st_t<KT::VDT>(p.win_val, g, a);
     const int ent = c.slot * c.kbs + pos;
     reinterpret_cast<int16_t*>(c.smem + c.L.widx)[ent] = static_cast<int16_t>(e);
-    st_val(c.smem + c.L.wval, p.v_dtype, ent, a);
+    st_t<KT::VDT>(c.smem + c.L.wval, ent, a);
     (c.smem + c.L.owner)[e] = static_cast<uint8_t>(c.slot);
 }
 
@@ -183,6 +234,7 @@ __device__ __forceinline__ void emit_selected(const Ctx& c, int e, double a) {
 // count left [k_b, kCandCap]: the generic radix select on a recomputed from
 // the (L2-hot) inputs. Sets the selection bitmap + prefix, emits the new row
 // and misc[1] = next threshold.
+template <class KT>
 __device__ __noinline__ void fallback_select(const Ctx& c) {
     unsigned char* sm = c.smem;
     uint32_t* s_sel = reinterpret_cast<uint32_t*>(sm + c.L.sel);
@@ -200,7 +252,7 @@ __device__ __noinline__ void fallback_select(const Ctx& c) {
     for (int s = 0; s < kEPT; ++s) {
         a[s] = 0.0;
         if (elem(s) < c.block) {
-            a[s] = recompute_a(c, elem(s));
+            a[s] = recompute_a<KT>(c, elem(s));
             valid |= 1u << s;
         }
     }
@@ -239,18 +291,17 @@ __device__ __noinline__ void fallback_select(const Ctx& c) {
     wait_stage(reinterpret_cast<uint64_t*>(sm + c.L.bar));
 #pragma unroll
     for (int s = 0; s < kEPT; ++s)
-        if ((sel >> s) & 1u) emit_selected(c, elem(s), a[s]);
+        if ((sel >> s) & 1u) emit_selected<KT>(c, elem(s), a[s]);
     if (tid == 0) {
         const uint32_t km = static_cast<uint32_t>(s_misc[2]);
         s_misc[1] = static_cast<int>(km > (1u << 15) ? km - (1u << 15) : 1u);
     }
 }
 
-template <int G, int LPB>
+template <class KT>
 __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_constant__ StepArgs p) {
     constexpr int NW = kNT / 32;
-    constexpr int BUCKET = 8 * LPB;
-    constexpr int BLOCK = 8 * kNT * G;
+    constexpr int G = KT::G, LPB = KT::LPB, BUCKET = KT::BUCKET, BLOCK = KT::BLOCK;
     static_assert(8 * G <= kEPT, "candidate masks are 32-bit");
     extern __shared__ __align__(128) unsigned char smem[];
     Ctx c;
@@ -263,7 +314,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     c.kbs = p.kb_stride;
     c.kb = p.per_block_k;
     c.slot = p.slot;
-    c.L = Layout4(BLOCK, BUCKET, p.m, p.kb_stride, p.p_dtype, p.v_dtype);
+    c.L = Layout4(BLOCK, BUCKET, p.m, p.kb_stride, KT::PDT, KT::VDT);
     c.b = p.block_offset + blockIdx.x;
     c.base = c.b * BLOCK;
     const Layout4& L = c.L;
@@ -283,11 +334,13 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     int* s_misc = reinterpret_cast<int*>(smem + L.misc);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int psz = dtype_bytes(p.p_dtype), vsz = dtype_bytes(p.v_dtype);
+    constexpr int psz = KT::PDT == F64 ? 8 : (KT::PDT == F32 ? 4 : 2);
+    constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
     const int kb = c.kb, kbs = c.kbs, slot = c.slot, filled = p.filled, m = c.m;
     const int nent = filled * kb;
+    const float inv_kb = 1.0f / static_cast<float>(kb);
     const int64_t b = c.b, base = c.base;
-    const bool want_report = p.partials != nullptr;
+    constexpr bool want_report = KT::REPORT;
 
     // ---- prologue: θ + window rows HBM→smem (bulk async), bucket grids ----
     if (tid == 0) {
@@ -317,11 +370,11 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     // ---- P1: a = g + decode(EF); keys above T become Top-K candidates ----
     uint32_t kmax = 0;
     double rep[kReportFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
+#pragma unroll 1
     for (int g = 0; g < G; ++g) {
         const int e0 = (g * kNT + tid) * 8;
         double a[8];
-        decode8(c, e0, a);
+        decode8<KT>(c, e0, a);
         uint32_t m8 = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -366,15 +419,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
                 eq += v == kh;
             }
             int rank = above;
-            if (eq > 1) {  // high words tie: full key, then index (compress.cpp:43-48)
-                const uint64_t kt = key_of(s_cval[t]);
-                const int it = s_cidx[t];
-                for (int q = 0; q < ncand; ++q) {
-                    if (q == t || s_ckhi[q] != kh) continue;
-                    const uint64_t kq = key_of(s_cval[q]);
-                    rank += (kq > kt) || (kq == kt && s_cidx[q] < it);
-                }
-            }
+            if (eq > 1) rank += tie_rank_hi(s_cval, s_ckhi, s_cidx, ncand, t);
             if (rank < kb) atomicOr(&s_sel[s_cidx[t] >> 5], 1u << (s_cidx[t] & 31));
             if (rank == target)
                 s_misc[1] = static_cast<int>(ncand > kTarget ? kh : (kh > (1u << 15) ? kh - (1u << 15) : 1u));
@@ -385,28 +430,28 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
         wait_stage(s_bar);
         for (int t = tid; t < ncand; t += kNT) {
             const int e = s_cidx[t];
-            if ((s_sel[e >> 5] >> (e & 31)) & 1u) emit_selected(c, e, s_cval[t]);
+            if ((s_sel[e >> 5] >> (e & 31)) & 1u) emit_selected<KT>(c, e, s_cval[t]);
         }
     } else {
-        fallback_select(c);
+        fallback_select<KT>(c);
     }
     if (tid == 0) p.thresh[b] = static_cast<uint32_t>(s_misc[1]);
 
     // ---- pass A (older rows): owner row per coordinate ----
     wait_stage(s_bar);
     for (int t = tid; t < nent; t += kNT) {
-        const int r = t / kb;
+        const int r = row_of(t, kb, inv_kb);
         if (r == slot) continue;
         s_owner[swi[r * kbs + (t - r * kb)]] = static_cast<uint8_t>(r);
     }
 
     // ---- P3/P4: residual (compress.cpp:95-102) + 4-bit re-quantization
     //      (quantize.cpp:15-24, 42-55, 102-114, 142-162) ----
-#pragma unroll
+#pragma unroll 1
     for (int g = 0; g < G; ++g) {
         const int e0 = (g * kNT + tid) * 8;
         double a[8];
-        decode8(c, e0, a);
+        decode8<KT>(c, e0, a);
         const uint32_t sel8 = (s_sel[e0 >> 5] >> (e0 & 31)) & 0xFFu;
         double lo = __longlong_as_double(0x7FF0000000000000ll), hi = -lo;
 #pragma unroll
@@ -435,21 +480,12 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
                 word |= (xq >> 20) << (4 * i);
                 bad |= static_cast<uint32_t>(((xq + kGuard) & 0xFFFFFu) < 2 * kGuard) << i;
             }
-            if (bad) {  // rare: the exact IEEE quotient for elements in the guard band
-                const double level = __ddiv_rn(rng, 15.0);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if (!((bad >> i) & 1u)) continue;
-                    double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(a[i], lo), level), 0.5));
-                    f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
-                    word = (word & ~(15u << (4 * i))) | (static_cast<uint32_t>(f) << (4 * i));
-                }
-            }
+            if (bad) word = exact_codes(a, lo, rng, bad, word);  // rare: guard band
         }
         if (want_report) {
             const double level = rng == 0.0 ? 0.0 : __ddiv_rn(rng, 15.0);
             double x[8];
-            load_g8(p.grads, p.g_dtype, base + e0, x);
+            load_g8<KT::GDT>(p.grads, base + e0, x);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const double en =
@@ -465,7 +501,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
 
     // ---- P6 pass B: duplicate bit (coordinate present in more than one row) ----
     for (int t = tid; t < nent; t += kNT) {
-        const int r = t / kb;
+        const int r = row_of(t, kb, inv_kb);
         const int idx = swi[r * kbs + (t - r * kb)];
         if ((s_owner[idx] & 0x7F) != r) s_owner[idx] |= 0x80;
     }
@@ -473,14 +509,14 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
 
     // ---- P6 pass C: ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) ----
     for (int t = tid; t < nent; t += kNT) {
-        const int r = t / kb;
+        const int r = row_of(t, kb, inv_kb);
         const int e = r * kbs + (t - r * kb);
         const int idx = swi[e];
         const uint32_t own = s_owner[idx];
         if ((own & 0x7F) != static_cast<uint32_t>(r)) continue;
         double z1, z2;
         if (!(own & 0x80)) {
-            const double v = ld_val(swv, p.v_dtype, e);
+            const double v = ld_t<KT::VDT>(swv, e);
             z1 = __dadd_rn(0.0, __dmul_rn(p.w1[r], v));
             z2 = __dadd_rn(0.0, __dmul_rn(p.w2[r], __dmul_rn(v, v)));
         } else {
@@ -494,7 +530,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
                     if (row[mid] < idx) lo_i = mid + 1; else hi_i = mid;
                 }
                 if (lo_i < kb && row[lo_i] == idx) {
-                    const double v = ld_val(swv, p.v_dtype, rr * kbs + lo_i);
+                    const double v = ld_t<KT::VDT>(swv, rr * kbs + lo_i);
                     z1 = __dadd_rn(z1, __dmul_rn(p.w1[rr], v));
                     z2 = __dadd_rn(z2, __dmul_rn(p.w2[rr], __dmul_rn(v, v)));
                 }
@@ -503,8 +539,8 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
         const double mhat = __dmul_rn(z1, p.scale1);
         const double vhat = __dmul_rn(z2, p.scale2);
         const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
-        const double th = ld_val(sth, p.p_dtype, idx);
-        st_val(sth, p.p_dtype, idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
+        const double th = ld_t<KT::PDT>(sth, idx);
+        st_t<KT::PDT>(sth, idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
         if (want_report && u != 0.0) rep[4] += 1.0;
     }
     fence_proxy_async_smem();
@@ -514,7 +550,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
                  static_cast<uint32_t>(BLOCK * psz));
         bulk_wait_read();
     }
-    if (want_report) {
+    if constexpr (want_report) {
 #pragma unroll
         for (int f = 0; f < kReportFields; ++f) {
 #pragma unroll
@@ -530,10 +566,10 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     }
 }
 
-template <int G, int LPB>
-cudaError_t launch_g(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
-    const size_t smem = Layout4(8 * kNT * G, 8 * LPB, a.m, a.kb_stride, a.p_dtype, a.v_dtype).total;
-    auto k = microadam_step_fast<G, LPB>;
+template <class KT>
+cudaError_t launch_k(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
+    const size_t smem = Layout4(KT::BLOCK, KT::BUCKET, a.m, a.kb_stride, KT::PDT, KT::VDT).total;
+    auto k = microadam_step_fast<KT>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem));
     if (err != cudaSuccess) return err;
@@ -541,22 +577,54 @@ cudaError_t launch_g(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int LPB>
-cudaError_t launch_lpb(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
-    switch (a.block) {
-        case 1024: return launch_g<1, LPB>(a, nblocks, s);
-        case 2048: return launch_g<2, LPB>(a, nblocks, s);
-        case 4096: return launch_g<4, LPB>(a, nblocks, s);
+// Instantiated dtype combos (g, θ, window value); others use the generic kernel.
+#define MA_FAST_DTYPES(X)         \
+    X(BF16, BF16, BF16)           \
+    X(F32, F32, BF16)             \
+    X(F32, F32, F32)              \
+    X(BF16, F32, BF16)            \
+    X(F64, F64, F64)
+
+constexpr int dtype_key(int g, int p, int v) { return g * 9 + p * 3 + v; }
+
+template <int LPB, bool REP>
+cudaError_t launch_dt(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
+    switch (dtype_key(a.g_dtype, a.p_dtype, a.v_dtype)) {
+#define MA_CASE(G_, P_, V_) \
+        case dtype_key(G_, P_, V_): return launch_k<K<4, LPB, G_, P_, V_, REP>>(a, nblocks, s);
+        MA_FAST_DTYPES(MA_CASE)
+#undef MA_CASE
         default: return cudaErrorInvalidConfiguration;
+    }
+}
+
+template <bool REP>
+cudaError_t launch_rep(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
+    switch (a.bucket) {
+        case 16: return launch_dt<2, REP>(a, nblocks, s);
+        case 32: return launch_dt<4, REP>(a, nblocks, s);
+        case 64: return launch_dt<8, REP>(a, nblocks, s);
+        default: return cudaErrorInvalidConfiguration;
+    }
+}
+
+bool fast_dtypes(int g, int p, int v) {
+    switch (dtype_key(g, p, v)) {
+#define MA_CASE(G_, P_, V_) case dtype_key(G_, P_, V_): return true;
+        MA_FAST_DTYPES(MA_CASE)
+#undef MA_CASE
+        default: return false;
     }
 }
 
 }  // namespace
 
-// Fast path: B_q in {16, 32, 64}; B_d in {1024, 2048, 4096}; m <= 127.
-Variant pick_fast_variant(int block, int bucket, int m, int kb_stride) {
+// Fast path: B_d = 4096, B_q in {16, 32, 64}, m <= 127, and an instantiated
+// dtype combo (MA_FAST_DTYPES).
+Variant pick_fast_variant(int block, int bucket, int m, int kb_stride, int g_dtype, int p_dtype,
+                          int v_dtype) {
     if (bucket != 16 && bucket != 32 && bucket != 64) return {0, 0};
-    if (block != 1024 && block != 2048 && block != 4096) return {0, 0};
+    if (block != 4096 || !fast_dtypes(g_dtype, p_dtype, v_dtype)) return {0, 0};
     if (m > kMaxRowsFast || m * kb_stride > 32768) return {0, 0};
     return {kNT, block / kNT};
 }
@@ -579,12 +647,8 @@ cudaError_t launch_step_fast(const StepArgs& a, Variant v, int grid, cudaStream_
     (void)grid;
     (void)v;
     if (a.block_count <= 0) return cudaSuccess;
-    switch (a.bucket) {
-        case 16: return launch_lpb<2>(a, a.block_count, s);
-        case 32: return launch_lpb<4>(a, a.block_count, s);
-        case 64: return launch_lpb<8>(a, a.block_count, s);
-        default: return cudaErrorInvalidConfiguration;
-    }
+    if (a.block_count > 0x7FFFFFFFll) return cudaErrorInvalidConfiguration;
+    return a.partials ? launch_rep<true>(a, a.block_count, s) : launch_rep<false>(a, a.block_count, s);
 }
 
 }  // namespace ma

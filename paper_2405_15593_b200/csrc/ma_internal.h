@@ -53,7 +53,8 @@ cudaError_t launch_step(const StepArgs& a, Variant v, int64_t nblocks, cudaStrea
 
 // Fast persistent kernel (ma_fast.cu): full blocks only; B_q in {16, 32, 64},
 // B_d in {1024, 2048, 4096, 8192}, m*kb_stride <= 65535. ept = 8 * groups per thread.
-Variant pick_fast_variant(int block, int bucket, int m, int kb_stride);
+Variant pick_fast_variant(int block, int bucket, int m, int kb_stride, int g_dtype, int p_dtype,
+                          int v_dtype);
 size_t fast_smem_bytes(Variant v, int block, int bucket, int m, int kb_stride, int g_dtype,
                        int p_dtype, int v_dtype);
 int fast_blocks_per_sm(Variant v, int bucket, size_t smem);
