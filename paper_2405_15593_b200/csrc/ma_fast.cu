@@ -98,6 +98,25 @@ struct Ctx {
     int block, bucket, nwords, kb, m, kbs, slot;
 };
 
+template <class KT>
+__device__ __forceinline__ Ctx make_ctx(const StepArgs& p) {
+    extern __shared__ __align__(128) unsigned char smem_dyn[];
+    Ctx c;
+    c.p = &p;
+    c.smem = smem_dyn;
+    c.block = KT::BLOCK;
+    c.bucket = KT::BUCKET;
+    c.nwords = KT::BLOCK / 32;
+    c.m = p.m;
+    c.kbs = p.kb_stride;
+    c.kb = p.per_block_k;
+    c.slot = p.slot;
+    c.L = Layout4(KT::BLOCK, KT::BUCKET, p.m, p.kb_stride, KT::PDT, KT::VDT);
+    c.b = p.block_offset + blockIdx.x;
+    c.base = c.b * KT::BLOCK;
+    return c;
+}
+
 // 8 consecutive g values (element e0, 8-aligned) as doubles.
 template <int DT>
 __device__ __forceinline__ void load_g8(const void* g, int64_t e0, double (&x)[8]) {
@@ -175,20 +194,12 @@ __device__ __noinline__ int tie_rank_hi(const double* cval, const uint32_t* ckhi
     return extra;
 }
 
-// The IEEE path of quantize_nearest (quantize.cpp:51-53) for the elements
-// whose fast fixed-point code fell in the guard band. Out of line: rare.
-__device__ __noinline__ uint32_t exact_codes(const double (&a)[8], double lo, double rng,
-                                             uint32_t bad, uint32_t word) {
-    const double level = __ddiv_rn(rng, 15.0);
-#pragma unroll 1
-    for (int i = 0; i < 8; ++i) {
-        if (!((bad >> i) & 1u)) continue;
-        double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(a[i], lo), level), 0.5));
-        f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
-        word = (word & ~(15u << (4 * i))) | (static_cast<uint32_t>(f) << (4 * i));
-    }
-    return word;
-}
+// The IEEE path of quantize_nearest (quantize.cpp:51-53) for the elements of
+// the 8-group at e0 whose fast fixed-point code fell in the guard band; the
+// residual is recomputed (selected -> 0). Out of line: rare.
+template <class KT>
+__device__ __noinline__ uint32_t exact_codes(const StepArgs* pp, int e0, uint32_t sel8, double lo,
+                                             double rng, uint32_t bad, uint32_t word);
 
 __device__ __forceinline__ void word_prefix(const uint32_t* bits, int nwords, int* pref) {
     const int lane = threadIdx.x & 31;
@@ -213,6 +224,22 @@ __device__ __forceinline__ void wait_stage(uint64_t* bar) {
     }
 }
 
+template <class KT>
+__device__ __noinline__ uint32_t exact_codes(const StepArgs* pp, int e0, uint32_t sel8, double lo,
+                                             double rng, uint32_t bad, uint32_t word) {
+    const Ctx c = make_ctx<KT>(*pp);
+    const double level = __ddiv_rn(rng, 15.0);
+#pragma unroll 1
+    for (int i = 0; i < 8; ++i) {
+        if (!((bad >> i) & 1u)) continue;
+        const double x = ((sel8 >> i) & 1u) ? 0.0 : recompute_a<KT>(c, e0 + i);
+        double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(x, lo), level), 0.5));
+        f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+        word = (word & ~(15u << (4 * i))) | (static_cast<uint32_t>(f) << (4 * i));
+    }
+    return word;
+}
+
 // Selected element e (value a) -> window row `slot` at its ascending position
 // (window.cpp:14-26): global ring, the staged rows, and its owner mark.
 template <class KT>
@@ -235,7 +262,8 @@ __device__ __forceinline__ void emit_selected(const Ctx& c, int e, double a) {
 // the (L2-hot) inputs. Sets the selection bitmap + prefix, emits the new row
 // and misc[1] = next threshold.
 template <class KT>
-__device__ __noinline__ void fallback_select(const Ctx& c) {
+__device__ __noinline__ void fallback_select(const StepArgs* pp) {
+    const Ctx c = make_ctx<KT>(*pp);
     unsigned char* sm = c.smem;
     uint32_t* s_sel = reinterpret_cast<uint32_t*>(sm + c.L.sel);
     uint32_t* s_tmpb = reinterpret_cast<uint32_t*>(sm + c.L.tmpb);
@@ -304,19 +332,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     constexpr int G = KT::G, LPB = KT::LPB, BUCKET = KT::BUCKET, BLOCK = KT::BLOCK;
     static_assert(8 * G <= kEPT, "candidate masks are 32-bit");
     extern __shared__ __align__(128) unsigned char smem[];
-    Ctx c;
-    c.p = &p;
-    c.smem = smem;
-    c.block = BLOCK;
-    c.bucket = BUCKET;
-    c.nwords = BLOCK / 32;
-    c.m = p.m;
-    c.kbs = p.kb_stride;
-    c.kb = p.per_block_k;
-    c.slot = p.slot;
-    c.L = Layout4(BLOCK, BUCKET, p.m, p.kb_stride, KT::PDT, KT::VDT);
-    c.b = p.block_offset + blockIdx.x;
-    c.base = c.b * BLOCK;
+    const Ctx c = make_ctx<KT>(p);
     const Layout4& L = c.L;
     unsigned char* sth = smem + L.theta;
     int16_t* swi = reinterpret_cast<int16_t*>(smem + L.widx);
@@ -433,7 +449,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
             if ((s_sel[e >> 5] >> (e & 31)) & 1u) emit_selected<KT>(c, e, s_cval[t]);
         }
     } else {
-        fallback_select<KT>(c);
+        fallback_select<KT>(&p);
     }
     if (tid == 0) p.thresh[b] = static_cast<uint32_t>(s_misc[1]);
 
@@ -480,7 +496,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
                 word |= (xq >> 20) << (4 * i);
                 bad |= static_cast<uint32_t>(((xq + kGuard) & 0xFFFFFu) < 2 * kGuard) << i;
             }
-            if (bad) word = exact_codes(a, lo, rng, bad, word);  // rare: guard band
+            if (bad) word = exact_codes<KT>(&p, e0, sel8, lo, rng, bad, word);  // rare: guard band
         }
         if (want_report) {
             const double level = rng == 0.0 ? 0.0 : __ddiv_rn(rng, 15.0);
