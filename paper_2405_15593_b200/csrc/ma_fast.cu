@@ -16,13 +16,16 @@
 //    are computed once per block into smem.
 //  * P1 decodes a = g + e only for the Top-K keys; P3 recomputes a (an
 //    L2-hot re-read of g and the codes) instead of holding 32 doubles/thread.
-//  * Block Top-K fast path: each block carries a 32-bit threshold on the high
-//    word of |a| (≈ the kTarget-th largest key of the previous step). The
-//    candidates above it are ranked exactly by (|a| desc, index asc) — high
-//    word first, full key and index only on ties — so the selection is always
-//    exact; the threshold only decides the work. Outside [k_b, kCandCap]
-//    candidates an out-of-line exact radix select runs. Selected elements get
-//    their ascending window position from a word prefix of a selection bitmap.
+//  * Block Top-K: P1 keeps a 16-bit key (bits 62..48 of |a|) per element in
+//    registers. A threshold t with k_b <= #{key16 >= t} <= cap is taken from
+//    the previous step (≈ the kTarget-th largest key, carried per block) or
+//    found by bisection on block-wide counts (SIMD __vcmpgeu2 + popc, one
+//    barrier per probe). The candidates above t are ranked exactly by
+//    (|a| desc, index asc) — high word first, full key and index only on ties
+//    — so the selection is always exact; t only decides the work. Only when
+//    more than `cap` keys tie at 16-bit resolution does an out-of-line exact
+//    radix select run. Selected elements get their ascending window position
+//    from a word prefix of a selection bitmap.
 //  * ADAM_STATS with no per-row barrier: every window coordinate gets one
 //    owner row (last-writer-wins byte + duplicate bit). Coordinates present in
 //    one row take z = 0 + w·v; duplicated ones are re-summed by the owner in
@@ -50,12 +53,18 @@ constexpr int kTarget = 56;       // candidate rank that seeds the next step's t
 constexpr uint32_t kGuard = 64;   // fixed-point guard band (units of 2^-20)
 constexpr int kMaxRowsFast = 127; // owner byte holds the row (7 bits) + a duplicate bit
 
+// Candidate capacity of the exact-rank stage: 2 k_b, at least 128, at most 512.
+__host__ __device__ inline int cand_cap(int kb) {
+    const int c = ((2 * kb + 3) / 4) * 4;
+    return c < 128 ? 128 : (c > 512 ? 512 : c);
+}
+
 // Shared-memory carve-up (host and device agree).
 struct Layout4 {
     uint32_t theta, widx, wval, lo, lvl, cval, red, bar, owner, selm, ckhi, cidx, sel, tmpb, wpref,
         hist, misc, ckey, total;
     __host__ __device__ Layout4() {}
-    __host__ __device__ Layout4(int block, int bucket, int m, int kbs, int pdt, int vdt) {
+    __host__ __device__ Layout4(int block, int bucket, int m, int kbs, int pdt, int vdt, int cap) {
         const size_t ent = size_t(m) * size_t(kbs);
         const size_t nbk = size_t(block / bucket);
         const size_t nwords = size_t(block / 32);
@@ -65,14 +74,14 @@ struct Layout4 {
         wval = uint32_t(o);  o = align_up(o + ent * dtype_bytes(vdt), 128);
         lo = uint32_t(o);    o = align_up(o + nbk * 8, 16);
         lvl = uint32_t(o);   o = align_up(o + nbk * 8, 16);
-        cval = uint32_t(o);  o = align_up(o + size_t(kCandCap + 4) * 8, 16);
-        ckey = uint32_t(o);  o = align_up(o + size_t(kCandCap + 4) * 8, 16);
+        cval = uint32_t(o);  o = align_up(o + size_t(cap + 4) * 8, 16);
+        ckey = uint32_t(o);  o = align_up(o + size_t(cap + 4) * 8, 16);
         red = uint32_t(o);   o = align_up(o + size_t(kNT / 32) * kReportFields * 8, 16);
         bar = uint32_t(o);   o = align_up(o + 16, 16);
         owner = uint32_t(o); o = align_up(o + size_t(block), 16);
         selm = uint32_t(o);  o = align_up(o + size_t(block), 16);
-        ckhi = uint32_t(o);  o = align_up(o + size_t(kCandCap + 4) * 4, 16);
-        cidx = uint32_t(o);  o = align_up(o + size_t(kCandCap + 4) * 4, 16);
+        ckhi = uint32_t(o);  o = align_up(o + size_t(cap + 4) * 4, 16);
+        cidx = uint32_t(o);  o = align_up(o + size_t(cap + 4) * 4, 16);
         sel = uint32_t(o);   o = align_up(o + nwords * 4, 16);
         tmpb = uint32_t(o);  o = align_up(o + nwords * 4, 16);
         wpref = uint32_t(o); o = align_up(o + (nwords + 1) * 4, 16);
@@ -111,7 +120,7 @@ __device__ __forceinline__ Ctx make_ctx(const StepArgs& p) {
     c.kbs = p.kb_stride;
     c.kb = p.per_block_k;
     c.slot = p.slot;
-    c.L = Layout4(KT::BLOCK, KT::BUCKET, p.m, p.kb_stride, KT::PDT, KT::VDT);
+    c.L = Layout4(KT::BLOCK, KT::BUCKET, p.m, p.kb_stride, KT::PDT, KT::VDT, cand_cap(p.per_block_k));
     c.b = p.block_offset + blockIdx.x;
     c.base = c.b * KT::BLOCK;
     return c;
@@ -257,8 +266,8 @@ __device__ __forceinline__ void emit_selected(const Ctx& c, int e, double a) {
     (c.smem + c.L.owner)[e] = static_cast<uint8_t>(c.slot);
 }
 
-// Exact fallback selection (compress.cpp:39-53) for blocks whose candidate
-// count left [k_b, kCandCap]: the generic radix select on a recomputed from
+// Exact fallback selection (compress.cpp:39-53) for blocks where more than
+// `cap` keys tie at 16-bit resolution: the generic radix select on a recomputed from
 // the (L2-hot) inputs. Sets the selection bitmap + prefix, emits the new row
 // and misc[1] = next threshold.
 template <class KT>
@@ -321,8 +330,8 @@ __device__ __noinline__ void fallback_select(const StepArgs* pp) {
     for (int s = 0; s < kEPT; ++s)
         if ((sel >> s) & 1u) emit_selected<KT>(c, elem(s), a[s]);
     if (tid == 0) {
-        const uint32_t km = static_cast<uint32_t>(s_misc[2]);
-        s_misc[1] = static_cast<int>(km > (1u << 15) ? km - (1u << 15) : 1u);
+        const uint32_t km = static_cast<uint32_t>(s_misc[2]) >> 16;
+        s_misc[1] = static_cast<int>(km > 1 ? km - 1 : 1u);
     }
 }
 
@@ -354,6 +363,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
     const int kb = c.kb, kbs = c.kbs, slot = c.slot, filled = p.filled, m = c.m;
     const int nent = filled * kb;
+    const int cap = cand_cap(kb);
     const float inv_kb = 1.0f / static_cast<float>(kb);
     const int64_t b = c.b, base = c.base;
     constexpr bool want_report = KT::REPORT;
@@ -383,42 +393,109 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     }
     __syncthreads();  // [L]
 
-    // ---- P1: a = g + decode(EF); keys above T become Top-K candidates ----
+    // ---- P1: a = g + decode(EF) -> 16-bit Top-K keys: bits 62..48 of |a|
+    //      (exponent + 4 mantissa bits), two per register ----
+    uint32_t k16[4 * G];
     uint32_t kmax = 0;
     double rep[kReportFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 1
+#pragma unroll
     for (int g = 0; g < G; ++g) {
-        const int e0 = (g * kNT + tid) * 8;
         double a[8];
-        decode8<KT>(c, e0, a);
-        uint32_t m8 = 0;
+        decode8<KT>(c, (g * kNT + tid) * 8, a);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const uint32_t kh = hi_key(a[i]);
-            kmax = max(kmax, kh);
-            m8 |= static_cast<uint32_t>(kh >= T) << i;
-            if (want_report) rep[1] += a[i] * a[i];
+        for (int i = 0; i < 8; i += 2) {
+            const uint32_t h0 = hi_key(a[i]) >> 16, h1 = hi_key(a[i + 1]) >> 16;
+            k16[g * 4 + i / 2] = h0 | (h1 << 16);
+            kmax = max(kmax, max(h0, h1));
+            if (want_report) rep[1] += a[i] * a[i] + a[i + 1] * a[i + 1];
         }
-        if (m8) {
-            int s0 = atomicAdd(&s_misc[NW], __popc(m8));
+    }
+    if (p.check_finite && kmax >= 0x7FF0u) atomicOr(p.flag, 1u);  // inf/NaN in g or a
+
+    // ---- P2: block Top-K (compress.cpp:39-53, 73-85). Find a 16-bit threshold t
+    //      with k_b <= #{key16 >= t} <= cap (carried from the previous step, else
+    //      bisection on block-wide counts), then rank those candidates exactly. ----
+    int* s_cnt = s_misc + 64;  // [2][NW] per-warp counts, double-buffered
+    auto block_count = [&](uint32_t t, int par) -> int {
+        const uint32_t tt = t | (t << 16);
+        int n = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (!((m8 >> i) & 1u)) continue;
-                if (s0 < kCandCap) {
+        for (int k = 0; k < 4 * G; ++k) n += __popc(__vcmpgeu2(k16[k], tt));
+        n = __reduce_add_sync(0xFFFFFFFFu, n >> 4);
+        if (lane == 0) s_cnt[par * NW + warp] = n;
+        __syncthreads();
+        int tot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) tot += s_cnt[par * NW + w];
+        return tot;
+    };
+    const uint32_t wmax = __reduce_max_sync(0xFFFFFFFFu, kmax);
+    if (lane == 0) s_misc[48 + warp] = static_cast<int>(wmax);
+    const uint32_t carried = __ldg(p.thresh + b);
+    int par = 0;
+    int cnt0 = block_count(carried, par);  // [A0] also publishes the warp maxima
+    uint32_t bmax = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) bmax = max(bmax, static_cast<uint32_t>(s_misc[48 + w]));
+    uint32_t t16 = carried;
+    bool found = carried != 0 && cnt0 >= kb && cnt0 <= cap;
+    if (!found) {
+        uint32_t lo = 0, hi = bmax + 1, mid;  // invariant: count(lo) >= kb > count(hi)
+        if (carried == 0) {
+            mid = bmax >= 8 ? bmax - 8 : bmax / 2;  // ~half a binade below the block max
+        } else if (cnt0 > cap) {
+            lo = carried;
+            mid = (lo + hi) / 2;
+        } else {
+            hi = carried;
+            mid = carried > 8 ? carried - 8 : carried / 2;
+        }
+        while (hi - lo > 1) {
+            if (mid <= lo || mid >= hi) mid = (lo + hi) / 2;
+            par ^= 1;
+            const int n = block_count(mid, par);
+            if (n > cap) {
+                lo = mid;
+            } else if (n < kb) {
+                hi = mid;
+            } else {
+                found = true;
+                t16 = mid;
+                break;
+            }
+            mid = (lo + hi) / 2;
+        }
+    }
+    if (tid == 0) s_misc[NW] = 0;
+    __syncthreads();  // candidate counter reset visible
+    if (found) {
+        // Collect the candidates (a recomputed for groups that hold one).
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            uint32_t m8 = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t w = k16[g * 4 + k];
+                m8 |= static_cast<uint32_t>((w & 0xFFFFu) >= t16) << (2 * k);
+                m8 |= static_cast<uint32_t>((w >> 16) >= t16) << (2 * k + 1);
+            }
+            if (m8) {
+                const int e0 = (g * kNT + tid) * 8;
+                double a[8];
+                decode8<KT>(c, e0, a);
+                int s0 = atomicAdd(&s_misc[NW], __popc(m8));
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (!((m8 >> i) & 1u)) continue;
                     s_cval[s0] = a[i];
                     s_ckhi[s0] = hi_key(a[i]);
                     s_cidx[s0] = e0 + i;
+                    ++s0;
                 }
-                ++s0;
             }
         }
-    }
-    if (p.check_finite && kmax >= 0x7FF00000u) atomicOr(p.flag, 1u);  // inf/NaN in g or a
-    __syncthreads();  // [A] candidates
-
-    // ---- P2: block Top-K (compress.cpp:39-53, 73-85) ----
-    const int ncand = s_misc[NW];
-    if (ncand >= kb && ncand <= kCandCap) {
+        __syncthreads();  // [A] candidates
+        const int ncand = s_misc[NW];
         const int target = (ncand > kTarget ? kTarget : ncand) - 1;
         const int n4 = ncand & ~3;
         for (int t = tid; t < ncand; t += kNT) {
@@ -437,8 +514,10 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
             int rank = above;
             if (eq > 1) rank += tie_rank_hi(s_cval, s_ckhi, s_cidx, ncand, t);
             if (rank < kb) atomicOr(&s_sel[s_cidx[t] >> 5], 1u << (s_cidx[t] & 31));
-            if (rank == target)
-                s_misc[1] = static_cast<int>(ncand > kTarget ? kh : (kh > (1u << 15) ? kh - (1u << 15) : 1u));
+            if (rank == target) {
+                const uint32_t h = kh >> 16;  // next step's threshold
+                s_misc[1] = static_cast<int>(ncand > kTarget ? h : (h > 1 ? h - 1 : 1u));
+            }
         }
         __syncthreads();  // [B] selection bitmap
         if (warp == 0) word_prefix(s_sel, BLOCK / 32, s_wpref);
@@ -449,7 +528,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
             if ((s_sel[e >> 5] >> (e & 31)) & 1u) emit_selected<KT>(c, e, s_cval[t]);
         }
     } else {
-        fallback_select<KT>(&p);
+        fallback_select<KT>(&p);  // more than `cap` keys tie at 16-bit resolution
     }
     if (tid == 0) p.thresh[b] = static_cast<uint32_t>(s_misc[1]);
 
@@ -584,7 +663,8 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
 
 template <class KT>
 cudaError_t launch_k(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
-    const size_t smem = Layout4(KT::BLOCK, KT::BUCKET, a.m, a.kb_stride, KT::PDT, KT::VDT).total;
+    const size_t smem =
+        Layout4(KT::BLOCK, KT::BUCKET, a.m, a.kb_stride, KT::PDT, KT::VDT, cand_cap(a.per_block_k)).total;
     auto k = microadam_step_fast<KT>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem));
@@ -649,7 +729,8 @@ size_t fast_smem_bytes(Variant v, int block, int bucket, int m, int kb_stride, i
                        int p_dtype, int v_dtype) {
     (void)v;
     (void)g_dtype;
-    return Layout4(block, bucket, m, kb_stride, p_dtype, v_dtype).total;
+    const int kb = kb_stride;  // upper bound of per_block_k (kb_stride = round_up(k_b, 8))
+    return Layout4(block, bucket, m, kb_stride, p_dtype, v_dtype, cand_cap(kb)).total;
 }
 
 int fast_blocks_per_sm(Variant v, int bucket, size_t smem) {

@@ -1,0 +1,32 @@
+#!/usr/bin/env python
+"""Time the fused step at several vector sizes (diagnostic, not a bench line)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2405_15593_b200 as ma  # noqa: E402
+
+sizes = [int(float(x)) for x in (sys.argv[1:] or ["1.1e8", "4.4e8", "1.3e9", "3e9", "6.738415616e9"])]
+L = ma.lib()
+s = torch.cuda.current_stream().cuda_stream
+for d in sizes:
+    eng = ma.MicroAdam(d, dict(), param_dtype="bf16", grad_dtype="bf16", value_dtype="bf16")
+    p = torch.empty(d, dtype=torch.bfloat16, device="cuda")
+    g = torch.empty(d, dtype=torch.bfloat16, device="cuda")
+    ma._capi.check(L.ma_fill_synthetic(p.data_ptr(), 2, d, 1, 0, 0, 0, s))
+    times = []
+    for i in range(12):
+        ma._capi.check(L.ma_fill_synthetic(g.data_ptr(), 2, d, 42, i + 1, 0, 0, s))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        eng.step(p, g, 1e-3)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    t = sorted(times[6:])[len(times[6:]) // 2]
+    print(f"d={d:>12,}  step {t:9.3f} ms  {d / t / 1e6:8.3f} Gparam/s  {7.9 * d / t / 1e6:8.1f} GB/s  "
+          f"steps: {' '.join(f'{x:.2f}' for x in times)}", flush=True)
+    del eng, p, g
+    torch.cuda.empty_cache()
