@@ -181,6 +181,12 @@ MA_API ma_status ma_get_layout(const ma_handle* h, ma_layout_info* out);
 /* Number of step-kernel launches issued so far by this handle (all kernels). */
 MA_API int64_t ma_kernel_launches(const ma_handle* h);
 
+/* Diagnostics of the fast kernel, collected only when the handle was created
+ * with MA_DEBUG_COUNTERS=1 in the environment (else zeros): out[0] blocks that
+ * took the exact radix-select fallback, out[1] elements quantized through the
+ * IEEE-division path, out[2] Top-K threshold bisection probes. */
+MA_API ma_status ma_debug_counters(ma_handle* h, int64_t* out, int n);
+
 MA_API const char* ma_last_error(void);
 MA_API const char* ma_version(void);
 

@@ -25,7 +25,7 @@ EXPORTED = [
     "ma_config_default", "ma_validate", "ma_layout", "ma_create", "ma_create_shard", "ma_destroy",
     "ma_step", "ma_step_host", "ma_sync", "ma_get_counters", "ma_read_error_buffer",
     "ma_read_window_row", "ma_write_state", "ma_set_params", "ma_get_layout",
-    "ma_kernel_launches", "ma_last_error", "ma_version", "ma_fill_synthetic",
+    "ma_kernel_launches", "ma_last_error", "ma_version", "ma_fill_synthetic", "ma_debug_counters",
 ]
 
 
@@ -98,6 +98,7 @@ def lib():
     L.ma_get_layout.argtypes = [vp, P(Layout)]
     L.ma_kernel_launches.argtypes = [vp]
     L.ma_kernel_launches.restype = C.c_int64
+    L.ma_debug_counters.argtypes = [vp, P(C.c_int64), C.c_int]
     L.ma_last_error.restype = C.c_char_p
     L.ma_last_error.argtypes = []
     L.ma_version.restype = C.c_char_p

@@ -167,6 +167,7 @@ struct ma_handle {
     double* d_partials = nullptr;
     double* d_report = nullptr;
     uint32_t* d_thresh = nullptr;
+    unsigned int* d_dbg = nullptr;  // diagnostics counters (MA_DEBUG_COUNTERS=1)
     // host counters (window.hpp:10-33)
     int64_t step = 0, head = 0, filled = 0;
     std::vector<int64_t> stamps;
@@ -205,6 +206,7 @@ void free_handle(ma_handle* h) {
     cudaFree(h->d_partials);
     cudaFree(h->d_report);
     cudaFree(h->d_thresh);
+    cudaFree(h->d_dbg);
     cudaFree(h->d_theta);
     cudaFree(h->d_gstage);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
@@ -242,6 +244,7 @@ void base_args(ma_handle* h, ma::StepArgs* a) {
     a->win_val = h->d_win_val;
     a->flag = h->d_flag;
     a->thresh = h->d_thresh;
+    a->dbg = h->d_dbg;
     a->dim = s.dim;
     a->num_blocks = s.b1 - s.b0;
     a->block = static_cast<int32_t>(s.block);
@@ -430,6 +433,8 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     alloc(reinterpret_cast<void**>(&h->d_partials), size_t(nb) * ma::kReportFields * sizeof(double));
     alloc(reinterpret_cast<void**>(&h->d_report), ma::kReportFields * sizeof(double));
     alloc(reinterpret_cast<void**>(&h->d_thresh), size_t(nb) * sizeof(uint32_t));
+    const char* dbg = std::getenv("MA_DEBUG_COUNTERS");
+    if (dbg && dbg[0] == '1') alloc(reinterpret_cast<void**>(&h->d_dbg), 4 * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         free_handle(h);
@@ -676,6 +681,18 @@ ma_status ma_get_layout(const ma_handle* h, ma_layout_info* out) {
 }
 
 int64_t ma_kernel_launches(const ma_handle* h) { return h ? h->launches : 0; }
+
+ma_status ma_debug_counters(ma_handle* h, int64_t* out, int n) {
+    if (!h || !out || n < 0) return fail(MA_ERR_INVALID_ARG, "bad argument");
+    DeviceGuard g(h->device);
+    unsigned v[4] = {0, 0, 0, 0};
+    if (h->d_dbg) {
+        MA_CUDA(cudaDeviceSynchronize());
+        MA_CUDA(cudaMemcpy(v, h->d_dbg, sizeof(v), cudaMemcpyDeviceToHost));
+    }
+    for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
+    return MA_OK;
+}
 
 const char* ma_last_error(void) { return g_last_error.c_str(); }
 

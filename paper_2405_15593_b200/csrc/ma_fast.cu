@@ -203,12 +203,14 @@ __device__ __noinline__ int tie_rank_hi(const double* cval, const uint32_t* ckhi
     return extra;
 }
 
-// The IEEE path of quantize_nearest (quantize.cpp:51-53) for the elements of
-// the 8-group at e0 whose fast fixed-point code fell in the guard band; the
-// residual is recomputed (selected -> 0). Out of line: rare.
-template <class KT>
-__device__ __noinline__ uint32_t exact_codes(const StepArgs* pp, int e0, uint32_t sel8, double lo,
-                                             double rng, uint32_t bad, uint32_t word);
+// The IEEE path of quantize_nearest (quantize.cpp:51-53): the code of x in a
+// bucket with grid (lo, level), for elements whose fast fixed-point estimate
+// fell in the guard band. Out of line: rare, and scalar arguments only.
+__device__ __noinline__ uint32_t exact_code(double x, double lo, double level) {
+    double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(x, lo), level), 0.5));
+    f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+    return static_cast<uint32_t>(f);
+}
 
 __device__ __forceinline__ void word_prefix(const uint32_t* bits, int nwords, int* pref) {
     const int lane = threadIdx.x & 31;
@@ -231,22 +233,6 @@ __device__ __forceinline__ void word_prefix(const uint32_t* bits, int nwords, in
 __device__ __forceinline__ void wait_stage(uint64_t* bar) {
     while (!mbar_try_wait(bar, 0)) {
     }
-}
-
-template <class KT>
-__device__ __noinline__ uint32_t exact_codes(const StepArgs* pp, int e0, uint32_t sel8, double lo,
-                                             double rng, uint32_t bad, uint32_t word) {
-    const Ctx c = make_ctx<KT>(*pp);
-    const double level = __ddiv_rn(rng, 15.0);
-#pragma unroll 1
-    for (int i = 0; i < 8; ++i) {
-        if (!((bad >> i) & 1u)) continue;
-        const double x = ((sel8 >> i) & 1u) ? 0.0 : recompute_a<KT>(c, e0 + i);
-        double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(x, lo), level), 0.5));
-        f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
-        word = (word & ~(15u << (4 * i))) | (static_cast<uint32_t>(f) << (4 * i));
-    }
-    return word;
 }
 
 // Selected element e (value a) -> window row `slot` at its ascending position
@@ -454,6 +440,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
             if (mid <= lo || mid >= hi) mid = (lo + hi) / 2;
             par ^= 1;
             const int n = block_count(mid, par);
+            if (p.dbg && tid == 0) atomicAdd(p.dbg + 2, 1u);
             if (n > cap) {
                 lo = mid;
             } else if (n < kb) {
@@ -529,6 +516,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
         }
     } else {
         fallback_select<KT>(&p);  // more than `cap` keys tie at 16-bit resolution
+        if (p.dbg && tid == 0) atomicAdd(p.dbg + 0, 1u);
     }
     if (tid == 0) p.thresh[b] = static_cast<uint32_t>(s_misc[1]);
 
@@ -575,7 +563,14 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
                 word |= (xq >> 20) << (4 * i);
                 bad |= static_cast<uint32_t>(((xq + kGuard) & 0xFFFFFu) < 2 * kGuard) << i;
             }
-            if (bad) word = exact_codes<KT>(&p, e0, sel8, lo, rng, bad, word);  // rare: guard band
+            if (bad) {  // rare: guard band -> the exact quotient
+                const double level = __ddiv_rn(rng, 15.0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if ((bad >> i) & 1u)
+                        word = (word & ~(15u << (4 * i))) | (exact_code(a[i], lo, level) << (4 * i));
+                if (p.dbg) atomicAdd(p.dbg + 1, __popc(bad));
+            }
         }
         if (want_report) {
             const double level = rng == 0.0 ? 0.0 : __ddiv_rn(rng, 15.0);

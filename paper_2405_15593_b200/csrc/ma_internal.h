@@ -27,6 +27,8 @@ struct StepArgs {
     unsigned int* flag;
     double* partials; // nullable: [num_blocks][kReportFields]
     uint32_t* thresh; // [num_blocks] Top-K fast-path threshold carried across steps (fast kernel)
+    unsigned int* dbg;  // nullable diagnostics: [0] exact-select fallbacks, [1] exact-quotient
+                        // elements, [2] threshold bisection probes (fast kernel)
     int64_t dim;
     int64_t num_blocks;
     int64_t block_offset;

@@ -26,7 +26,8 @@ for d in sizes:
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
     t = sorted(times[6:])[len(times[6:]) // 2]
+    dbg = eng.debug_counters() if os.environ.get("MA_DEBUG_COUNTERS") == "1" else {}
     print(f"d={d:>12,}  step {t:9.3f} ms  {d / t / 1e6:8.3f} Gparam/s  {7.9 * d / t / 1e6:8.1f} GB/s  "
-          f"steps: {' '.join(f'{x:.2f}' for x in times)}", flush=True)
+          f"steps: {' '.join(f'{x:.2f}' for x in times)} {dbg}", flush=True)
     del eng, p, g
     torch.cuda.empty_cache()
