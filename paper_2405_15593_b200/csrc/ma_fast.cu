@@ -62,7 +62,7 @@ __host__ __device__ inline int cand_cap(int kb) {
 // Shared-memory carve-up (host and device agree).
 struct Layout4 {
     uint32_t theta, widx, wval, lo, lvl, cval, red, bar, owner, selm, ckhi, cidx, sel, tmpb, wpref,
-        hist, misc, ckey, total;
+        hist, misc, ckey, k16, total;
     __host__ __device__ Layout4() {}
     __host__ __device__ Layout4(int block, int bucket, int m, int kbs, int pdt, int vdt, int cap) {
         const size_t ent = size_t(m) * size_t(kbs);
@@ -78,8 +78,9 @@ struct Layout4 {
         ckey = uint32_t(o);  o = align_up(o + size_t(cap + 4) * 8, 16);
         red = uint32_t(o);   o = align_up(o + size_t(kNT / 32) * kReportFields * 8, 16);
         bar = uint32_t(o);   o = align_up(o + 16, 16);
+        k16 = uint32_t(o);   o = align_up(o + size_t(block) * 2, 16);
         owner = uint32_t(o); o = align_up(o + size_t(block), 16);
-        selm = uint32_t(o);  o = align_up(o + size_t(block), 16);
+        selm = owner;  // fallback scratch; owner marks are written after the selection
         ckhi = uint32_t(o);  o = align_up(o + size_t(cap + 4) * 4, 16);
         cidx = uint32_t(o);  o = align_up(o + size_t(cap + 4) * 4, 16);
         sel = uint32_t(o);   o = align_up(o + nwords * 4, 16);
@@ -379,21 +380,31 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     }
     __syncthreads();  // [L]
 
-    // ---- P1: a = g + decode(EF) -> 16-bit Top-K keys: bits 62..48 of |a|
-    //      (exponent + 4 mantissa bits), two per register ----
-    uint32_t k16[4 * G];
+    // ---- P1: a = g + decode(EF) -> 16-bit Top-K keys (bits 62..48 of |a|:
+    //      exponent + 4 mantissa bits) in smem, counted against the carried
+    //      threshold on the fly ----
+    uint16_t* s_k16 = reinterpret_cast<uint16_t*>(smem + L.k16);
+    const uint32_t carried = __ldg(p.thresh + b);
     uint32_t kmax = 0;
+    int cnt0 = 0;
     double rep[kReportFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    {
+        const uint32_t tt = carried | (carried << 16);
+#pragma unroll 1
+        for (int g = 0; g < G; ++g) {
+            const int e0 = (g * kNT + tid) * 8;
+            double a[8];
+            decode8<KT>(c, e0, a);
+            uint32_t w[4];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        double a[8];
-        decode8<KT>(c, (g * kNT + tid) * 8, a);
-#pragma unroll
-        for (int i = 0; i < 8; i += 2) {
-            const uint32_t h0 = hi_key(a[i]) >> 16, h1 = hi_key(a[i + 1]) >> 16;
-            k16[g * 4 + i / 2] = h0 | (h1 << 16);
-            kmax = max(kmax, max(h0, h1));
-            if (want_report) rep[1] += a[i] * a[i] + a[i + 1] * a[i + 1];
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t h0 = hi_key(a[2 * k]) >> 16, h1 = hi_key(a[2 * k + 1]) >> 16;
+                w[k] = h0 | (h1 << 16);
+                kmax = max(kmax, max(h0, h1));
+                cnt0 += __popc(__vcmpgeu2(w[k], tt));
+                if (want_report) rep[1] += a[2 * k] * a[2 * k] + a[2 * k + 1] * a[2 * k + 1];
+            }
+            *reinterpret_cast<uint4*>(s_k16 + e0) = make_uint4(w[0], w[1], w[2], w[3]);
         }
     }
     if (p.check_finite && kmax >= 0x7FF0u) atomicOr(p.flag, 1u);  // inf/NaN in g or a
@@ -402,11 +413,7 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     //      with k_b <= #{key16 >= t} <= cap (carried from the previous step, else
     //      bisection on block-wide counts), then rank those candidates exactly. ----
     int* s_cnt = s_misc + 64;  // [2][NW] per-warp counts, double-buffered
-    auto block_count = [&](uint32_t t, int par) -> int {
-        const uint32_t tt = t | (t << 16);
-        int n = 0;
-#pragma unroll
-        for (int k = 0; k < 4 * G; ++k) n += __popc(__vcmpgeu2(k16[k], tt));
+    auto publish = [&](int n, int par) -> int {
         n = __reduce_add_sync(0xFFFFFFFFu, n >> 4);
         if (lane == 0) s_cnt[par * NW + warp] = n;
         __syncthreads();
@@ -415,11 +422,21 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
         for (int w = 0; w < NW; ++w) tot += s_cnt[par * NW + w];
         return tot;
     };
+    auto block_count = [&](uint32_t t, int par) -> int {
+        const uint32_t tt = t | (t << 16);
+        int n = 0;
+#pragma unroll 1
+        for (int g = 0; g < G; ++g) {
+            const uint4 v = *reinterpret_cast<const uint4*>(s_k16 + (g * kNT + tid) * 8);
+            n += __popc(__vcmpgeu2(v.x, tt)) + __popc(__vcmpgeu2(v.y, tt)) +
+                 __popc(__vcmpgeu2(v.z, tt)) + __popc(__vcmpgeu2(v.w, tt));
+        }
+        return publish(n, par);
+    };
     const uint32_t wmax = __reduce_max_sync(0xFFFFFFFFu, kmax);
     if (lane == 0) s_misc[48 + warp] = static_cast<int>(wmax);
-    const uint32_t carried = __ldg(p.thresh + b);
     int par = 0;
-    int cnt0 = block_count(carried, par);  // [A0] also publishes the warp maxima
+    cnt0 = publish(cnt0, par);  // [A0] also publishes the warp maxima and the keys
     uint32_t bmax = 0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) bmax = max(bmax, static_cast<uint32_t>(s_misc[48 + w]));
@@ -457,17 +474,17 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     __syncthreads();  // candidate counter reset visible
     if (found) {
         // Collect the candidates (a recomputed for groups that hold one).
-#pragma unroll
+#pragma unroll 1
         for (int g = 0; g < G; ++g) {
+            const int e0 = (g * kNT + tid) * 8;
+            const uint4 v = *reinterpret_cast<const uint4*>(s_k16 + e0);
+            const uint32_t tt = t16 | (t16 << 16);
+            const uint32_t w[4] = {__vcmpgeu2(v.x, tt), __vcmpgeu2(v.y, tt), __vcmpgeu2(v.z, tt),
+                                   __vcmpgeu2(v.w, tt)};
             uint32_t m8 = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t w = k16[g * 4 + k];
-                m8 |= static_cast<uint32_t>((w & 0xFFFFu) >= t16) << (2 * k);
-                m8 |= static_cast<uint32_t>((w >> 16) >= t16) << (2 * k + 1);
-            }
+            for (int k = 0; k < 4; ++k) m8 |= ((w[k] & 1u) << (2 * k)) | (((w[k] >> 16) & 1u) << (2 * k + 1));
             if (m8) {
-                const int e0 = (g * kNT + tid) * 8;
                 double a[8];
                 decode8<KT>(c, e0, a);
                 int s0 = atomicAdd(&s_misc[NW], __popc(m8));
