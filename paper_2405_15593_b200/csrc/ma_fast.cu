@@ -473,54 +473,66 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
     if (tid == 0) s_misc[NW] = 0;
     __syncthreads();  // candidate counter reset visible
     if (found) {
-        // Collect the candidates (a recomputed for groups that hold one).
-#pragma unroll 1
+        // Collect the candidates: each thread scans its 32 keys and recomputes a
+        // only for its candidates (warp-aggregated slot allocation).
+        const uint32_t tt = t16 | (t16 << 16);
+        uint32_t cm = 0;
+#pragma unroll
         for (int g = 0; g < G; ++g) {
-            const int e0 = (g * kNT + tid) * 8;
-            const uint4 v = *reinterpret_cast<const uint4*>(s_k16 + e0);
-            const uint32_t tt = t16 | (t16 << 16);
-            const uint32_t w[4] = {__vcmpgeu2(v.x, tt), __vcmpgeu2(v.y, tt), __vcmpgeu2(v.z, tt),
+            const uint4 v = *reinterpret_cast<const uint4*>(s_k16 + (g * kNT + tid) * 8);
+            const uint32_t r[4] = {__vcmpgeu2(v.x, tt), __vcmpgeu2(v.y, tt), __vcmpgeu2(v.z, tt),
                                    __vcmpgeu2(v.w, tt)};
-            uint32_t m8 = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) m8 |= ((w[k] & 1u) << (2 * k)) | (((w[k] >> 16) & 1u) << (2 * k + 1));
-            if (m8) {
-                double a[8];
-                decode8<KT>(c, e0, a);
-                int s0 = atomicAdd(&s_misc[NW], __popc(m8));
+            for (int k = 0; k < 4; ++k)
+                cm |= ((r[k] & 1u) | ((r[k] >> 15) & 2u)) << (g * 8 + 2 * k);
+        }
+        const int n = __popc(cm);
+        int incl = n;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if (!((m8 >> i) & 1u)) continue;
-                    s_cval[s0] = a[i];
-                    s_ckhi[s0] = hi_key(a[i]);
-                    s_cidx[s0] = e0 + i;
-                    ++s0;
-                }
-            }
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+            if (lane >= off) incl += t;
+        }
+        int slot0 = 0;
+        if (lane == 31 && incl) slot0 = atomicAdd(&s_misc[NW], incl);
+        int sidx = __shfl_sync(0xFFFFFFFFu, slot0, 31) + incl - n;
+        while (cm) {
+            const int sb = __ffs(cm) - 1;
+            cm &= cm - 1;
+            const int e = ((sb >> 3) * kNT + tid) * 8 + (sb & 7);
+            const double av = recompute_a<KT>(c, e);
+            s_cval[sidx] = av;
+            s_ckhi[sidx] = hi_key(av);
+            s_cidx[sidx] = e;
+            ++sidx;
         }
         __syncthreads();  // [A] candidates
         const int ncand = s_misc[NW];
-        const int target = (ncand > kTarget ? kTarget : ncand) - 1;
-        const int n4 = ncand & ~3;
-        for (int t = tid; t < ncand; t += kNT) {
-            const uint32_t kh = s_ckhi[t];
-            int above = 0, eq = 0;
-            for (int q = 0; q < n4; q += 4) {
-                const uint4 v = *reinterpret_cast<const uint4*>(s_ckhi + q);
-                above += (v.x > kh) + (v.y > kh) + (v.z > kh) + (v.w > kh);
-                eq += (v.x == kh) + (v.y == kh) + (v.z == kh) + (v.w == kh);
+        if (warp == 0) {
+            // Exact Top-k_b among the candidates (compress.cpp:39-53): bisect the
+            // k_b-th largest high word with warp-wide counts; ties on the high
+            // word resolve on the full |a| key, then the lower index.
+            auto count_ge = [&](uint32_t v) {
+                int cnt = 0;
+                for (int q = lane; q < ncand; q += 32) cnt += s_ckhi[q] >= v;
+                return __reduce_add_sync(0xFFFFFFFFu, cnt);
+            };
+            uint32_t lo = t16 << 16, hi = (bmax + 1) << 16;  // count(lo) >= kb > count(hi)
+            while (hi - lo > 1) {
+                const uint32_t mid = lo + (hi - lo) / 2;
+                if (count_ge(mid) >= kb) lo = mid; else hi = mid;
             }
-            for (int q = n4; q < ncand; ++q) {
-                const uint32_t v = s_ckhi[q];
-                above += v > kh;
-                eq += v == kh;
+            const int above = count_ge(lo + 1);
+            const int need = kb - above, eqc = count_ge(lo) - above;
+            for (int q = lane; q < ncand; q += 32) {
+                const uint32_t kh = s_ckhi[q];
+                bool sel = kh > lo;
+                if (kh == lo) sel = eqc == need || tie_rank_hi(s_cval, s_ckhi, s_cidx, ncand, q) < need;
+                if (sel) atomicOr(&s_sel[s_cidx[q] >> 5], 1u << (s_cidx[q] & 31));
             }
-            int rank = above;
-            if (eq > 1) rank += tie_rank_hi(s_cval, s_ckhi, s_cidx, ncand, t);
-            if (rank < kb) atomicOr(&s_sel[s_cidx[t] >> 5], 1u << (s_cidx[t] & 31));
-            if (rank == target) {
-                const uint32_t h = kh >> 16;  // next step's threshold
-                s_misc[1] = static_cast<int>(ncand > kTarget ? h : (h > 1 ? h - 1 : 1u));
+            if (lane == 0) {
+                const uint32_t h = lo >> 16;  // next step: one 16-bit bucket below the k_b-th key
+                s_misc[1] = static_cast<int>(h > 1 ? h - 1 : 1u);
             }
         }
         __syncthreads();  // [B] selection bitmap
@@ -553,18 +565,32 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
         double a[8];
         decode8<KT>(c, e0, a);
         const uint32_t sel8 = (s_sel[e0 >> 5] >> (e0 & 31)) & 0xFFu;
-        double lo = __longlong_as_double(0x7FF0000000000000ll), hi = -lo;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             if ((sel8 >> i) & 1u) a[i] = 0.0;
-            lo = fmin(lo, a[i]);
-            hi = fmax(hi, a[i]);
             if (want_report) rep[2] += a[i] * a[i];
         }
+        // min / max of the 8 residuals (quantize.cpp:15-24; no NaN, no -0.0 here):
+        // a compare-exchange per pair, then two 4-way trees.
+        double l4[4], h4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool lt = a[2 * k] < a[2 * k + 1];
+            l4[k] = lt ? a[2 * k] : a[2 * k + 1];
+            h4[k] = lt ? a[2 * k + 1] : a[2 * k];
+        }
+        double lo = l4[0] < l4[1] ? l4[0] : l4[1];
+        const double lo2 = l4[2] < l4[3] ? l4[2] : l4[3];
+        lo = lo < lo2 ? lo : lo2;
+        double hi = h4[0] > h4[1] ? h4[0] : h4[1];
+        const double hi2 = h4[2] > h4[3] ? h4[2] : h4[3];
+        hi = hi > hi2 ? hi : hi2;
 #pragma unroll
         for (int off = 1; off < LPB; off <<= 1) {
-            lo = fmin(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, off));
-            hi = fmax(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, off));
+            const double ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
+            const double oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+            lo = ol < lo ? ol : lo;
+            hi = oh > hi ? oh : hi;
         }
         const double rng = __dsub_rn(hi, lo);
         uint32_t word = 0;
