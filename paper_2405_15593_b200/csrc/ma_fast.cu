@@ -509,59 +509,31 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
         __syncthreads();  // [A] candidates
         const int ncand = s_misc[NW];
         if (warp == 0) {
-            // Exact Top-k_b among the candidates (compress.cpp:39-53). Walk the
-            // 16-bit key buckets down from the block max with warp ballots to
-            // find the bucket B holding the k_b-th largest key; inside B rank by
-            // the full |a| key, then the lower index.
-            constexpr int kRegCand = 4;  // candidates per lane held in registers
-            uint32_t kh[kRegCand];
-#pragma unroll
-            for (int j = 0; j < kRegCand; ++j) {
-                const int q = lane + 32 * j;
-                kh[j] = q < ncand ? s_ckhi[q] : 0u;
+            // Exact Top-k_b among the candidates (compress.cpp:39-53): bisect the
+            // k_b-th largest high word with warp-wide counts; ties on the high
+            // word resolve on the full |a| key, then the lower index.
+            auto count_ge = [&](uint32_t v) {
+                int cnt = 0;
+                for (int q = lane; q < ncand; q += 32) cnt += s_ckhi[q] >= v;
+                return __reduce_add_sync(0xFFFFFFFFu, cnt);
+            };
+            uint32_t lo = t16 << 16, hi = (bmax + 1) << 16;  // count(lo) >= kb > count(hi)
+            while (hi - lo > 1) {
+                const uint32_t mid = lo + (hi - lo) / 2;
+                if (count_ge(mid) >= kb) lo = mid; else hi = mid;
             }
-            uint32_t bucket = bmax + 1, above = 0;
-            if (ncand <= 32 * kRegCand) {
-                while (bucket > t16) {
-                    --bucket;
-                    uint32_t n = 0;
-#pragma unroll
-                    for (int j = 0; j < kRegCand; ++j)
-                        n += __popc(__ballot_sync(0xFFFFFFFFu, (kh[j] >> 16) == bucket));
-                    if (above + n >= static_cast<uint32_t>(kb)) break;
-                    above += n;
-                }
-            } else {  // large candidate sets (k_b > 64): same walk over smem
-                while (bucket > t16) {
-                    --bucket;
-                    int n = 0;
-                    for (int q = lane; q < ncand; q += 32) n += (s_ckhi[q] >> 16) == bucket;
-                    n = __reduce_add_sync(0xFFFFFFFFu, n);
-                    if (above + n >= static_cast<uint32_t>(kb)) break;
-                    above += n;
-                }
-            }
-            const int need = kb - static_cast<int>(above);  // taken from bucket B
+            const int above = count_ge(lo + 1);
+            const int need = kb - above, eqc = count_ge(lo) - above;
             for (int q = lane; q < ncand; q += 32) {
-                const uint32_t k = s_ckhi[q];
-                const uint32_t kb16 = k >> 16;
-                bool sel = kb16 > bucket;
-                if (kb16 == bucket) {
-                    // rank inside B: candidates of B that beat q (key desc, idx asc)
-                    const uint64_t kt = key_of(s_cval[q]);
-                    const int it = s_cidx[q];
-                    int r = 0;
-                    for (int u = 0; u < ncand; ++u) {
-                        if ((s_ckhi[u] >> 16) != bucket || u == q) continue;
-                        const uint64_t ku = key_of(s_cval[u]);
-                        r += (ku > kt) || (ku == kt && s_cidx[u] < it);
-                    }
-                    sel = r < need;
-                }
+                const uint32_t kh = s_ckhi[q];
+                bool sel = kh > lo;
+                if (kh == lo) sel = eqc == need || tie_rank_hi(s_cval, s_ckhi, s_cidx, ncand, q) < need;
                 if (sel) atomicOr(&s_sel[s_cidx[q] >> 5], 1u << (s_cidx[q] & 31));
             }
-            if (lane == 0)  // next step: two 16-bit buckets below B (room for scale drift)
-                s_misc[1] = static_cast<int>(bucket > 2 ? bucket - 2 : 1u);
+            if (lane == 0) {
+                const uint32_t h = lo >> 16;  // next step: one 16-bit bucket below the k_b-th key
+                s_misc[1] = static_cast<int>(h > 1 ? h - 1 : 1u);
+            }
         }
         __syncthreads();  // [B] selection bitmap
         if (warp == 0) word_prefix(s_sel, BLOCK / 32, s_wpref);
@@ -593,14 +565,10 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
         double a[8];
         decode8<KT>(c, e0, a);
         const uint32_t sel8 = (s_sel[e0 >> 5] >> (e0 & 31)) & 0xFFu;
-        if (sel8) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                if ((sel8 >> i) & 1u) a[i] = 0.0;
-        }
-        if (want_report) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) rep[2] += a[i] * a[i];
+        for (int i = 0; i < 8; ++i) {
+            if ((sel8 >> i) & 1u) a[i] = 0.0;
+            if (want_report) rep[2] += a[i] * a[i];
         }
         // min / max of the 8 residuals (quantize.cpp:15-24; no NaN, no -0.0 here):
         // a compare-exchange per pair, then two 4-way trees.
@@ -629,21 +597,16 @@ __global__ void __launch_bounds__(kNT, 8) microadam_step_fast(const __grid_const
         if (rng != 0.0) {
             const float r32 = __double2float_rn(rng);
             const bool fastq = r32 >= 0x1p-100f && r32 <= 0x1p100f;
-            const float kk = fastq ? __fdiv_rn(15.0f * 1048576.0f, r32) : 0.0f;  // 15/rng in 2^-20 units
-            uint32_t gmin = fastq ? 0xFFFFFu : 0u;
-            uint32_t xs[8];
+            const float k32 = fastq ? __fdiv_rn(15.0f, r32) : 0.0f;
+            uint32_t bad = fastq ? 0u : 0xFFu;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const float d32 = __double2float_rn(__dsub_rn(a[i], lo));
-                xs[i] = __float2uint_rz(__fmaf_rn(d32, kk, 524288.0f));  // (q + 1/2) * 2^20
-                word |= (xs[i] >> 20) << (4 * i);
-                gmin = min(gmin, (xs[i] + kGuard) & 0xFFFFFu);
+                const uint32_t xq = __float2uint_rz(__fmaf_rn(__fmul_rn(d32, k32), 1048576.0f, 524288.0f));
+                word |= (xq >> 20) << (4 * i);
+                bad |= static_cast<uint32_t>(((xq + kGuard) & 0xFFFFFu) < 2 * kGuard) << i;
             }
-            if (gmin < 2 * kGuard) {  // rare: some element in the guard band -> exact quotient
-                uint32_t bad = fastq ? 0u : 0xFFu;
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    bad |= static_cast<uint32_t>(((xs[i] + kGuard) & 0xFFFFFu) < 2 * kGuard) << i;
+            if (bad) {  // rare: guard band -> the exact quotient
                 const double level = __ddiv_rn(rng, 15.0);
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
