@@ -17,7 +17,7 @@ for d in sizes:
     g = torch.empty(d, dtype=torch.bfloat16, device="cuda")
     ma._capi.check(L.ma_fill_synthetic(p.data_ptr(), 2, d, 1, 0, 0, 0, s))
     times = []
-    for i in range(12):
+    for i in range(int(os.environ.get("SCAN_STEPS", "12"))):
         ma._capi.check(L.ma_fill_synthetic(g.data_ptr(), 2, d, 42, i + 1, 0, 0, s))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
