@@ -156,7 +156,8 @@ struct ma_handle {
     Shape shape;
     ma::Variant variant{};
     ma::Variant tail_variant{};  // generic kernel for the partial tail block (fast path)
-    bool fast = false;  // ma_fast.cu kernel (else the generic ma_kernels.cu kernel)
+    bool fast = false;  // ma_fast.cu / ma_warp.cu kernel (else the generic ma_kernels.cu kernel)
+    bool warp = false;  // fast path runs the warp-per-block kernel (ma_warp.cu)
     int persist_grid = 0;
     int device = 0;
     uint8_t* d_codes = nullptr;
@@ -270,7 +271,8 @@ cudaError_t launch(ma_handle* h, ma::StepArgs& a, int64_t nblocks, cudaStream_t 
     if (nfull > 0) {
         a.block_count = nfull;
         const int64_t grid = std::min<int64_t>(nfull, h->persist_grid);
-        cudaError_t e = ma::launch_step_fast(a, h->variant, int(grid), st);
+        cudaError_t e = h->warp ? ma::launch_step_warp(a, st)
+                                : ma::launch_step_fast(a, h->variant, int(grid), st);
         if (e != cudaSuccess) return e;
     }
     if (tail_partial) {
@@ -415,6 +417,12 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
             smem = std::max(smem, fs);
         }
     }
+    const char* force_cta = std::getenv("MA_FAST_CTA");  // A/B: the CTA-per-block fast kernel
+    if (h->fast && !(force_cta && force_cta[0] == '1') &&
+        ma::warp_path_ok(int(s.block), int(s.bucket), int(s.per_block_k), int(cfg->hp.window),
+                         int(s.kb_stride), cfg->grad_dtype, cfg->param_dtype, cfg->value_dtype) &&
+        ma::warp_smem_bytes(int(s.bucket)) <= size_t(smem_max))
+        h->warp = true;
     if (!h->fast) h->variant = h->tail_variant;
     if (smem > size_t(smem_max)) {
         delete h;

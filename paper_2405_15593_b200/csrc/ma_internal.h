@@ -61,6 +61,11 @@ size_t fast_smem_bytes(Variant v, int block, int bucket, int m, int kb_stride, i
                        int p_dtype, int v_dtype);
 int fast_blocks_per_sm(Variant v, int bucket, size_t smem);
 cudaError_t launch_step_fast(const StepArgs& a, Variant v, int grid, cudaStream_t s);
+// Warp-per-block kernel (ma_warp.cu): full B_d = 4096 blocks, k_b <= 64.
+bool warp_path_ok(int block, int bucket, int kb, int m, int kb_stride, int g_dtype, int p_dtype,
+                  int v_dtype);
+size_t warp_smem_bytes(int bucket);
+cudaError_t launch_step_warp(const StepArgs& a, cudaStream_t s);
 cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int* flag,
                                cudaStream_t s);
 cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double* out5,

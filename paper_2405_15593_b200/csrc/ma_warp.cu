@@ -1,0 +1,789 @@
+// ma_warp.cu — the warp-per-block sm_100a MicroAdam step kernel (default path).
+//
+// Same contract and bit-exact results as ma_kernels.cu / ma_fast.cu, shaped so
+// that no Top-K block ever waits on a CTA barrier: ONE WARP owns one
+// B_d = 4096 block end to end (optim.cpp:164-190), four independent warps per
+// 128-thread CTA, eight CTAs per SM (≤ 64 registers, ~4.5 KB smem per warp).
+// The serial parts of a block (exact select, window bookkeeping) overlap with
+// the streaming passes of the 31 other warps on the SM.
+//
+//  * Lane 0 starts the block's HBM traffic at once: 1-D bulk L2 prefetches
+//    (cp.async.bulk.prefetch.L2) of g, the EF codes, the bucket (lo, hi), the
+//    window rows and θ. The passes then read L2-hot lines.
+//  * Pass 1 (optim.cpp:166-168, quantize.cpp:164-178): a = g + decode(EF) in
+//    fp64 for 8 consecutive elements per lane per iteration; the 16-bit Top-K
+//    key (bits 62..48 of |a|) is compared with the threshold carried from the
+//    previous step (SIMD __vcmpgeu2); the hits stay as a 128-bit candidate
+//    mask in registers.
+//  * Exact block Top-K (compress.cpp:39-53): if k_b <= #hits <= 128 the hits'
+//    a values are gathered and the k_b-th largest high word is bisected with
+//    warp-wide counts over register-held keys; ties on the high word resolve on
+//    the full |a| key, then the lower index. Otherwise (first step, drift, or
+//    heavy ties) an out-of-line radix descent over 7-bit digits of the full
+//    63-bit key finds either a candidate set of <= 128 or the exact k_b-th key.
+//    The selection is always exact; the carried threshold only decides work.
+//  * Window row (window.cpp:14-26) at ascending positions from a word prefix of
+//    the selection bitmap.
+//  * ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187): per-block
+//    seen/dup bitmaps; coordinates in one row take z = 0 + w·v, duplicated
+//    ones are claimed once and re-summed in physical slot order. θ is updated
+//    in place (L2-hot) — only window coordinates change.
+//  * Pass 2 (compress.cpp:95-102, quantize.cpp:15-24, 42-55, 102-114): the
+//    residual is re-decoded from L2, bucket min/max in registers + shuffles,
+//    the 4-bit codes by the fixed-point fast path with an exact IEEE fallback
+//    inside the guard band (same rule as ma_fast.cu).
+#include "../../include/ma_synth.h"
+#include "ma_async.cuh"
+#include "ma_device.cuh"
+#include "ma_internal.h"
+
+namespace ma {
+namespace {
+
+using namespace dev;
+
+constexpr int kWarps = 4;                 // Top-K blocks (warps) per CTA
+constexpr int kBlk = 4096;                // B_d of this kernel
+constexpr int kIter = kBlk / 256;         // iterations of 8 elements per lane
+constexpr int kCapL = 4;                  // candidate slots per lane
+constexpr int kCap = 32 * kCapL;          // candidate capacity of the exact stage
+constexpr uint32_t kGuard = 64;           // fixed-point guard band (units of 2^-20)
+constexpr int kTargetHits = 64;           // carried-threshold target count (k_b <= hits <= kCap)
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Per-warp shared-memory carve-up (bytes; host and device agree).
+struct WLayout {
+    uint32_t ll, sel, wpref, dup, cval, cidx, misc, total;
+    __host__ __device__ WLayout() {}
+    __host__ __device__ explicit WLayout(int bucket) {
+        size_t o = 0;
+        ll = uint32_t(o);    o = align_up(o + size_t(kBlk / bucket) * 16, 16);  // (lo, level)
+        sel = uint32_t(o);   o = align_up(o + kBlk / 8, 16);                     // selection bits
+        wpref = uint32_t(o); o = align_up(o + kBlk / 8, 16);  // word prefix; then "seen" bits
+        dup = uint32_t(o);   o = align_up(o + kBlk / 8, 16);                     // duplicate bits
+        cval = uint32_t(o);  o = align_up(o + kCap * 8, 16);  // candidates; radix hist; dup queue
+        cidx = uint32_t(o);  o = align_up(o + kCap * 2, 16);
+        misc = uint32_t(o);  o = align_up(o + 16 * 4, 16);
+        total = uint32_t(align_up(o, 128));
+    }
+};
+
+template <int LPB_, int GDT_, int PDT_, int VDT_, bool REP_>
+struct KW {
+    static constexpr int LPB = LPB_, GDT = GDT_, PDT = PDT_, VDT = VDT_;
+    static constexpr int BUCKET = 8 * LPB_;
+    static constexpr bool REPORT = REP_;
+};
+
+// ---- 8 consecutive gradient values: raw vector load, then widen to fp64 ----
+template <int DT>
+struct Raw8 {
+    static constexpr int N = DT == BF16 ? 1 : (DT == F32 ? 2 : 4);
+    uint4 v[N];
+};
+template <int DT>
+__device__ __forceinline__ Raw8<DT> load_raw8(const void* g, int64_t e0) {
+    Raw8<DT> r;
+    const uint4* q = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(g) +
+                                                    e0 * (DT == BF16 ? 2 : (DT == F32 ? 4 : 8)));
+#pragma unroll
+    for (int k = 0; k < Raw8<DT>::N; ++k) r.v[k] = __ldg(q + k);
+    return r;
+}
+template <int DT>
+__device__ __forceinline__ void widen8(const Raw8<DT>& r, double (&x)[8]) {
+    if constexpr (DT == BF16) {
+        const uint32_t w[4] = {r.v[0].x, r.v[0].y, r.v[0].z, r.v[0].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            x[2 * k] = static_cast<double>(__uint_as_float(w[k] << 16));
+            x[2 * k + 1] = static_cast<double>(__uint_as_float(w[k] & 0xFFFF0000u));
+        }
+    } else if constexpr (DT == F32) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            x[4 * k + 0] = __uint_as_float(r.v[k].x);
+            x[4 * k + 1] = __uint_as_float(r.v[k].y);
+            x[4 * k + 2] = __uint_as_float(r.v[k].z);
+            x[4 * k + 3] = __uint_as_float(r.v[k].w);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            x[2 * k] = __hiloint2double(int(r.v[k].y), int(r.v[k].x));
+            x[2 * k + 1] = __hiloint2double(int(r.v[k].w), int(r.v[k].z));
+        }
+    }
+}
+
+// a += code·level + lo (quantize.cpp:164-178, optim.cpp:166-168): separate
+// multiply and add in fp64, no FMA.
+__device__ __forceinline__ void add_decoded8(double (&a)[8], uint32_t cw, double2 ll) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        a[i] = __dadd_rn(a[i], __dadd_rn(__dmul_rn(static_cast<double>((cw >> (4 * i)) & 15u), ll.y), ll.x));
+}
+
+// a at one block-relative element (same arithmetic as pass 1).
+template <class KT>
+__device__ __forceinline__ double recompute_a(const StepArgs& p, int64_t base, const double2* ll, int e) {
+    const uint32_t byte = p.codes[(base + e) >> 1];
+    const double2 q = ll[e / KT::BUCKET];
+    const double ev = __dadd_rn(__dmul_rn(static_cast<double>((byte >> ((e & 1) * 4)) & 15u), q.y), q.x);
+    return __dadd_rn(ld_t<KT::GDT>(p.grads, base + e), ev);
+}
+
+// t / kb for t < 2^16 without an integer division (float reciprocal + fix-up).
+__device__ __forceinline__ int row_of(int t, int kb, float inv_kb) {
+    int r = __float2int_rz(static_cast<float>(t) * inv_kb);
+    r -= (r * kb > t);
+    r += ((r + 1) * kb <= t);
+    return r;
+}
+
+__device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total) {
+    int incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += t;
+    }
+    total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    return incl - v;
+}
+
+// Rank correction among candidates whose high words tie (compress.cpp:43-48:
+// full |a| key first, then the lower index). Out of line: rare.
+__device__ __noinline__ int tie_rank_w(const double* cval, const int16_t* cidx, int ncand, int t) {
+    const uint64_t kt = key_of(cval[t]);
+    const uint32_t kh = static_cast<uint32_t>(kt >> 32);
+    const int it = cidx[t];
+    int extra = 0;
+    for (int q = 0; q < ncand; ++q) {
+        const uint64_t kq = key_of(cval[q]);
+        if (q == t || static_cast<uint32_t>(kq >> 32) != kh) continue;
+        extra += (kq > kt) || (kq == kt && cidx[q] < it);
+    }
+    return extra;
+}
+
+// The IEEE path of quantize_nearest (quantize.cpp:51-53) for an element whose
+// fixed-point estimate fell in the guard band. Out of line: rare.
+__device__ __noinline__ uint32_t exact_code_w(double x, double lo, double level) {
+    double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(x, lo), level), 0.5));
+    f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+    return static_cast<uint32_t>(f);
+}
+
+// Slow selection (out of line): the carried threshold missed (first step,
+// drift) or keys tie heavily. A radix descent over 7-bit digits of the 63-bit
+// key |a| (9 digits) re-decoding the L2-hot block each pass, until the keys at
+// or above the current prefix number <= kCap; those are gathered as candidates
+// (returns their count; misc[0] = high word of the prefix, a lower bound of
+// the k_b-th high word). If all 63 bits are fixed with more than kCap keys
+// tied at the k_b-th key, the exact selection — every key above it plus the
+// lowest-index ties (compress.cpp:43-48) — is written to the selection bitmap
+// directly and -1 is returned (misc[1] = the k_b-th key's high word).
+template <class KT>
+__device__ __noinline__ int slow_select(const StepArgs* pp, unsigned char* ws, int64_t b) {
+    const StepArgs& p = *pp;
+    const WLayout L(KT::BUCKET);
+    const int lane = threadIdx.x & 31;
+    const int64_t base = b * kBlk;
+    const double2* s_ll = reinterpret_cast<const double2*>(ws + L.ll);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.cval);  // 128 bins
+    uint32_t* s_sel = reinterpret_cast<uint32_t*>(ws + L.sel);
+    int* s_misc = reinterpret_cast<int*>(ws + L.misc);
+    const int kb = p.per_block_k;
+    auto block_a = [&](int j, double (&a)[8]) {
+        const int e0 = j * 256 + lane * 8;
+        widen8<KT::GDT>(load_raw8<KT::GDT>(p.grads, base + e0), a);
+        add_decoded8(a, *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0) >> 1)),
+                     s_ll[e0 / KT::BUCKET]);
+    };
+    uint64_t prefix = 0, pmask = 0;
+    int need = kb, above_total = 0, binc = 0;
+    for (int sh = 56;; sh -= 7) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) hist[lane * 4 + k] = 0;
+        __syncwarp();
+        for (int j = 0; j < kIter; ++j) {
+            double a[8];
+            block_a(j, a);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint64_t k = key_of(a[i]);
+                if ((k & pmask) == prefix) atomicAdd(&hist[(k >> sh) & 127u], 1u);
+            }
+        }
+        __syncwarp();
+        // digit d: the largest with #{digit >= d} >= need (suffix sums from the top)
+        const uint32_t h0 = hist[lane * 4], h1 = hist[lane * 4 + 1], h2 = hist[lane * 4 + 2],
+                       h3 = hist[lane * 4 + 3];
+        const int local = int(h0 + h1 + h2 + h3);
+        int incl = local;  // inclusive suffix over lanes >= lane
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_down_sync(0xFFFFFFFFu, incl, off);
+            if (lane + off < 32) incl += t;
+        }
+        const int s3 = incl - local + int(h3), s2 = s3 + int(h2), s1 = s2 + int(h1), s0 = s1 + int(h0);
+        int dl = -1;
+        if (s0 >= need) dl = lane * 4;
+        if (s1 >= need) dl = lane * 4 + 1;
+        if (s2 >= need) dl = lane * 4 + 2;
+        if (s3 >= need) dl = lane * 4 + 3;
+        const int d = __reduce_max_sync(0xFFFFFFFFu, dl);
+        const int owner = d >> 2;
+        const int sd = d & 3;
+        const int sfx = sd == 0 ? s0 : (sd == 1 ? s1 : (sd == 2 ? s2 : s3));
+        const int hd = int(sd == 0 ? h0 : (sd == 1 ? h1 : (sd == 2 ? h2 : h3)));
+        const int above = __shfl_sync(0xFFFFFFFFu, sfx - hd, owner);
+        binc = __shfl_sync(0xFFFFFFFFu, hd, owner);
+        above_total += above;
+        need -= above;
+        prefix |= static_cast<uint64_t>(d) << sh;
+        pmask |= uint64_t(127) << sh;
+        __syncwarp();
+        if (above_total + binc <= kCap || sh == 0) break;
+    }
+    double* s_cval = reinterpret_cast<double*>(ws + L.cval);
+    int16_t* s_cidx = reinterpret_cast<int16_t*>(ws + L.cidx);
+    if (above_total + binc <= kCap) {
+        // gather every key >= prefix (numeric) — exactly above_total + binc keys
+        if (lane == 0) s_misc[2] = 0;
+        __syncwarp();
+        for (int j = 0; j < kIter; ++j) {
+            double a[8];
+            block_a(j, a);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (key_of(a[i]) >= prefix) {
+                    const int q = atomicAdd(&s_misc[2], 1);
+                    s_cval[q] = a[i];
+                    s_cidx[q] = static_cast<int16_t>(j * 256 + lane * 8 + i);
+                }
+        }
+        __syncwarp();
+        if (lane == 0) s_misc[0] = static_cast<int>(prefix >> 32);
+        __syncwarp();
+        return above_total + binc;
+    }
+    // All 63 bits fixed: K* = prefix; `need` of the keys equal to K* in index order.
+    int eq_before = 0;
+    for (int j = 0; j < kIter; ++j) {
+        double a[8];
+        block_a(j, a);
+        uint32_t gt = 0, eq = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint64_t k = key_of(a[i]);
+            gt |= static_cast<uint32_t>(k > prefix) << i;
+            eq |= static_cast<uint32_t>(k == prefix) << i;
+        }
+        int tot;
+        const int ex = warp_excl_scan(__popc(eq), lane, tot);
+        uint32_t selm = gt;
+        int r = eq_before + ex;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if ((eq >> i) & 1u) {
+                if (r < need) selm |= 1u << i;
+                ++r;
+            }
+        eq_before += tot;
+        const int e0 = j * 256 + lane * 8;
+        if (selm) atomicOr(&s_sel[e0 >> 5], selm << (e0 & 31));
+    }
+    __syncwarp();
+    if (lane == 0) s_misc[1] = static_cast<int>(prefix >> 32);
+    if (p.dbg && lane == 0) atomicAdd(p.dbg + 0, 1u);
+    __syncwarp();
+    return -1;
+}
+
+template <class KT>
+__global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __grid_constant__ StepArgs p) {
+    constexpr int BUCKET = KT::BUCKET, LPB = KT::LPB;
+    constexpr int gsz = KT::GDT == F64 ? 8 : (KT::GDT == F32 ? 4 : 2);
+    constexpr int psz = KT::PDT == F64 ? 8 : (KT::PDT == F32 ? 4 : 2);
+    constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
+    constexpr bool want_report = KT::REPORT;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t bl = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+    if (bl >= p.block_count) return;
+    const int64_t b = p.block_offset + bl;
+    const int64_t base = b * kBlk;
+    const WLayout L(BUCKET);
+    unsigned char* ws = smem + warp * L.total;
+    double2* s_ll = reinterpret_cast<double2*>(ws + L.ll);
+    uint32_t* s_sel = reinterpret_cast<uint32_t*>(ws + L.sel);
+    int* s_wpref = reinterpret_cast<int*>(ws + L.wpref);
+    uint32_t* s_seen = reinterpret_cast<uint32_t*>(ws + L.wpref);
+    uint32_t* s_dup = reinterpret_cast<uint32_t*>(ws + L.dup);
+    double* s_cval = reinterpret_cast<double*>(ws + L.cval);
+    int16_t* s_cidx = reinterpret_cast<int16_t*>(ws + L.cidx);
+    int* s_misc = reinterpret_cast<int*>(ws + L.misc);
+    const int kb = p.per_block_k, kbs = p.kb_stride, m = p.m, slot = p.slot, filled = p.filled;
+    const int64_t went = b * m * static_cast<int64_t>(kbs);
+    int16_t* gwi = p.win_idx + went;
+    unsigned char* gwv = static_cast<unsigned char*>(p.win_val) + went * vsz;
+
+    // ---- prologue: start the block's HBM reads; bucket grids (quantize.cpp:7-13) ----
+    if (lane == 0) {
+        prefetch_l2(static_cast<const unsigned char*>(p.grads) + base * gsz, kBlk * gsz);
+        prefetch_l2(p.codes + base / 2, kBlk / 2);
+        prefetch_l2(p.meta + base / BUCKET, (kBlk / BUCKET) * 16);
+        prefetch_l2(gwi, uint32_t(m * kbs * 2));
+        prefetch_l2(gwv, uint32_t(m * kbs * vsz));
+        prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
+    }
+    for (int i = lane; i < kBlk / BUCKET; i += 32) {
+        const double2 mt = p.meta[base / BUCKET + i];
+        s_ll[i] = make_double2(mt.x, (mt.x == mt.y) ? 0.0 : __ddiv_rn(__dsub_rn(mt.y, mt.x), 15.0));
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        s_sel[lane * 4 + k] = 0;
+        s_dup[lane * 4 + k] = 0;
+    }
+    __syncwarp();
+
+    // ---- pass 1: a = g + decode(EF), 16-bit keys vs the carried threshold ----
+    // carried state: low 16 bits = key16 threshold, high 16 = hits it was chosen for
+    const uint32_t tstate = __ldg(p.thresh + b);
+    const uint32_t T = tstate & 0xFFFFu;
+    const uint32_t tt = T | (T << 16);
+    uint32_t cm0 = 0, cm1 = 0, cm2 = 0, cm3 = 0;  // candidate bits: byte j = iteration j
+    uint32_t kmax2 = 0;
+    double rep[kReportFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    {
+        Raw8<KT::GDT> nr = load_raw8<KT::GDT>(p.grads, base + lane * 8);
+        uint32_t ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + lane * 8) >> 1));
+#pragma unroll 1
+        for (int j = 0; j < kIter; ++j) {
+            const int e0 = j * 256 + lane * 8;
+            const Raw8<KT::GDT> r = nr;
+            const uint32_t cw = ncw;
+            if (j + 1 < kIter) {
+                nr = load_raw8<KT::GDT>(p.grads, base + e0 + 256);
+                ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0 + 256) >> 1));
+            }
+            double a[8];
+            widen8<KT::GDT>(r, a);
+            add_decoded8(a, cw, s_ll[e0 / BUCKET]);
+            uint32_t m8 = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t w = (hi_key(a[2 * k]) >> 16) | (hi_key(a[2 * k + 1]) & 0xFFFF0000u);
+                kmax2 = __vmaxu2(kmax2, w);
+                const uint32_t c = __vcmpgeu2(w, tt);
+                m8 |= ((c & 1u) | ((c >> 15) & 2u)) << (2 * k);
+                if (want_report) rep[1] += a[2 * k] * a[2 * k] + a[2 * k + 1] * a[2 * k + 1];
+            }
+            cm0 = __funnelshift_r(cm0, cm1, 8);
+            cm1 = __funnelshift_r(cm1, cm2, 8);
+            cm2 = __funnelshift_r(cm2, cm3, 8);
+            cm3 = (cm3 >> 8) | (m8 << 24);
+        }
+    }
+    const uint32_t kmax = __reduce_max_sync(0xFFFFFFFFu, max(kmax2 & 0xFFFFu, kmax2 >> 16));
+    if (p.check_finite && kmax >= 0x7FF0u && lane == 0) atomicOr(p.flag, 1u);  // inf/NaN in g or a
+    const int nmine = __popc(cm0) + __popc(cm1) + __popc(cm2) + __popc(cm3);
+    const int cnt = __reduce_add_sync(0xFFFFFFFFu, nmine);
+
+    // ---- block Top-K (compress.cpp:39-53, 73-85) ----
+    int ncand = -1;
+    uint32_t lo32 = T << 16;
+    if (T != 0 && cnt >= kb && cnt <= kCap) {
+        int total;
+        int pos = warp_excl_scan(nmine, lane, total);
+        const uint32_t cms[4] = {cm0, cm1, cm2, cm3};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            uint32_t bits = cms[w];
+            while (bits) {
+                const int s = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int e = (w * 4 + (s >> 3)) * 256 + lane * 8 + (s & 7);
+                s_cval[pos] = recompute_a<KT>(p, base, s_ll, e);
+                s_cidx[pos] = static_cast<int16_t>(e);
+                ++pos;
+            }
+        }
+        ncand = cnt;
+        __syncwarp();
+    } else {
+        ncand = slow_select<KT>(&p, ws, b);
+        if (p.dbg && lane == 0) {
+            atomicAdd(p.dbg + 2, 1u);
+            if (cnt > kCap) atomicAdd(p.dbg + 3, 1u);
+        }
+        if (ncand >= 0) lo32 = static_cast<uint32_t>(s_misc[0]);
+    }
+    uint32_t next_t;
+    uint32_t selc = 0;  // which of my candidate slots are selected
+    if (ncand >= 0) {
+        uint32_t kh[kCapL];
+#pragma unroll
+        for (int s = 0; s < kCapL; ++s) {
+            const int q = lane + 32 * s;
+            kh[s] = q < ncand ? hi_key(s_cval[q]) : 0u;
+        }
+        auto count_ge = [&](uint32_t v) {
+            int c = 0;
+#pragma unroll
+            for (int s = 0; s < kCapL; ++s) c += kh[s] >= v;
+            return __reduce_add_sync(0xFFFFFFFFu, c);
+        };
+        // bisect the k_b-th largest high word: count(lo) >= kb > count(hi)
+        uint32_t lo = lo32, hi = (kmax + 1) << 16;
+        while (hi - lo > 1) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            if (count_ge(mid) >= kb) lo = mid; else hi = mid;
+        }
+        const int above = count_ge(lo + 1);
+        const int need = kb - above, eqc = count_ge(lo) - above;
+#pragma unroll
+        for (int s = 0; s < kCapL; ++s) {
+            const int q = lane + 32 * s;
+            bool sel = q < ncand && kh[s] > lo;
+            if (q < ncand && kh[s] == lo) sel = eqc == need || tie_rank_w(s_cval, s_cidx, ncand, q) < need;
+            if (sel) {
+                const int e = s_cidx[q];
+                atomicOr(&s_sel[e >> 5], 1u << (e & 31));
+                selc |= 1u << s;
+            }
+        }
+        // Next step's threshold. The hits seen at T against the hits T was
+        // chosen for estimate the step-to-step drift of |a| (the EF grows
+        // until it saturates); aim the new threshold at kTargetHits after the
+        // same drift: the largest 16-bit key t whose candidate count reaches
+        // want = kTargetHits * planned / seen. Counts below the candidate floor
+        // are unknown; there one key below the floor is taken (~1.3x hits).
+        const int planned = T ? static_cast<int>(tstate >> 16) : 0;
+        int want = planned ? (kTargetHits * planned) / max(cnt, 1) : kTargetHits;
+        want = min(max(want, kb + (kb >> 2)), kCap - (kCap >> 2));
+        const uint32_t floor16 = (lo32 + 0xFFFFu) >> 16;  // every key16 >= floor16 is a candidate
+        uint32_t t = lo >> 16;
+        int c = count_ge(t << 16);
+        while (t > floor16 && c < want) c = count_ge(--t << 16);
+        if (c < want && t > 1) {
+            --t;
+            c += c >> 2;
+        }
+        next_t = t | (static_cast<uint32_t>(min(c, 0xFFFF)) << 16);
+    } else {
+        const uint32_t h = static_cast<uint32_t>(s_misc[1]) >> 16;
+        next_t = h > 2 ? h - 2 : 1u;
+    }
+    if (lane == 0) p.thresh[b] = (next_t & 0xFFFFu) ? next_t : (next_t | 1u);
+    __syncwarp();
+
+    // ---- window row `slot` (window.cpp:14-26): ascending positions ----
+    {
+        uint32_t wv[4];
+        int loc = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            wv[k] = s_sel[lane * 4 + k];
+            loc += __popc(wv[k]);
+        }
+        int tot;
+        int run = warp_excl_scan(loc, lane, tot);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            s_wpref[lane * 4 + k] = run;
+            run += __popc(wv[k]);
+        }
+    }
+    __syncwarp();
+    const int64_t row0 = static_cast<int64_t>(slot) * kbs;
+    if (ncand >= 0) {
+#pragma unroll
+        for (int s = 0; s < kCapL; ++s)
+            if ((selc >> s) & 1u) {
+                const int q = lane + 32 * s;
+                const int e = s_cidx[q];
+                const int pos = s_wpref[e >> 5] + __popc(s_sel[e >> 5] & ((1u << (e & 31)) - 1u));
+                gwi[row0 + pos] = static_cast<int16_t>(e);
+                st_t<KT::VDT>(gwv, row0 + pos, s_cval[q]);
+            }
+    } else {
+        // heavy-tie path: the selected elements straight from the bitmap
+        for (int w = lane; w < kBlk / 32; w += 32) {
+            uint32_t bits = s_sel[w];
+            int pos = s_wpref[w];
+            while (bits) {
+                const int e = w * 32 + __ffs(bits) - 1;
+                bits &= bits - 1;
+                gwi[row0 + pos] = static_cast<int16_t>(e);
+                st_t<KT::VDT>(gwv, row0 + pos, recompute_a<KT>(p, base, s_ll, e));
+                ++pos;
+            }
+        }
+    }
+    __threadfence_block();
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s_seen[lane * 4 + k] = 0;  // word prefix is dead
+    __syncwarp();
+
+    // ---- ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) ----
+    const int nent = filled * kb;
+    const float inv_kb = 1.0f / static_cast<float>(kb);
+    for (int t = lane; t < nent; t += 32) {
+        const int r = row_of(t, kb, inv_kb);
+        const int idx = gwi[r * kbs + (t - r * kb)];
+        const uint32_t bit = 1u << (idx & 31);
+        if (atomicOr(&s_seen[idx >> 5], bit) & bit) atomicOr(&s_dup[idx >> 5], bit);
+    }
+    __syncwarp();
+    auto update = [&](int idx, double z1, double z2) {
+        const double mhat = __dmul_rn(z1, p.scale1);
+        const double vhat = __dmul_rn(z2, p.scale2);
+        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+        const double th = ld_t<KT::PDT>(p.params, base + idx);
+        st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
+        if (want_report && u != 0.0) rep[4] += 1.0;
+    };
+    // Entries of duplicated coordinates go to an ordered list (warp ballots in
+    // entry order = (slot, position) order); one claimant per coordinate then
+    // sums its entries in list order, i.e. physical slot order.
+    int* dupl = reinterpret_cast<int*>(s_cval);  // candidates are dead
+    constexpr int qcap = kCap * 2;
+    int ndup = 0;
+    // unique coordinates, four entries per lane in flight (θ loads overlap)
+    for (int t0 = 0; t0 < nent; t0 += 4 * 32) {
+        int idx[4], e[4], r[4];
+        bool mine[4];
+        double th[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int t = t0 + k * 32 + lane;
+            mine[k] = false;
+            r[k] = 0;
+            e[k] = 0;
+            idx[k] = 0;
+            bool dup = false;
+            if (t < nent) {
+                r[k] = row_of(t, kb, inv_kb);
+                e[k] = r[k] * kbs + (t - r[k] * kb);
+                idx[k] = gwi[e[k]];
+                dup = (s_dup[idx[k] >> 5] >> (idx[k] & 31)) & 1u;
+                mine[k] = !dup;
+            }
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
+            const int q = ndup + __popc(bal & lanemask_lt());
+            if (dup && q < qcap) dupl[q] = (idx[k] << 16) | (r[k] << 8) | (t - r[k] * kb);
+            ndup += __popc(bal);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) th[k] = mine[k] ? ld_t<KT::PDT>(p.params, base + idx[k]) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!mine[k]) continue;
+            const double v = ld_t<KT::VDT>(gwv, e[k]);
+            const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r[k]], v)), p.scale1);
+            const double vhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w2[r[k]], __dmul_rn(v, v))), p.scale2);
+            const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+            st_t<KT::PDT>(p.params, base + idx[k], __dsub_rn(th[k], __dmul_rn(p.lr, u)));
+            if (want_report && u != 0.0) rep[4] += 1.0;
+        }
+    }
+    __syncwarp();
+    if (ndup <= qcap) {
+        for (int q = lane; q < ndup; q += 32) {
+            const int idx = dupl[q] >> 16;
+            const uint32_t bit = 1u << (idx & 31);
+            if (!(atomicAnd(&s_seen[idx >> 5], ~bit) & bit)) continue;  // another entry claimed it
+            double z1 = 0.0, z2 = 0.0;
+            for (int q2 = 0; q2 < ndup; ++q2) {  // list order = physical slot order (window.cpp:32-39)
+                const int x = dupl[q2];
+                if ((x >> 16) != idx) continue;
+                const int rr = (x >> 8) & 0xFF;
+                const double v = ld_t<KT::VDT>(gwv, rr * kbs + (x & 0xFF));
+                z1 = __dadd_rn(z1, __dmul_rn(p.w1[rr], v));
+                z2 = __dadd_rn(z2, __dmul_rn(p.w2[rr], __dmul_rn(v, v)));
+            }
+            update(idx, z1, z2);
+        }
+    } else {  // list overflow (pathological windows): binary search per claimant
+        for (int t = lane; t < nent; t += 32) {
+            const int r = row_of(t, kb, inv_kb);
+            const int idx = gwi[r * kbs + (t - r * kb)];
+            const uint32_t bit = 1u << (idx & 31);
+            if (!((s_dup[idx >> 5] >> (idx & 31)) & 1u)) continue;
+            if (!(atomicAnd(&s_seen[idx >> 5], ~bit) & bit)) continue;
+            double z1 = 0.0, z2 = 0.0;
+            for (int rr = 0; rr < filled; ++rr) {  // physical slot order (window.cpp:32-39)
+                const int16_t* row = gwi + rr * kbs;
+                int lo_i = 0, hi_i = kb;
+                while (lo_i < hi_i) {
+                    const int mid = (lo_i + hi_i) >> 1;
+                    if (row[mid] < idx) lo_i = mid + 1; else hi_i = mid;
+                }
+                if (lo_i < kb && row[lo_i] == idx) {
+                    const double v = ld_t<KT::VDT>(gwv, rr * kbs + lo_i);
+                    z1 = __dadd_rn(z1, __dmul_rn(p.w1[rr], v));
+                    z2 = __dadd_rn(z2, __dmul_rn(p.w2[rr], __dmul_rn(v, v)));
+                }
+            }
+            update(idx, z1, z2);
+        }
+    }
+
+    // ---- pass 2: residual (compress.cpp:95-102) + 4-bit re-quantization
+    //      (quantize.cpp:15-24, 42-55, 102-114, 142-162) ----
+#pragma unroll 1
+    for (int j = 0; j < kIter; ++j) {
+        const int e0 = j * 256 + lane * 8;
+        double a[8];
+        widen8<KT::GDT>(load_raw8<KT::GDT>(p.grads, base + e0), a);
+        add_decoded8(a, *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0) >> 1)),
+                     s_ll[e0 / BUCKET]);
+        const uint32_t sel8 = (s_sel[e0 >> 5] >> (e0 & 31)) & 0xFFu;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if ((sel8 >> i) & 1u) a[i] = 0.0;
+            if (want_report) rep[2] += a[i] * a[i];
+        }
+        double l4[4], h4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool lt = a[2 * k] < a[2 * k + 1];
+            l4[k] = lt ? a[2 * k] : a[2 * k + 1];
+            h4[k] = lt ? a[2 * k + 1] : a[2 * k];
+        }
+        double lo = l4[0] < l4[1] ? l4[0] : l4[1];
+        const double lo2 = l4[2] < l4[3] ? l4[2] : l4[3];
+        lo = lo < lo2 ? lo : lo2;
+        double hi = h4[0] > h4[1] ? h4[0] : h4[1];
+        const double hi2 = h4[2] > h4[3] ? h4[2] : h4[3];
+        hi = hi > hi2 ? hi : hi2;
+#pragma unroll
+        for (int off = 1; off < LPB; off <<= 1) {
+            const double ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
+            const double oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+            lo = ol < lo ? ol : lo;
+            hi = oh > hi ? oh : hi;
+        }
+        const double rng = __dsub_rn(hi, lo);
+        uint32_t word = 0;
+        if (rng != 0.0) {
+            const float r32 = __double2float_rn(rng);
+            const bool fastq = r32 >= 0x1p-100f && r32 <= 0x1p100f;
+            const float k32 = fastq ? __fdividef(15.0f, r32) : 0.0f;  // ≤ 2 ulp
+            uint32_t bad = fastq ? 0u : 0xFFu;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float d32 = __double2float_rn(__dsub_rn(a[i], lo));
+                const uint32_t xq = __float2uint_rz(__fmaf_rn(__fmul_rn(d32, k32), 1048576.0f, 524288.0f));
+                word |= (xq >> 20) << (4 * i);
+                bad |= static_cast<uint32_t>(((xq + kGuard) & 0xFFFFFu) < 2 * kGuard) << i;
+            }
+            if (bad) {  // rare: guard band -> the exact quotient
+                const double level = __ddiv_rn(rng, 15.0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if ((bad >> i) & 1u)
+                        word = (word & ~(15u << (4 * i))) | (exact_code_w(a[i], lo, level) << (4 * i));
+                if (p.dbg) atomicAdd(p.dbg + 1, __popc(bad));
+            }
+        }
+        if (want_report) {
+            const double level = rng == 0.0 ? 0.0 : __ddiv_rn(rng, 15.0);
+            double x[8];
+            widen8<KT::GDT>(load_raw8<KT::GDT>(p.grads, base + e0), x);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double en =
+                    __dadd_rn(__dmul_rn(static_cast<double>((word >> (4 * i)) & 15u), level), lo);
+                rep[3] += en * en;
+                rep[0] += x[i] * x[i];
+            }
+        }
+        *reinterpret_cast<uint32_t*>(p.codes + ((base + e0) >> 1)) = word;
+        if ((lane & (LPB - 1)) == 0) p.meta[(base + e0) / BUCKET] = make_double2(lo, hi);
+    }
+    if constexpr (want_report) {
+#pragma unroll
+        for (int f = 0; f < kReportFields; ++f) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) rep[f] += __shfl_xor_sync(0xFFFFFFFFu, rep[f], off);
+            if (lane == 0) p.partials[b * kReportFields + f] = rep[f];
+        }
+    }
+}
+
+template <class KT>
+cudaError_t launch_kw(const StepArgs& a, cudaStream_t s) {
+    const size_t smem = size_t(kWarps) * WLayout(KT::BUCKET).total;
+    auto k = microadam_step_warp<KT>;
+    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+    if (err != cudaSuccess) return err;
+    const int64_t grid = (a.block_count + kWarps - 1) / kWarps;
+    k<<<static_cast<unsigned>(grid), 32 * kWarps, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+#define MA_WARP_DTYPES(X)         \
+    X(BF16, BF16, BF16)           \
+    X(F32, F32, BF16)             \
+    X(F32, F32, F32)              \
+    X(BF16, F32, BF16)            \
+    X(F64, F64, F64)
+
+constexpr int dtype_key_w(int g, int p, int v) { return g * 9 + p * 3 + v; }
+
+template <int LPB, bool REP>
+cudaError_t launch_wdt(const StepArgs& a, cudaStream_t s) {
+    switch (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype)) {
+#define MA_CASE(G_, P_, V_) \
+        case dtype_key_w(G_, P_, V_): return launch_kw<KW<LPB, G_, P_, V_, REP>>(a, s);
+        MA_WARP_DTYPES(MA_CASE)
+#undef MA_CASE
+        default: return cudaErrorInvalidConfiguration;
+    }
+}
+
+template <bool REP>
+cudaError_t launch_wrep(const StepArgs& a, cudaStream_t s) {
+    switch (a.bucket) {
+        case 16: return launch_wdt<2, REP>(a, s);
+        case 32: return launch_wdt<4, REP>(a, s);
+        case 64: return launch_wdt<8, REP>(a, s);
+        default: return cudaErrorInvalidConfiguration;
+    }
+}
+
+}  // namespace
+
+// Warp path: B_d = 4096, k_b <= 64 (candidates fit kCap), B_q in {16, 32, 64},
+// an instantiated dtype combo; window rows addressable with 16-bit offsets.
+bool warp_path_ok(int block, int bucket, int kb, int m, int kb_stride, int g, int p, int v) {
+    if (block != kBlk || kb < 1 || kb > kCap / 2) return false;
+    if (bucket != 16 && bucket != 32 && bucket != 64) return false;
+    if (m < 1 || m > kMaxWindow || m * kb_stride > 32768) return false;
+    switch (dtype_key_w(g, p, v)) {
+#define MA_CASE(G_, P_, V_) case dtype_key_w(G_, P_, V_): return true;
+        MA_WARP_DTYPES(MA_CASE)
+#undef MA_CASE
+        default: return false;
+    }
+}
+
+size_t warp_smem_bytes(int bucket) { return size_t(kWarps) * WLayout(bucket).total; }
+
+cudaError_t launch_step_warp(const StepArgs& a, cudaStream_t s) {
+    if (a.block_count <= 0) return cudaSuccess;
+    if ((a.block_count + kWarps - 1) / kWarps > 0x7FFFFFFFll) return cudaErrorInvalidConfiguration;
+    return a.partials ? launch_wrep<true>(a, s) : launch_wrep<false>(a, s);
+}
+
+}  // namespace ma

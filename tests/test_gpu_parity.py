@@ -39,14 +39,14 @@ def _host(t):
     return t.detach().to(torch.float64).cpu().numpy()
 
 
-KERNELS = {"fast": {}, "fast_g2": {"MA_FAST_G2": "1"}, "generic": {"MA_FORCE_GENERIC": "1"}}
+KERNELS = {"fast": {}, "fast_cta": {"MA_FAST_CTA": "1"}, "generic": {"MA_FORCE_GENERIC": "1"}}
 
 
 def make_engine(kernel, *args, **kw):
     """Create a MicroAdam engine with the kernel family selected at ma_create time."""
     import os
     from paper_2405_15593_b200 import MicroAdam
-    saved = {k: os.environ.get(k) for k in ("MA_FAST_G2", "MA_FORCE_GENERIC")}
+    saved = {k: os.environ.get(k) for k in ("MA_FAST_CTA", "MA_FORCE_GENERIC")}
     for k in saved:
         os.environ.pop(k, None)
     os.environ.update(KERNELS[kernel])
@@ -76,7 +76,7 @@ def run_parity(d, hp, *, gdt="f32", pdt="f32", vdt="bf16", steps=12, levels=Fals
     params = _dev(theta0, pdt)
     for s in range(1, steps + 1):
         g = grad_fn(s) if grad_fn else oracle.synth(seed, s, 0, d, gdt, levels=levels)
-        g = np.asarray(g, np.float64)
+        g = _host(_dev(np.asarray(g, np.float64), gdt))  # the values the device sees
         want_rep = bool(report_every) and s % report_every == 0
         rep = eng.step(params, _dev(g, gdt), lr, report=want_rep)
         orep = orc.step(g, lr)
@@ -334,3 +334,24 @@ def test_kernel_counts_and_library_is_native():
     import os
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert "libmicroadam_cuda.so" in maps
+
+
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
+def test_persistent_spikes_duplicate_window_coordinates(kernel):
+    # the same coordinates win every step: each window row repeats them, so
+    # ADAM_STATS re-sums duplicated coordinates across all m rows.
+    rng = np.random.default_rng(5)
+    spikes = rng.choice(50_000, 400, replace=False)
+
+    def g(s):
+        x = oracle.synth(11, s, 0, 50_000) * 1e-3
+        x[spikes] += 50.0 + s
+        return x
+    run_parity(50_000, dict(lr=1e-2, window=12), gdt="bf16", pdt="f32", vdt="bf16", steps=16,
+               grad_fn=g, kernel=kernel)
+
+
+@pytest.mark.parametrize("density,m", [(0.015, 10), (0.002, 30), (0.01, 127)])
+def test_warp_kernel_shapes(density, m):
+    run_parity(4096 * 9, dict(lr=1e-2, density=density, window=m), gdt="bf16", pdt="bf16",
+               vdt="bf16", steps=min(m + 3, 20))

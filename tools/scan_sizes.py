@@ -17,6 +17,9 @@ for d in sizes:
     g = torch.empty(d, dtype=torch.bfloat16, device="cuda")
     ma._capi.check(L.ma_fill_synthetic(p.data_ptr(), 2, d, 1, 0, 0, 0, s))
     times = []
+    dbgon = os.environ.get("MA_DEBUG_COUNTERS") == "1"
+    prev = None
+    per = []
     for i in range(int(os.environ.get("SCAN_STEPS", "12"))):
         ma._capi.check(L.ma_fill_synthetic(g.data_ptr(), 2, d, 42, i + 1, 0, 0, s))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -25,9 +28,18 @@ for d in sizes:
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
+        if dbgon:
+            cur = eng.debug_counters()
+            if prev is not None:
+                per.append({k: cur[k] - prev[k] for k in cur})
+            prev = cur
     t = sorted(times[6:])[len(times[6:]) // 2]
     dbg = eng.debug_counters() if os.environ.get("MA_DEBUG_COUNTERS") == "1" else {}
     print(f"d={d:>12,}  step {t:9.3f} ms  {d / t / 1e6:8.3f} Gparam/s  {7.9 * d / t / 1e6:8.1f} GB/s  "
           f"steps: {' '.join(f'{x:.2f}' for x in times)} {dbg}", flush=True)
+    nb = d // 4096
+    for i, c in enumerate(per):
+        print(f"   step {i + 2:3d}: misses {c['threshold_misses'] / nb:6.3f}  too_low {c['threshold_too_low'] / nb:6.3f}"
+              f"  exactq/blk {c['exact_quotient_elems'] / nb:6.2f}  fallback {c['select_fallback_blocks']}")
     del eng, p, g
     torch.cuda.empty_cache()
