@@ -53,6 +53,12 @@ constexpr int kTargetHits = 64;           // carried-threshold target count (k_b
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2_keep(const void* p, uint32_t bytes) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+                 : "memory");
+}
 
 // Per-warp shared-memory carve-up (bytes; host and device agree).
 struct WLayout {
@@ -335,12 +341,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
 
     // ---- prologue: start the block's HBM reads; bucket grids (quantize.cpp:7-13) ----
     if (lane == 0) {
-        prefetch_l2(static_cast<const unsigned char*>(p.grads) + base * gsz, kBlk * gsz);
-        prefetch_l2(p.codes + base / 2, kBlk / 2);
+        prefetch_l2_keep(static_cast<const unsigned char*>(p.grads) + base * gsz, kBlk * gsz);
+        prefetch_l2_keep(p.codes + base / 2, kBlk / 2);
         prefetch_l2(p.meta + base / BUCKET, (kBlk / BUCKET) * 16);
-        prefetch_l2(gwi, uint32_t(m * kbs * 2));
-        prefetch_l2(gwv, uint32_t(m * kbs * vsz));
-        prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
     }
     for (int i = lane; i < kBlk / BUCKET; i += 32) {
         const double2 mt = p.meta[base / BUCKET + i];
@@ -390,6 +393,11 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
             cm2 = __funnelshift_r(cm2, cm3, 8);
             cm3 = (cm3 >> 8) | (m8 << 24);
         }
+    }
+    if (lane == 0) {
+        prefetch_l2(gwi, uint32_t(m * kbs * 2));
+        prefetch_l2(gwv, uint32_t(m * kbs * vsz));
+        prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
     }
     const uint32_t kmax = __reduce_max_sync(0xFFFFFFFFu, max(kmax2 & 0xFFFFu, kmax2 >> 16));
     if (p.check_finite && kmax >= 0x7FF0u && lane == 0) atomicOr(p.flag, 1u);  // inf/NaN in g or a
@@ -707,8 +715,8 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
                 rep[0] += x[i] * x[i];
             }
         }
-        *reinterpret_cast<uint32_t*>(p.codes + ((base + e0) >> 1)) = word;
-        if ((lane & (LPB - 1)) == 0) p.meta[(base + e0) / BUCKET] = make_double2(lo, hi);
+        __stcs(reinterpret_cast<unsigned int*>(p.codes + ((base + e0) >> 1)), word);
+        if ((lane & (LPB - 1)) == 0) __stcs(p.meta + (base + e0) / BUCKET, make_double2(lo, hi));
     }
     if constexpr (want_report) {
 #pragma unroll
