@@ -48,7 +48,8 @@ constexpr int kIter = kBlk / 256;         // iterations of 8 elements per lane
 constexpr int kCapL = 4;                  // candidate slots per lane
 constexpr int kCap = 32 * kCapL;          // candidate capacity of the exact stage
 constexpr uint32_t kGuard = 64;           // fixed-point guard band (units of 2^-20)
-constexpr int kTargetHits = 64;           // carried-threshold target count (k_b <= hits <= kCap)
+constexpr int kTargetHits = 64;
+constexpr int kDupCap = kCap * 2;         // ordered duplicate-entry list (ints in the candidate area)           // carried-threshold target count (k_b <= hits <= kCap)
 
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -311,6 +312,76 @@ __device__ __noinline__ int slow_select(const StepArgs* pp, unsigned char* ws, i
     return -1;
 }
 
+// ADAM_STATS + update of the duplicated window coordinates (window.cpp:28-46,
+// optim.cpp:183-187), out of line: one claimant per coordinate sums its
+// entries in physical slot order — from the ordered duplicate list when it
+// fit (ndup <= capacity), else by binary search in the ascending rows.
+// Returns the number of nonzero updates (report field 4).
+template <class KT>
+__device__ __noinline__ double dup_stats(const StepArgs* pp, unsigned char* ws, int64_t b, int ndup,
+                                         int nent) {
+    const StepArgs& p = *pp;
+    const WLayout L(KT::BUCKET);
+    const int lane = threadIdx.x & 31;
+    const int kb = p.per_block_k, kbs = p.kb_stride, filled = p.filled;
+    constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
+    const int64_t went = b * p.m * static_cast<int64_t>(kbs);
+    const int16_t* gwi = p.win_idx + went;
+    const unsigned char* gwv = static_cast<const unsigned char*>(p.win_val) + went * vsz;
+    const int64_t base = b * kBlk;
+    const int* dupl = reinterpret_cast<const int*>(ws + L.cval);
+    uint32_t* s_seen = reinterpret_cast<uint32_t*>(ws + L.wpref);
+    const uint32_t* s_dup = reinterpret_cast<const uint32_t*>(ws + L.dup);
+    const float inv_kb = 1.0f / static_cast<float>(kb);
+    const bool listed = ndup <= kDupCap;
+    const int n = listed ? ndup : nent;
+    double nnz = 0.0;
+    for (int q = lane; q < n; q += 32) {
+        int idx;
+        if (listed) {
+            idx = dupl[q] >> 16;
+        } else {
+            const int r = row_of(q, kb, inv_kb);
+            idx = gwi[r * kbs + (q - r * kb)];
+            if (!((s_dup[idx >> 5] >> (idx & 31)) & 1u)) continue;
+        }
+        const uint32_t bit = 1u << (idx & 31);
+        if (!(atomicAnd(&s_seen[idx >> 5], ~bit) & bit)) continue;  // another entry claimed it
+        double z1 = 0.0, z2 = 0.0;
+        if (listed) {
+            for (int q2 = 0; q2 < ndup; ++q2) {  // list order = physical slot order (window.cpp:32-39)
+                const int x = dupl[q2];
+                if ((x >> 16) != idx) continue;
+                const int rr = (x >> 8) & 0xFF;
+                const double v = ld_t<KT::VDT>(gwv, rr * kbs + (x & 0xFF));
+                z1 = __dadd_rn(z1, __dmul_rn(p.w1[rr], v));
+                z2 = __dadd_rn(z2, __dmul_rn(p.w2[rr], __dmul_rn(v, v)));
+            }
+        } else {
+            for (int rr = 0; rr < filled; ++rr) {  // physical slot order (window.cpp:32-39)
+                const int16_t* row = gwi + rr * kbs;
+                int lo_i = 0, hi_i = kb;
+                while (lo_i < hi_i) {
+                    const int mid = (lo_i + hi_i) >> 1;
+                    if (row[mid] < idx) lo_i = mid + 1; else hi_i = mid;
+                }
+                if (lo_i < kb && row[lo_i] == idx) {
+                    const double v = ld_t<KT::VDT>(gwv, rr * kbs + lo_i);
+                    z1 = __dadd_rn(z1, __dmul_rn(p.w1[rr], v));
+                    z2 = __dadd_rn(z2, __dmul_rn(p.w2[rr], __dmul_rn(v, v)));
+                }
+            }
+        }
+        const double mhat = __dmul_rn(z1, p.scale1);
+        const double vhat = __dmul_rn(z2, p.scale2);
+        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+        const double th = ld_t<KT::PDT>(p.params, base + idx);
+        st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
+        nnz += u != 0.0 ? 1.0 : 0.0;
+    }
+    return nnz;
+}
+
 template <class KT>
 __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __grid_constant__ StepArgs p) {
     constexpr int BUCKET = KT::BUCKET, LPB = KT::LPB;
@@ -410,10 +481,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
     if (T != 0 && cnt >= kb && cnt <= kCap) {
         int total;
         int pos = warp_excl_scan(nmine, lane, total);
-        const uint32_t cms[4] = {cm0, cm1, cm2, cm3};
-#pragma unroll
+#pragma unroll 1
         for (int w = 0; w < 4; ++w) {
-            uint32_t bits = cms[w];
+            uint32_t bits = w == 0 ? cm0 : (w == 1 ? cm1 : (w == 2 ? cm2 : cm3));
             while (bits) {
                 const int s = __ffs(bits) - 1;
                 bits &= bits - 1;
@@ -551,27 +621,19 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
         if (atomicOr(&s_seen[idx >> 5], bit) & bit) atomicOr(&s_dup[idx >> 5], bit);
     }
     __syncwarp();
-    auto update = [&](int idx, double z1, double z2) {
-        const double mhat = __dmul_rn(z1, p.scale1);
-        const double vhat = __dmul_rn(z2, p.scale2);
-        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
-        const double th = ld_t<KT::PDT>(p.params, base + idx);
-        st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
-        if (want_report && u != 0.0) rep[4] += 1.0;
-    };
     // Entries of duplicated coordinates go to an ordered list (warp ballots in
     // entry order = (slot, position) order); one claimant per coordinate then
     // sums its entries in list order, i.e. physical slot order.
     int* dupl = reinterpret_cast<int*>(s_cval);  // candidates are dead
-    constexpr int qcap = kCap * 2;
+    constexpr int qcap = kDupCap;
     int ndup = 0;
-    // unique coordinates, four entries per lane in flight (θ loads overlap)
-    for (int t0 = 0; t0 < nent; t0 += 4 * 32) {
-        int idx[4], e[4], r[4];
-        bool mine[4];
-        double th[4];
+    // unique coordinates, two entries per lane in flight (θ loads overlap)
+    for (int t0 = 0; t0 < nent; t0 += 2 * 32) {
+        int idx[2], e[2], r[2];
+        bool mine[2];
+        double th[2];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 2; ++k) {
             const int t = t0 + k * 32 + lane;
             mine[k] = false;
             r[k] = 0;
@@ -591,9 +653,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
             ndup += __popc(bal);
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) th[k] = mine[k] ? ld_t<KT::PDT>(p.params, base + idx[k]) : 0.0;
+        for (int k = 0; k < 2; ++k) th[k] = mine[k] ? ld_t<KT::PDT>(p.params, base + idx[k]) : 0.0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 2; ++k) {
             if (!mine[k]) continue;
             const double v = ld_t<KT::VDT>(gwv, e[k]);
             const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r[k]], v)), p.scale1);
@@ -604,46 +666,8 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
         }
     }
     __syncwarp();
-    if (ndup <= qcap) {
-        for (int q = lane; q < ndup; q += 32) {
-            const int idx = dupl[q] >> 16;
-            const uint32_t bit = 1u << (idx & 31);
-            if (!(atomicAnd(&s_seen[idx >> 5], ~bit) & bit)) continue;  // another entry claimed it
-            double z1 = 0.0, z2 = 0.0;
-            for (int q2 = 0; q2 < ndup; ++q2) {  // list order = physical slot order (window.cpp:32-39)
-                const int x = dupl[q2];
-                if ((x >> 16) != idx) continue;
-                const int rr = (x >> 8) & 0xFF;
-                const double v = ld_t<KT::VDT>(gwv, rr * kbs + (x & 0xFF));
-                z1 = __dadd_rn(z1, __dmul_rn(p.w1[rr], v));
-                z2 = __dadd_rn(z2, __dmul_rn(p.w2[rr], __dmul_rn(v, v)));
-            }
-            update(idx, z1, z2);
-        }
-    } else {  // list overflow (pathological windows): binary search per claimant
-        for (int t = lane; t < nent; t += 32) {
-            const int r = row_of(t, kb, inv_kb);
-            const int idx = gwi[r * kbs + (t - r * kb)];
-            const uint32_t bit = 1u << (idx & 31);
-            if (!((s_dup[idx >> 5] >> (idx & 31)) & 1u)) continue;
-            if (!(atomicAnd(&s_seen[idx >> 5], ~bit) & bit)) continue;
-            double z1 = 0.0, z2 = 0.0;
-            for (int rr = 0; rr < filled; ++rr) {  // physical slot order (window.cpp:32-39)
-                const int16_t* row = gwi + rr * kbs;
-                int lo_i = 0, hi_i = kb;
-                while (lo_i < hi_i) {
-                    const int mid = (lo_i + hi_i) >> 1;
-                    if (row[mid] < idx) lo_i = mid + 1; else hi_i = mid;
-                }
-                if (lo_i < kb && row[lo_i] == idx) {
-                    const double v = ld_t<KT::VDT>(gwv, rr * kbs + lo_i);
-                    z1 = __dadd_rn(z1, __dmul_rn(p.w1[rr], v));
-                    z2 = __dadd_rn(z2, __dmul_rn(p.w2[rr], __dmul_rn(v, v)));
-                }
-            }
-            update(idx, z1, z2);
-        }
-    }
+    const double dn = dup_stats<KT>(&p, ws, b, ndup, nent);
+    if (want_report) rep[4] += dn;
 
     // ---- pass 2: residual (compress.cpp:95-102) + 4-bit re-quantization
     //      (quantize.cpp:15-24, 42-55, 102-114, 142-162) ----
