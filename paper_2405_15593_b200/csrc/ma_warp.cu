@@ -217,15 +217,20 @@ __device__ __noinline__ int slow_select(const StepArgs* pp, unsigned char* ws, i
 #pragma unroll
         for (int k = 0; k < 4; ++k) hist[lane * 4 + k] = 0;
         __syncwarp();
+        uint64_t kmx = 0;
         for (int j = 0; j < kIter; ++j) {
             double a[8];
             block_a(j, a);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const uint64_t k = key_of(a[i]);
+                kmx = k > kmx ? k : kmx;
                 if ((k & pmask) == prefix) atomicAdd(&hist[(k >> sh) & 127u], 1u);
             }
         }
+        // inf/NaN in g or a (the fast path checks its candidates instead)
+        if (sh == 56 && p.check_finite && __any_sync(0xFFFFFFFFu, (kmx >> 48) >= 0x7FF0u) && lane == 0)
+            atomicOr(p.flag, 1u);
         __syncwarp();
         // digit d: the largest with #{digit >= d} >= need (suffix sums from the top)
         const uint32_t h0 = hist[lane * 4], h1 = hist[lane * 4 + 1], h2 = hist[lane * 4 + 2],
@@ -431,9 +436,8 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
     // carried state: low 16 bits = key16 threshold, high 16 = hits it was chosen for
     const uint32_t tstate = __ldg(p.thresh + b);
     const uint32_t T = tstate & 0xFFFFu;
-    const uint32_t tt = T | (T << 16);
+    const uint32_t T2 = T << 17;
     uint32_t cm0 = 0, cm1 = 0, cm2 = 0, cm3 = 0;  // candidate bits: byte j = iteration j
-    uint32_t kmax2 = 0;
     double rep[kReportFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
     {
         Raw8<KT::GDT> nr = load_raw8<KT::GDT>(p.grads, base + lane * 8);
@@ -452,12 +456,11 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
             add_decoded8(a, cw, s_ll[e0 / BUCKET]);
             uint32_t m8 = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t w = (hi_key(a[2 * k]) >> 16) | (hi_key(a[2 * k + 1]) & 0xFFFF0000u);
-                kmax2 = __vmaxu2(kmax2, w);
-                const uint32_t c = __vcmpgeu2(w, tt);
-                m8 |= ((c & 1u) | ((c >> 15) & 2u)) << (2 * k);
-                if (want_report) rep[1] += a[2 * k] * a[2 * k] + a[2 * k + 1] * a[2 * k + 1];
+            for (int i = 0; i < 8; ++i) {
+                // bits 62..31 of a: key16 >= T  <=>  (|a| bits >> 31) >= T << 17
+                const uint32_t h2 = static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(a[i])) >> 31);
+                m8 |= static_cast<uint32_t>(h2 >= T2) << i;
+                if (want_report) rep[1] += a[i] * a[i];
             }
             cm0 = __funnelshift_r(cm0, cm1, 8);
             cm1 = __funnelshift_r(cm1, cm2, 8);
@@ -470,8 +473,6 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
         prefetch_l2(gwv, uint32_t(m * kbs * vsz));
         prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
     }
-    const uint32_t kmax = __reduce_max_sync(0xFFFFFFFFu, max(kmax2 & 0xFFFFu, kmax2 >> 16));
-    if (p.check_finite && kmax >= 0x7FF0u && lane == 0) atomicOr(p.flag, 1u);  // inf/NaN in g or a
     const int nmine = __popc(cm0) + __popc(cm1) + __popc(cm2) + __popc(cm3);
     const int cnt = __reduce_add_sync(0xFFFFFFFFu, nmine);
 
@@ -518,8 +519,11 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
             for (int s = 0; s < kCapL; ++s) c += kh[s] >= v;
             return __reduce_add_sync(0xFFFFFFFFu, c);
         };
+        // the candidates hold every key >= T, so also the block's largest
+        const uint32_t kmaxc = __reduce_max_sync(0xFFFFFFFFu, max(max(kh[0], kh[1]), max(kh[2], kh[3])));
+        if (p.check_finite && kmaxc >= 0x7FF00000u && lane == 0) atomicOr(p.flag, 1u);  // inf/NaN in g or a
         // bisect the k_b-th largest high word: count(lo) >= kb > count(hi)
-        uint32_t lo = lo32, hi = (kmax + 1) << 16;
+        uint32_t lo = lo32, hi = kmaxc + 1;
         while (hi - lo > 1) {
             const uint32_t mid = lo + (hi - lo) / 2;
             if (count_ge(mid) >= kb) lo = mid; else hi = mid;

@@ -355,3 +355,30 @@ def test_persistent_spikes_duplicate_window_coordinates(kernel):
 def test_warp_kernel_shapes(density, m):
     run_parity(4096 * 9, dict(lr=1e-2, density=density, window=m), gdt="bf16", pdt="bf16",
                vdt="bf16", steps=min(m + 3, 20))
+
+
+@pytest.mark.parametrize("bad", [np.inf, -np.inf, np.nan])
+def test_nonfinite_flag_after_warm_threshold(bad):
+    # the fast path (carried threshold) is active from step ~3: a non-finite
+    # gradient there must still raise the flag (exact re-check on that path).
+    from paper_2405_15593_b200 import InvalidArgument, MicroAdam
+    d = 4096 * 6
+    eng = MicroAdam(d, dict(lr=1e-2), param_dtype="bf16", grad_dtype="bf16", value_dtype="bf16",
+                    finite_mode="flag")
+    params = _dev(oracle.synth(1, 0, 0, d, "bf16"), "bf16")
+    for s in range(1, 7):
+        eng.step(params, _dev(oracle.synth(42, s, 0, d, "bf16"), "bf16"), 1e-2)
+    eng.synchronize()
+    g = oracle.synth(42, 7, 0, d, "bf16")
+    g[4096 * 3 + 77] = bad
+    eng.step(params, _dev(g, "bf16"), 1e-2)
+    with pytest.raises(InvalidArgument):
+        eng.synchronize()
+
+
+@pytest.mark.parametrize("scale", [2.0 ** 120, 2.0 ** -130, 2.0 ** 300])
+def test_fp64_magnitudes_outside_fp32_filter(scale):
+    # |a| beyond the fp32 filter's safe range (or in fp32 denormals): the
+    # kernel must fall back to the exact path and stay bit-exact.
+    run_parity(4096 * 5, dict(lr=1e-3), gdt="f64", pdt="f64", vdt="f64", steps=6,
+               grad_fn=lambda s: oracle.synth(7, s, 0, 4096 * 5) * scale)
