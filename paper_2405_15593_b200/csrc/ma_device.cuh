@@ -15,18 +15,16 @@ __device__ __forceinline__ uint64_t key_of(double x) {
     return static_cast<uint64_t>(__double_as_longlong(x)) & kAbsMask;
 }
 
-// Round-to-nearest-even of a double to bfloat16, returned as the (exactly
-// representable) double. Same rule as oracle/microadam_oracle.c:mo_bf16_round.
+// Round-to-nearest-even of a double to bfloat16 (one rounding, subnormals and
+// overflow to inf included: the sm_100 F2F.BF16.F64 conversion), returned as the
+// exactly representable double. Same rule as oracle/microadam_oracle.c:mo_bf16_round.
+__device__ __forceinline__ uint16_t bf16_bits(double x) {
+    uint16_t r;
+    asm("{ .reg .b16 t; cvt.rn.bf16.f64 t, %1; mov.b16 %0, t; }" : "=h"(r) : "d"(x));
+    return r;
+}
 __device__ __forceinline__ double bf16_round(double x) {
-    if (!isfinite(x) || x == 0.0) return x;
-    if (fabs(x) < 0x1p-126) return __dmul_rn(rint(__dmul_rn(x, 0x1p133)), 0x1p-133);
-    uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
-    const uint64_t lsb = (u >> 45) & 1u;
-    u += ((uint64_t(1) << 44) - 1u) + lsb;
-    u &= ~((uint64_t(1) << 45) - 1u);
-    const double y = __longlong_as_double(static_cast<long long>(u));
-    if (fabs(y) >= 0x1p128) return copysign(__longlong_as_double(0x7FF0000000000000ll), x);
-    return y;
+    return static_cast<double>(__uint_as_float(static_cast<uint32_t>(bf16_bits(x)) << 16));
 }
 
 __device__ __forceinline__ double round_to(double x, int dt) {
@@ -65,8 +63,7 @@ __device__ __forceinline__ void st_val(void* p, int dt, int64_t i, double x) {
     } else if (dt == F32) {
         static_cast<float*>(p)[i] = __double2float_rn(x);
     } else {
-        const float f = static_cast<float>(bf16_round(x));  // exact
-        static_cast<uint16_t*>(p)[i] = static_cast<uint16_t>(__float_as_uint(f) >> 16);
+        static_cast<uint16_t*>(p)[i] = bf16_bits(x);
     }
 }
 
@@ -81,8 +78,7 @@ template <int DT>
 __device__ __forceinline__ void st_t(void* p, int64_t i, double x) {
     if constexpr (DT == F64) static_cast<double*>(p)[i] = x;
     else if constexpr (DT == F32) static_cast<float*>(p)[i] = __double2float_rn(x);
-    else static_cast<uint16_t*>(p)[i] =
-        static_cast<uint16_t>(__float_as_uint(static_cast<float>(bf16_round(x))) >> 16);
+    else static_cast<uint16_t*>(p)[i] = bf16_bits(x);
 }
 template <int DT>
 __device__ __forceinline__ double round_t(double x) {
