@@ -391,7 +391,7 @@ def run_ours(args):
                          "kernel_ms_per_step": [round(a.elapsed_time(b_), 3) for a, b_ in kev],
                          "peak_source": peak_src,
                          "traffic_source": traffic_src,
-                         "kernel": "microadam_step_fast (fused decode/Top-K/requant/window/ADAM_STATS/update)"},
+                         "kernel": "microadam_step_warp (warp per Top-K block: fused EF decode, Top-K, window, ADAM_STATS, update, 4-bit requant)"},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,

@@ -442,7 +442,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     alloc(reinterpret_cast<void**>(&h->d_report), ma::kReportFields * sizeof(double));
     alloc(reinterpret_cast<void**>(&h->d_thresh), size_t(nb) * sizeof(uint32_t));
     const char* dbg = std::getenv("MA_DEBUG_COUNTERS");
-    if (dbg && dbg[0] == '1') alloc(reinterpret_cast<void**>(&h->d_dbg), 4 * sizeof(unsigned));
+    if (dbg && dbg[0] == '1') alloc(reinterpret_cast<void**>(&h->d_dbg), 8 * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         free_handle(h);
@@ -693,12 +693,12 @@ int64_t ma_kernel_launches(const ma_handle* h) { return h ? h->launches : 0; }
 ma_status ma_debug_counters(ma_handle* h, int64_t* out, int n) {
     if (!h || !out || n < 0) return fail(MA_ERR_INVALID_ARG, "bad argument");
     DeviceGuard g(h->device);
-    unsigned v[4] = {0, 0, 0, 0};
+    unsigned v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (h->d_dbg) {
         MA_CUDA(cudaDeviceSynchronize());
         MA_CUDA(cudaMemcpy(v, h->d_dbg, sizeof(v), cudaMemcpyDeviceToHost));
     }
-    for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
+    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
     return MA_OK;
 }
 

@@ -48,8 +48,9 @@ constexpr int kIter = kBlk / 256;         // iterations of 8 elements per lane
 constexpr int kCapL = 4;                  // candidate slots per lane
 constexpr int kCap = 32 * kCapL;          // candidate capacity of the exact stage
 constexpr uint32_t kGuard = 64;           // fixed-point guard band (units of 2^-20)
-constexpr int kTargetHits = 64;
-constexpr int kDupCap = kCap * 2;         // ordered duplicate-entry list (ints in the candidate area)           // carried-threshold target count (k_b <= hits <= kCap)
+constexpr int kTargetHits = 64;           // carried-threshold target count (k_b <= hits <= kCap)
+constexpr int kDupCap = kCap * 2;         // ordered duplicate-entry list (ints in the candidate area)
+constexpr int kRefineMax = 1024;          // hits at T refined from the hit mask (else radix path)
 
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -479,7 +480,60 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
     // ---- block Top-K (compress.cpp:39-53, 73-85) ----
     int ncand = -1;
     uint32_t lo32 = T << 16;
-    if (T != 0 && cnt >= kb && cnt <= kCap) {
+    bool refined = false;
+    if (T != 0 && cnt > kCap && cnt <= kRefineMax) {
+        // Too many hits at T (the |a| distribution moved up): refine from the hit
+        // mask instead of re-reading the block. A histogram of key16 - T over the
+        // hits gives the largest T' = T + d with >= k_b hits; the hits at or
+        // above T' become the candidates (still a superset of the top k_b).
+        uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.cval);  // dead until the gather
+        hist[lane] = 0;
+        __syncwarp();
+        auto for_hits = [&](auto&& f) {
+#pragma unroll 1
+            for (int w = 0; w < 4; ++w) {
+                uint32_t bits = w == 0 ? cm0 : (w == 1 ? cm1 : (w == 2 ? cm2 : cm3));
+                while (bits) {
+                    const int sb = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const int e = (w * 4 + (sb >> 3)) * 256 + lane * 8 + (sb & 7);
+                    f(e, recompute_a<KT>(p, base, s_ll, e));
+                }
+            }
+        };
+        for_hits([&](int, double a) { atomicAdd(&hist[min((hi_key(a) >> 16) - T, 31u)], 1u); });
+        __syncwarp();
+        int sfx = static_cast<int>(hist[lane]);  // #hits with key16 - T >= lane
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_down_sync(0xFFFFFFFFu, sfx, off);
+            if (lane + off < 32) sfx += t;
+        }
+        const uint32_t ok = __ballot_sync(0xFFFFFFFFu, sfx >= kb);  // bit 0 always set
+        const int d = 31 - __clz(ok);
+        const int n = __shfl_sync(0xFFFFFFFFu, sfx, d);
+        __syncwarp();
+        if (n <= kCap) {
+            const uint32_t T1 = T + static_cast<uint32_t>(d);
+            if (lane == 0) s_misc[4] = 0;
+            __syncwarp();
+            for_hits([&](int e, double a) {
+                if ((hi_key(a) >> 16) >= T1) {
+                    const int q = atomicAdd(&s_misc[4], 1);
+                    s_cval[q] = a;
+                    s_cidx[q] = static_cast<int16_t>(e);
+                }
+            });
+            __syncwarp();
+            ncand = n;
+            lo32 = T1 << 16;
+            refined = true;
+        }
+        if (p.dbg && lane == 0) atomicAdd(p.dbg + 6, 1u);
+    }
+    if (refined) {
+        // candidates gathered by the refinement
+    } else if (T != 0 && cnt >= kb && cnt <= kCap) {
         int total;
         int pos = warp_excl_scan(nmine, lane, total);
 #pragma unroll 1
@@ -670,6 +724,10 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
         }
     }
     __syncwarp();
+    if (p.dbg && lane == 0) {
+        atomicAdd(p.dbg + 5, static_cast<unsigned>(ndup));
+        if (ndup > kDupCap) atomicAdd(p.dbg + 4, 1u);
+    }
     const double dn = dup_stats<KT>(&p, ws, b, ndup, nent);
     if (want_report) rep[4] += dn;
 

@@ -382,3 +382,10 @@ def test_fp64_magnitudes_outside_fp32_filter(scale):
     # kernel must fall back to the exact path and stay bit-exact.
     run_parity(4096 * 5, dict(lr=1e-3), gdt="f64", pdt="f64", vdt="f64", steps=6,
                grad_fn=lambda s: oracle.synth(7, s, 0, 4096 * 5) * scale)
+
+
+def test_bf16_subnormal_window_values():
+    # window values below 2^-126 round to bf16 subnormals (F2F.BF16.F64 on the
+    # device vs the oracle's software RNE).
+    run_parity(4096 * 3, dict(lr=1e-3), gdt="f64", pdt="f64", vdt="bf16", steps=5,
+               grad_fn=lambda s: oracle.synth(5, s, 0, 4096 * 3) * 2.0 ** -133)

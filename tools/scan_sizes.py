@@ -21,7 +21,8 @@ for d in sizes:
     prev = None
     per = []
     for i in range(int(os.environ.get("SCAN_STEPS", "12"))):
-        ma._capi.check(L.ma_fill_synthetic(g.data_ptr(), 2, d, 42, i + 1, 0, 0, s))
+        cyc = int(os.environ.get("SCAN_CYCLE", "0"))  # >0: gradients repeat with this period (bench.py)
+        ma._capi.check(L.ma_fill_synthetic(g.data_ptr(), 2, d, 42, (i % cyc if cyc else i) + 1, 0, 0, s))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         eng.step(p, g, 1e-3)
@@ -40,6 +41,7 @@ for d in sizes:
     nb = d // 4096
     for i, c in enumerate(per):
         print(f"   step {i + 2:3d}: misses {c['threshold_misses'] / nb:6.3f}  too_low {c['threshold_too_low'] / nb:6.3f}"
-              f"  exactq/blk {c['exact_quotient_elems'] / nb:6.2f}  fallback {c['select_fallback_blocks']}")
+              f"  exactq/blk {c['exact_quotient_elems'] / nb:6.2f}  fallback {c['select_fallback_blocks']}"
+              f"  refine {c['threshold_refinements'] / nb:6.3f}  dup/blk {c['dup_entries'] / nb:6.1f}  dup-overflow {c['dup_list_overflow_blocks'] / nb:6.3f}")
     del eng, p, g
     torch.cuda.empty_cache()
