@@ -158,6 +158,7 @@ struct ma_handle {
     ma::Variant tail_variant{};  // generic kernel for the partial tail block (fast path)
     bool fast = false;  // ma_fast.cu / ma_warp.cu kernel (else the generic ma_kernels.cu kernel)
     bool warp = false;  // fast path runs the warp-per-block kernel (ma_warp.cu)
+    bool warp_exact = false;  // MA_WARP_EXACT=1: never the fp32-screened (lean) warp kernel
     int persist_grid = 0;
     int device = 0;
     uint8_t* d_codes = nullptr;
@@ -258,6 +259,7 @@ void base_args(ma_handle* h, ma::StepArgs* a) {
     a->p_dtype = h->cfg.param_dtype;
     a->v_dtype = h->cfg.value_dtype;
     a->eps = h->cfg.hp.eps;
+    a->force_exact = h->warp_exact ? 1 : 0;
 }
 
 // Fast path: the persistent kernel takes the range's full blocks and the
@@ -423,6 +425,8 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
                          int(s.kb_stride), cfg->grad_dtype, cfg->param_dtype, cfg->value_dtype) &&
         ma::warp_smem_bytes(int(s.bucket)) <= size_t(smem_max))
         h->warp = true;
+    const char* warp_exact = std::getenv("MA_WARP_EXACT");
+    h->warp_exact = warp_exact && warp_exact[0] == '1';
     if (!h->fast) h->variant = h->tail_variant;
     if (smem > size_t(smem_max)) {
         delete h;

@@ -35,7 +35,7 @@ struct StepArgs {
     int64_t block_count;  // blocks [block_offset, block_offset + block_count) (persistent kernel)
     int32_t block, per_block_k, kb_stride, bucket;
     int32_t m, filled, slot, check_finite;
-    int32_t g_dtype, p_dtype, v_dtype, pad0;
+    int32_t g_dtype, p_dtype, v_dtype, force_exact;  // force_exact: warp kernel without the fp32 screen (A/B, tests)
     double eps, lr, scale1, scale2;
     double w1[kMaxWindow];
     double w2[kMaxWindow];

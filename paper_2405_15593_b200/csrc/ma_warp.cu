@@ -37,6 +37,8 @@
 #include "ma_device.cuh"
 #include "ma_internal.h"
 
+#include <math_constants.h>
+
 namespace ma {
 namespace {
 
@@ -195,10 +197,10 @@ __device__ __noinline__ uint32_t exact_code_w(double x, double lo, double level)
 // tied at the k_b-th key, the exact selection — every key above it plus the
 // lowest-index ties (compress.cpp:43-48) — is written to the selection bitmap
 // directly and -1 is returned (misc[1] = the k_b-th key's high word).
-template <class KT>
+template <class KT, class LAY>
 __device__ __noinline__ int slow_select(const StepArgs* pp, unsigned char* ws, int64_t b) {
     const StepArgs& p = *pp;
-    const WLayout L(KT::BUCKET);
+    const LAY L(KT::BUCKET);
     const int lane = threadIdx.x & 31;
     const int64_t base = b * kBlk;
     const double2* s_ll = reinterpret_cast<const double2*>(ws + L.ll);
@@ -323,11 +325,11 @@ __device__ __noinline__ int slow_select(const StepArgs* pp, unsigned char* ws, i
 // entries in physical slot order — from the ordered duplicate list when it
 // fit (ndup <= capacity), else by binary search in the ascending rows.
 // Returns the number of nonzero updates (report field 4).
-template <class KT>
+template <class KT, class LAY>
 __device__ __noinline__ double dup_stats(const StepArgs* pp, unsigned char* ws, int64_t b, int ndup,
                                          int nent) {
     const StepArgs& p = *pp;
-    const WLayout L(KT::BUCKET);
+    const LAY L(KT::BUCKET);
     const int lane = threadIdx.x & 31;
     const int kb = p.per_block_k, kbs = p.kb_stride, filled = p.filled;
     constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
         ncand = cnt;
         __syncwarp();
     } else {
-        ncand = slow_select<KT>(&p, ws, b);
+        ncand = slow_select<KT, WLayout>(&p, ws, b);
         if (p.dbg && lane == 0) {
             atomicAdd(p.dbg + 2, 1u);
             if (cnt > kCap) atomicAdd(p.dbg + 3, 1u);
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
         atomicAdd(p.dbg + 5, static_cast<unsigned>(ndup));
         if (ndup > kDupCap) atomicAdd(p.dbg + 4, 1u);
     }
-    const double dn = dup_stats<KT>(&p, ws, b, ndup, nent);
+    const double dn = dup_stats<KT, WLayout>(&p, ws, b, ndup, nent);
     if (want_report) rep[4] += dn;
 
     // ---- pass 2: residual (compress.cpp:95-102) + 4-bit re-quantization
@@ -835,6 +837,605 @@ cudaError_t launch_kw(const StepArgs& a, cudaStream_t s) {
 
 constexpr int dtype_key_w(int g, int p, int v) { return g * 9 + p * 3 + v; }
 
+// ===========================================================================
+// Lean path (bf16 / f32 gradients, no StepReport): the per-element streaming
+// work runs in fp32 with proven error bounds, and every decision that the
+// fp32 values cannot settle is taken again in the reference's fp64
+// arithmetic. Results are bit-identical to the exact kernel above.
+//
+// Error bound. For bucket q with previous (lo, hi) and M = max(|lo|, |hi|),
+// the fp32 decode e32 = fma(c - 0, rn(level), rn(lo)) and a32 = g + e32 obey
+//     |a32 - a| <= E_q + |a32| * 2^-23,   E_q = M * 2^-21 + 2^-120
+// (3 roundings of at most M * 2^-24 each in e32, one of |a| * 2^-24 in a32,
+// the absolute term covers fp32 subnormals). Buckets with M >= 2^100 (or
+// non-finite) get E_q = inf, which sends every decision of that bucket to the
+// fp64 path.
+//   * Top-K screen: |a| >= V_T (key16 >= T) implies |a32| >= Tf_q with
+//     Tf_q = rd((V_T - E_q) * (1 - 2^-22)); hits are a superset of the keys
+//     at or above the carried threshold and are re-evaluated exactly.
+//   * Bucket min / max of the residual: the exact minimum lies among the
+//     elements with r32 <= m32 + 2 eps (eps = E_q + max|r32| * 2^-22), which
+//     are re-evaluated in fp64 (usually one element per bucket).
+//   * 4-bit code: t = (r32 - m32) * 15 / (M32 - m32) estimates
+//     q = (r - lo) / level within E_t <= 120 eps / R + 2^-15 (R = M32 - m32,
+//     R > 8 eps required); a 18-bit fixed-point read of t + 0.5 that lands
+//     within G = E_t of an integer is recomputed with the IEEE quotient
+//     (quantize.cpp:51-53).
+// ===========================================================================
+
+constexpr float kTwo23 = 8388608.0f;
+
+// Per-warp shared-memory carve-up of the lean kernel (bytes).
+struct LLayout {
+    uint32_t ll, llf, sel, wpref, dup, cval, cidx, misc, total;
+    __host__ __device__ LLayout() {}
+    __host__ __device__ explicit LLayout(int bucket) {
+        const size_t nbk = size_t(kBlk / bucket);
+        size_t o = 0;
+        ll = uint32_t(o);    o = align_up(o + nbk * 16, 16);     // exact (lo, level), fp64
+        llf = uint32_t(o);   o = align_up(o + nbk * 16, 16);     // (lo32, level32, E_q, Tf_q)
+        sel = uint32_t(o);   o = align_up(o + kBlk / 8, 16);
+        wpref = uint32_t(o); o = align_up(o + kBlk / 8, 16);    // member list; word prefix; seen bits
+        dup = uint32_t(o);   o = align_up(o + kBlk / 8, 16);
+        cval = uint32_t(o);  // candidates; radix histogram; bucket (lo, hi) keys; duplicate list
+        o = align_up(o + (size_t(kCap) * 8 > nbk * 16 ? size_t(kCap) * 8 : nbk * 16), 16);
+        cidx = uint32_t(o);  o = align_up(o + kCap * 2, 16);
+        misc = uint32_t(o);  o = align_up(o + 16 * 4, 16);
+        total = uint32_t(align_up(o, 128));
+    }
+};
+
+template <int DT>
+__device__ __forceinline__ void g32x8(const Raw8<DT>& r, float (&g)[8]) {
+    if constexpr (DT == BF16) {
+        const uint32_t w[4] = {r.v[0].x, r.v[0].y, r.v[0].z, r.v[0].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            g[2 * k] = __uint_as_float(w[k] << 16);
+            g[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            g[4 * k + 0] = __uint_as_float(r.v[k].x);
+            g[4 * k + 1] = __uint_as_float(r.v[k].y);
+            g[4 * k + 2] = __uint_as_float(r.v[k].z);
+            g[4 * k + 3] = __uint_as_float(r.v[k].w);
+        }
+    }
+}
+
+// a32 = g + (c * level32 + lo32) for 8 elements. The nibble becomes a float by
+// a byte permute into 2^23 + c (exact), no conversion instruction.
+template <int DT>
+__device__ __forceinline__ void a32x8(const Raw8<DT>& r, uint32_t cw, float lo32, float lv32, float (&a)[8]) {
+    float g[8];
+    g32x8<DT>(r, g);
+    const uint32_t ce = cw & 0x0F0F0F0Fu, co = (cw >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float c0 = __uint_as_float(__byte_perm(ce, 0x4B000000u, 0x7540u | k)) - kTwo23;
+        const float c1 = __uint_as_float(__byte_perm(co, 0x4B000000u, 0x7540u | k)) - kTwo23;
+        a[2 * k] = g[2 * k] + __fmaf_rn(c0, lv32, lo32);
+        a[2 * k + 1] = g[2 * k + 1] + __fmaf_rn(c1, lv32, lo32);
+    }
+}
+
+// Exact fp64 a of element i (runtime index) of a raw 8-group (same arithmetic
+// as add_decoded8: optim.cpp:166-168, quantize.cpp:164-178).
+template <int DT>
+__device__ __forceinline__ double exact_a_raw(const Raw8<DT>& r, uint32_t cw, int i, double2 ll) {
+    uint32_t bits;
+    if constexpr (DT == BF16) {
+        const int k = i >> 1;
+        const uint32_t w = k == 0 ? r.v[0].x : (k == 1 ? r.v[0].y : (k == 2 ? r.v[0].z : r.v[0].w));
+        bits = (i & 1) ? (w & 0xFFFF0000u) : (w << 16);
+    } else {
+        const uint4 v = (i >> 2) ? r.v[1] : r.v[0];
+        const int k = i & 3;
+        bits = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+    }
+    const double g = static_cast<double>(__uint_as_float(bits));
+    return __dadd_rn(g, __dadd_rn(__dmul_rn(static_cast<double>((cw >> (4 * i)) & 15u), ll.y), ll.x));
+}
+
+template <class KT>
+__global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __grid_constant__ StepArgs p) {
+    constexpr int BUCKET = KT::BUCKET, LPB = KT::LPB;
+    constexpr int gsz = KT::GDT == F32 ? 4 : 2;
+    constexpr int psz = KT::PDT == F64 ? 8 : (KT::PDT == F32 ? 4 : 2);
+    constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
+    constexpr int NBK = kBlk / BUCKET;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t bl = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+    if (bl >= p.block_count) return;
+    const int64_t b = p.block_offset + bl;
+    const int64_t base = b * kBlk;
+    const LLayout L(BUCKET);
+    unsigned char* ws = smem + warp * L.total;
+    double2* s_ll = reinterpret_cast<double2*>(ws + L.ll);
+    float4* s_llf = reinterpret_cast<float4*>(ws + L.llf);
+    uint32_t* s_sel = reinterpret_cast<uint32_t*>(ws + L.sel);
+    int* s_wpref = reinterpret_cast<int*>(ws + L.wpref);
+    int16_t* s_memb = reinterpret_cast<int16_t*>(ws + L.wpref);
+    uint32_t* s_seen = reinterpret_cast<uint32_t*>(ws + L.wpref);
+    uint32_t* s_dup = reinterpret_cast<uint32_t*>(ws + L.dup);
+    double* s_cval = reinterpret_cast<double*>(ws + L.cval);
+    int16_t* s_cidx = reinterpret_cast<int16_t*>(ws + L.cidx);
+    int* s_misc = reinterpret_cast<int*>(ws + L.misc);
+    const int kb = p.per_block_k, kbs = p.kb_stride, m = p.m, slot = p.slot, filled = p.filled;
+    const int64_t went = b * m * static_cast<int64_t>(kbs);
+    int16_t* gwi = p.win_idx + went;
+    unsigned char* gwv = static_cast<unsigned char*>(p.win_val) + went * vsz;
+
+    if (lane == 0) {
+        prefetch_l2_keep(static_cast<const unsigned char*>(p.grads) + base * gsz, kBlk * gsz);
+        prefetch_l2_keep(p.codes + base / 2, kBlk / 2);
+        prefetch_l2(p.meta + base / BUCKET, NBK * 16);
+    }
+    const uint32_t tstate = __ldg(p.thresh + b);
+    const uint32_t T = tstate & 0xFFFFu;
+    // V_T: the smallest |a| with key16 >= T (quantize-free: bits 62..48)
+    const double VT = __longlong_as_double(static_cast<long long>(static_cast<uint64_t>(T) << 48));
+    for (int i = lane; i < NBK; i += 32) {
+        const double2 mt = p.meta[base / BUCKET + i];
+        const double level = (mt.x == mt.y) ? 0.0 : __ddiv_rn(__dsub_rn(mt.y, mt.x), 15.0);
+        s_ll[i] = make_double2(mt.x, level);
+        const double M = fmax(fabs(mt.x), fabs(mt.y));
+        float E = __double2float_ru(M * 0x1p-21 + 0x1p-120);
+        if (!(M < 0x1p100)) E = CUDART_INF_F;
+        float Tf = CUDART_INF_F;  // T == 0: no carried threshold, no screen hits
+        if (T != 0) Tf = __double2float_rd((VT - static_cast<double>(E)) * (1.0 - 0x1p-22));
+        if (!(Tf > 0.0f)) Tf = 0.0f;
+        s_llf[i] = make_float4(__double2float_rn(mt.x), __double2float_rn(level), E, Tf);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        s_sel[lane * 4 + k] = 0;
+        s_dup[lane * 4 + k] = 0;
+    }
+    __syncwarp();
+
+    // ---- pass 1: fp32 screen of a = g + decode(EF) against the carried threshold ----
+    uint32_t cm0 = 0, cm1 = 0, cm2 = 0, cm3 = 0;
+    {
+        Raw8<KT::GDT> nr = load_raw8<KT::GDT>(p.grads, base + lane * 8);
+        uint32_t ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + lane * 8) >> 1));
+#pragma unroll 1
+        for (int j = 0; j < kIter; ++j) {
+            const int e0 = j * 256 + lane * 8;
+            const Raw8<KT::GDT> r = nr;
+            const uint32_t cw = ncw;
+            if (j + 1 < kIter) {
+                nr = load_raw8<KT::GDT>(p.grads, base + e0 + 256);
+                ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0 + 256) >> 1));
+            }
+            const float4 f = s_llf[e0 / BUCKET];
+            float a[8];
+            a32x8<KT::GDT>(r, cw, f.x, f.y, a);
+            uint32_t m8 = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m8 |= static_cast<uint32_t>(!(fabsf(a[i]) < f.w)) << i;
+            cm0 = __funnelshift_r(cm0, cm1, 8);
+            cm1 = __funnelshift_r(cm1, cm2, 8);
+            cm2 = __funnelshift_r(cm2, cm3, 8);
+            cm3 = (cm3 >> 8) | (m8 << 24);
+        }
+    }
+    const int nmine = __popc(cm0) + __popc(cm1) + __popc(cm2) + __popc(cm3);
+    const int cnt = __reduce_add_sync(0xFFFFFFFFu, nmine);
+    auto for_hits = [&](auto&& f) {
+#pragma unroll 1
+        for (int w = 0; w < 4; ++w) {
+            uint32_t bits = w == 0 ? cm0 : (w == 1 ? cm1 : (w == 2 ? cm2 : cm3));
+            while (bits) {
+                const int sb = __ffs(bits) - 1;
+                bits &= bits - 1;
+                f((w * 4 + (sb >> 3)) * 256 + lane * 8 + (sb & 7));
+            }
+        }
+    };
+
+    // ---- block Top-K (compress.cpp:39-53, 73-85) ----
+    // Candidates: a superset of the keys >= base16 (key16 units) whose exact
+    // values sit in s_cval / s_cidx; floor16: every key16 >= floor16 is a candidate.
+    int ncand = -1;
+    uint32_t base16 = T, floor16 = T;
+    if (T != 0 && cnt > kCap && cnt <= kRefineMax) {
+        // Overfull screen: refine from the hit mask (key16 histogram of the
+        // exact hits at or above T) instead of re-reading the block.
+        uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.cval);
+        hist[lane] = 0;
+        __syncwarp();
+        for_hits([&](int e) {
+            const uint32_t k16 = hi_key(recompute_a<KT>(p, base, s_ll, e)) >> 16;
+            if (k16 >= T) atomicAdd(&hist[min(k16 - T, 31u)], 1u);
+        });
+        __syncwarp();
+        int sfx = static_cast<int>(hist[lane]);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_down_sync(0xFFFFFFFFu, sfx, off);
+            if (lane + off < 32) sfx += t;
+        }
+        const uint32_t ok = __ballot_sync(0xFFFFFFFFu, sfx >= kb);
+        __syncwarp();
+        if (ok) {
+            const int d = 31 - __clz(ok);
+            const int n = __shfl_sync(0xFFFFFFFFu, sfx, d);
+            if (n <= kCap) {
+                const uint32_t T1 = T + static_cast<uint32_t>(d);
+                if (lane == 0) s_misc[4] = 0;
+                __syncwarp();
+                for_hits([&](int e) {
+                    const double a = recompute_a<KT>(p, base, s_ll, e);
+                    if ((hi_key(a) >> 16) >= T1) {
+                        const int q = atomicAdd(&s_misc[4], 1);
+                        s_cval[q] = a;
+                        s_cidx[q] = static_cast<int16_t>(e);
+                    }
+                });
+                __syncwarp();
+                ncand = n;
+                base16 = floor16 = T1;
+            }
+        }
+        if (p.dbg && lane == 0) atomicAdd(p.dbg + 6, 1u);
+    } else if (T != 0 && cnt >= kb && cnt <= kCap) {
+        int total;
+        int pos = warp_excl_scan(nmine, lane, total);
+        for_hits([&](int e) {
+            s_cval[pos] = recompute_a<KT>(p, base, s_ll, e);
+            s_cidx[pos] = static_cast<int16_t>(e);
+            ++pos;
+        });
+        ncand = cnt;
+        __syncwarp();
+    }
+    // 31-bit high words of the candidates' |a| keys (bits 62..32), 0 = empty slot
+    uint32_t kh[kCapL];
+    auto load_keys = [&]() {
+#pragma unroll
+        for (int s = 0; s < kCapL; ++s) {
+            const int q = lane + 32 * s;
+            kh[s] = q < ncand ? hi_key(s_cval[q]) : 0u;
+        }
+    };
+    auto count_ge = [&](uint32_t v) {
+        int c = 0;
+#pragma unroll
+        for (int s = 0; s < kCapL; ++s) c += kh[s] >= v;
+        return __reduce_add_sync(0xFFFFFFFFu, c);
+    };
+    load_keys();
+    int clo = ncand < 0 ? 0 : count_ge(base16 << 16);
+    if (clo < kb) {
+        ncand = slow_select<KT, LLayout>(&p, ws, b);
+        if (p.dbg && lane == 0) {
+            atomicAdd(p.dbg + 2, 1u);
+            if (cnt > kCap) atomicAdd(p.dbg + 3, 1u);
+        }
+        if (ncand >= 0) {
+            const uint32_t ph = static_cast<uint32_t>(s_misc[0]);  // prefix bits 62..32
+            base16 = ph >> 16;
+            floor16 = (ph + 0xFFFFu) >> 16;
+            load_keys();
+            clo = count_ge(base16 << 16);
+        }
+    }
+    uint32_t next_t;
+    uint32_t selc = 0;
+    if (ncand >= 0) {
+        const uint32_t kmax = __reduce_max_sync(0xFFFFFFFFu, max(max(kh[0], kh[1]), max(kh[2], kh[3])));
+        if (p.check_finite && kmax >= 0x7FF00000u && lane == 0) atomicOr(p.flag, 1u);  // inf/NaN in g or a
+        // Bisection for a high word lo with count(lo) >= kb > count(hi), stopping
+        // early once count(lo) == kb (then the keys >= lo are the selection).
+        uint32_t lo = base16 << 16, hi = kmax + 1;
+        while (clo != kb && hi - lo > 1) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            const int c = count_ge(mid);
+            if (c >= kb) {
+                lo = mid;
+                clo = c;
+            } else {
+                hi = mid;
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < kCapL; ++s)
+            if (kh[s] > lo || (clo == kb && kh[s] == lo)) selc |= 1u << s;
+        if (clo != kb) {
+            // lo is the k_b-th high word and ties on it: rank the tied keys on the
+            // full key, then the lower index (compress.cpp:43-48). Rare.
+            const int need = kb - count_ge(lo + 1);
+            int nm = 0;
+#pragma unroll
+            for (int s = 0; s < kCapL; ++s) {
+                const bool mem = kh[s] == lo && lane + 32 * s < ncand;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mem);
+                if (mem) s_memb[nm + __popc(bal & lanemask_lt())] = static_cast<int16_t>(lane + 32 * s);
+                nm += __popc(bal);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int s = 0; s < kCapL; ++s) {
+                const int q = lane + 32 * s;
+                if (kh[s] == lo && q < ncand) {
+                    const uint64_t kq = key_of(s_cval[q]);
+                    const int iq = s_cidx[q];
+                    int rank = 0;
+                    for (int t = 0; t < nm; ++t) {
+                        const int o = s_memb[t];
+                        const uint64_t ko = key_of(s_cval[o]);
+                        rank += (ko > kq) || (ko == kq && s_cidx[o] < iq);
+                    }
+                    if (rank < need) selc |= 1u << s;
+                }
+            }
+            __syncwarp();
+            if (p.dbg && lane == 0) atomicAdd(p.dbg + 7, 1u);
+        }
+#pragma unroll
+        for (int s = 0; s < kCapL; ++s)
+            if ((selc >> s) & 1u) {
+                const int e = s_cidx[lane + 32 * s];
+                atomicOr(&s_sel[e >> 5], 1u << (e & 31));
+            }
+        // next threshold (the exact kernel's rule): the largest key16 t in
+        // [floor16, lo16] whose candidate count reaches `want`
+        const int planned = T ? static_cast<int>(tstate >> 16) : 0;
+        int want = planned ? (kTargetHits * planned) / max(cnt, 1) : kTargetHits;
+        want = min(max(want, kb + (kb >> 2)), kCap - (kCap >> 2));
+        const uint32_t lo16 = lo >> 16;
+        const uint32_t fl = min(floor16, lo16);
+        uint32_t t;
+        int c = count_ge(fl << 16);
+        if (c < want) {
+            t = fl;
+            if (t > 1) {
+                --t;
+                c += c >> 2;
+            }
+        } else {
+            uint32_t l2 = fl, h2 = lo16 + 1;
+            while (h2 - l2 > 1) {
+                const uint32_t mid = l2 + (h2 - l2) / 2;
+                const int cm = count_ge(mid << 16);
+                if (cm >= want) {
+                    l2 = mid;
+                    c = cm;
+                } else {
+                    h2 = mid;
+                }
+            }
+            t = l2;
+        }
+        next_t = t | (static_cast<uint32_t>(min(c, 0xFFFF)) << 16);
+    } else {
+        const uint32_t h = static_cast<uint32_t>(s_misc[1]) >> 16;
+        next_t = h > 2 ? h - 2 : 1u;
+    }
+    if (lane == 0) p.thresh[b] = (next_t & 0xFFFFu) ? next_t : (next_t | 1u);
+    __syncwarp();
+
+    // ---- window row `slot` (window.cpp:14-26): ascending positions ----
+    {
+        uint32_t wv[4];
+        int loc = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            wv[k] = s_sel[lane * 4 + k];
+            loc += __popc(wv[k]);
+        }
+        int tot;
+        int run = warp_excl_scan(loc, lane, tot);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            s_wpref[lane * 4 + k] = run;
+            run += __popc(wv[k]);
+        }
+    }
+    __syncwarp();
+    const int64_t row0 = static_cast<int64_t>(slot) * kbs;
+    if (ncand >= 0) {
+#pragma unroll
+        for (int s = 0; s < kCapL; ++s)
+            if ((selc >> s) & 1u) {
+                const int q = lane + 32 * s;
+                const int e = s_cidx[q];
+                const int pos = s_wpref[e >> 5] + __popc(s_sel[e >> 5] & ((1u << (e & 31)) - 1u));
+                gwi[row0 + pos] = static_cast<int16_t>(e);
+                st_t<KT::VDT>(gwv, row0 + pos, s_cval[q]);
+            }
+    } else {
+        for (int w = lane; w < kBlk / 32; w += 32) {
+            uint32_t bits = s_sel[w];
+            int pos = s_wpref[w];
+            while (bits) {
+                const int e = w * 32 + __ffs(bits) - 1;
+                bits &= bits - 1;
+                gwi[row0 + pos] = static_cast<int16_t>(e);
+                st_t<KT::VDT>(gwv, row0 + pos, recompute_a<KT>(p, base, s_ll, e));
+                ++pos;
+            }
+        }
+    }
+    __threadfence_block();
+    __syncwarp();
+
+    // ---- pass 2: residual (compress.cpp:95-102) + 4-bit re-quantization
+    //      (quantize.cpp:15-24, 42-55, 102-114, 142-162), exact fp64 ----
+#pragma unroll 1
+    for (int j = 0; j < kIter; ++j) {
+        const int e0 = j * 256 + lane * 8;
+        if (j == kIter / 2 && lane == 0) {
+            prefetch_l2(gwi, uint32_t(m * kbs * 2));
+            prefetch_l2(gwv, uint32_t(m * kbs * vsz));
+            prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
+        }
+        double a[8];
+        widen8<KT::GDT>(load_raw8<KT::GDT>(p.grads, base + e0), a);
+        add_decoded8(a, *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0) >> 1)), s_ll[e0 / BUCKET]);
+        const uint32_t sel8 = (s_sel[e0 >> 5] >> (e0 & 31)) & 0xFFu;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if ((sel8 >> i) & 1u) a[i] = 0.0;
+        double l4[4], h4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool lt = a[2 * k] < a[2 * k + 1];
+            l4[k] = lt ? a[2 * k] : a[2 * k + 1];
+            h4[k] = lt ? a[2 * k + 1] : a[2 * k];
+        }
+        double lo = l4[0] < l4[1] ? l4[0] : l4[1];
+        const double lo2 = l4[2] < l4[3] ? l4[2] : l4[3];
+        lo = lo < lo2 ? lo : lo2;
+        double hi = h4[0] > h4[1] ? h4[0] : h4[1];
+        const double hi2 = h4[2] > h4[3] ? h4[2] : h4[3];
+        hi = hi > hi2 ? hi : hi2;
+#pragma unroll
+        for (int off = 1; off < LPB; off <<= 1) {
+            const double ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
+            const double oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+            lo = ol < lo ? ol : lo;
+            hi = oh > hi ? oh : hi;
+        }
+        // code = clamp(floor((r - lo) / level + 0.5)): t = (r - lo) * k with
+        // k = 15 / (hi - lo) to fp32 accuracy (relative error < 2^-21), read as
+        // an 18-bit fixed point from the low word of 2^34 + t + 0.5 + G 2^-18
+        // (one DFMA). |t - q| < 2^-16.5 = G / 2^18 with G = 8; fixed points
+        // within G of an integer take the IEEE quotient (quantize.cpp:51-53).
+        const double rng = __dsub_rn(hi, lo);
+        uint32_t word = 0, bad = 0;
+        if (rng != 0.0) {
+            const float r32 = __double2float_rn(rng);
+            bad = 0xFFu;
+            if (r32 >= 0x1p-100f && r32 <= 0x1p100f) {
+                constexpr uint32_t G = 8;
+                const double k64 = static_cast<double>(__fdividef(15.0f, r32));
+                const double add = 0x1p34 + 0.5 + static_cast<double>(G) * 0x1p-18;
+                bad = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t y = static_cast<uint32_t>(__double_as_longlong(__fma_rn(__dsub_rn(a[i], lo), k64, add)));
+                    word |= ((y >> 18) & 15u) << (4 * i);
+                    bad |= static_cast<uint32_t>((y & 0x3FFFFu) < 2 * G) << i;
+                }
+            }
+            if (bad) {  // rare: the exact quotient
+                const double level = __ddiv_rn(rng, 15.0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if ((bad >> i) & 1u)
+                        word = (word & ~(15u << (4 * i))) | (exact_code_w(a[i], lo, level) << (4 * i));
+                if (p.dbg) atomicAdd(p.dbg + 1, __popc(bad));
+            }
+        }
+        __stcs(reinterpret_cast<unsigned int*>(p.codes + ((base + e0) >> 1)), word);
+        if ((lane & (LPB - 1)) == 0) __stcs(p.meta + (base + e0) / BUCKET, make_double2(lo, hi));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s_seen[lane * 4 + k] = 0;
+    __syncwarp();
+
+    // ---- ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) ----
+    const int nent = filled * kb;
+    const float inv_kb = 1.0f / static_cast<float>(kb);
+    for (int t = lane; t < nent; t += 32) {
+        const int r = row_of(t, kb, inv_kb);
+        const int idx = gwi[r * kbs + (t - r * kb)];
+        const uint32_t bit = 1u << (idx & 31);
+        if (atomicOr(&s_seen[idx >> 5], bit) & bit) atomicOr(&s_dup[idx >> 5], bit);
+    }
+    __syncwarp();
+    int* dupl = reinterpret_cast<int*>(s_cval);
+    int ndup = 0;
+    for (int t0 = 0; t0 < nent; t0 += 2 * 32) {
+        int idx[2], e[2], r[2];
+        bool mine[2];
+        double th[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int t = t0 + k * 32 + lane;
+            mine[k] = false;
+            r[k] = 0;
+            e[k] = 0;
+            idx[k] = 0;
+            bool dup = false;
+            if (t < nent) {
+                r[k] = row_of(t, kb, inv_kb);
+                e[k] = r[k] * kbs + (t - r[k] * kb);
+                idx[k] = gwi[e[k]];
+                dup = (s_dup[idx[k] >> 5] >> (idx[k] & 31)) & 1u;
+                mine[k] = !dup;
+            }
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
+            const int qd = ndup + __popc(bal & lanemask_lt());
+            if (dup && qd < kDupCap) dupl[qd] = (idx[k] << 16) | (r[k] << 8) | (t - r[k] * kb);
+            ndup += __popc(bal);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) th[k] = mine[k] ? ld_t<KT::PDT>(p.params, base + idx[k]) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (!mine[k]) continue;
+            const double v = ld_t<KT::VDT>(gwv, e[k]);
+            const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r[k]], v)), p.scale1);
+            const double vhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w2[r[k]], __dmul_rn(v, v))), p.scale2);
+            const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+            st_t<KT::PDT>(p.params, base + idx[k], __dsub_rn(th[k], __dmul_rn(p.lr, u)));
+        }
+    }
+    __syncwarp();
+    if (p.dbg && lane == 0) {
+        atomicAdd(p.dbg + 5, static_cast<unsigned>(ndup));
+        if (ndup > kDupCap) atomicAdd(p.dbg + 4, 1u);
+    }
+    dup_stats<KT, LLayout>(&p, ws, b, ndup, nent);
+}
+
+template <class KT>
+cudaError_t launch_kl(const StepArgs& a, cudaStream_t s) {
+    const size_t smem = size_t(kWarps) * LLayout(KT::BUCKET).total;
+    auto k = microadam_step_lean<KT>;
+    cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+    if (err != cudaSuccess) return err;
+    const int64_t grid = (a.block_count + kWarps - 1) / kWarps;
+    k<<<static_cast<unsigned>(grid), 32 * kWarps, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+#define MA_LEAN_DTYPES(X) \
+    X(BF16, BF16, BF16)   \
+    X(F32, F32, BF16)     \
+    X(F32, F32, F32)      \
+    X(BF16, F32, BF16)
+
+template <int LPB>
+cudaError_t launch_ldt(const StepArgs& a, cudaStream_t s) {
+    switch (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype)) {
+#define MA_CASE(G_, P_, V_) \
+        case dtype_key_w(G_, P_, V_): return launch_kl<KW<LPB, G_, P_, V_, false>>(a, s);
+        MA_LEAN_DTYPES(MA_CASE)
+#undef MA_CASE
+        default: return cudaErrorInvalidConfiguration;
+    }
+}
+
+bool lean_ok(const StepArgs& a) {
+    if (a.partials || a.force_exact || (a.bucket != 32 && a.bucket != 64)) return false;
+    switch (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype)) {
+#define MA_CASE(G_, P_, V_) case dtype_key_w(G_, P_, V_): return true;
+        MA_LEAN_DTYPES(MA_CASE)
+#undef MA_CASE
+        default: return false;
+    }
+}
+
+
 template <int LPB, bool REP>
 cudaError_t launch_wdt(const StepArgs& a, cudaStream_t s) {
     switch (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype)) {
@@ -877,6 +1478,7 @@ size_t warp_smem_bytes(int bucket) { return size_t(kWarps) * WLayout(bucket).tot
 cudaError_t launch_step_warp(const StepArgs& a, cudaStream_t s) {
     if (a.block_count <= 0) return cudaSuccess;
     if ((a.block_count + kWarps - 1) / kWarps > 0x7FFFFFFFll) return cudaErrorInvalidConfiguration;
+    if (lean_ok(a)) return a.bucket == 64 ? launch_ldt<8>(a, s) : launch_ldt<4>(a, s);
     return a.partials ? launch_wrep<true>(a, s) : launch_wrep<false>(a, s);
 }
 

@@ -39,14 +39,15 @@ def _host(t):
     return t.detach().to(torch.float64).cpu().numpy()
 
 
-KERNELS = {"fast": {}, "fast_cta": {"MA_FAST_CTA": "1"}, "generic": {"MA_FORCE_GENERIC": "1"}}
+KERNELS = {"fast": {}, "warp_exact": {"MA_WARP_EXACT": "1"}, "fast_cta": {"MA_FAST_CTA": "1"},
+           "generic": {"MA_FORCE_GENERIC": "1"}}
 
 
 def make_engine(kernel, *args, **kw):
     """Create a MicroAdam engine with the kernel family selected at ma_create time."""
     import os
     from paper_2405_15593_b200 import MicroAdam
-    saved = {k: os.environ.get(k) for k in ("MA_FAST_CTA", "MA_FORCE_GENERIC")}
+    saved = {k: os.environ.get(k) for k in ("MA_FAST_CTA", "MA_FORCE_GENERIC", "MA_WARP_EXACT")}
     for k in saved:
         os.environ.pop(k, None)
     os.environ.update(KERNELS[kernel])
