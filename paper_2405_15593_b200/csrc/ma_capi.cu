@@ -232,6 +232,11 @@ int64_t push_and_weights(ma_handle* h, ma::StepArgs* a) {
     }
     a->scale1 = (1.0 - hp.beta1) / (1.0 - std::pow(hp.beta1, static_cast<double>(h->step)));
     a->scale2 = (1.0 - hp.beta2) / (1.0 - std::pow(hp.beta2, static_cast<double>(h->step)));
+    for (int64_t r = 0; r < h->filled; ++r) {
+        a->c1[r] = static_cast<float>(a->w1[r] * a->scale1);
+        a->c2[r] = static_cast<float>(std::sqrt(a->w2[r] * a->scale2));
+    }
+    a->eps32 = static_cast<float>(hp.eps);
     a->filled = static_cast<int32_t>(h->filled);
     a->slot = static_cast<int32_t>(slot);
     return slot;
@@ -326,6 +331,7 @@ ma_status run_step(ma_handle* h, void* d_params, const void* d_grads, double lr,
     a.grads = d_grads;
     a.params = d_params;
     a.lr = lr;
+    a.lr32 = static_cast<float>(lr);
     a.partials = report ? h->d_partials : nullptr;
     push_and_weights(h, &a);
     MA_CUDA(launch(h, a, h->shape.b1 - h->shape.b0, st));
@@ -511,6 +517,7 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
     a.grads = h->d_gstage;
     a.params = h->d_theta;
     a.lr = lr;
+    a.lr32 = static_cast<float>(lr);
     push_and_weights(h, &a);
     const int64_t nb = s.b1 - s.b0;
     const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(64) << 20) / (s.block * int64_t(gsz)));

@@ -39,6 +39,11 @@ struct StepArgs {
     double eps, lr, scale1, scale2;
     double w1[kMaxWindow];
     double w2[kMaxWindow];
+    // fp32 companions for the lean kernel's bf16-θ update screen (ma_warp.cu):
+    // c1[r] = rn(w1[r] * scale1), c2[r] = rn(sqrt(w2[r] * scale2)), rn(eps), rn(lr)
+    float c1[kMaxWindow];
+    float c2[kMaxWindow];
+    float eps32, lr32;
 };
 
 struct Variant {

@@ -833,6 +833,7 @@ cudaError_t launch_kw(const StepArgs& a, cudaStream_t s) {
     X(F32, F32, BF16)             \
     X(F32, F32, F32)              \
     X(BF16, F32, BF16)            \
+    X(BF16, BF16, F32)            \
     X(F64, F64, F64)
 
 constexpr int dtype_key_w(int g, int p, int v) { return g * 9 + p * 3 + v; }
@@ -937,6 +938,57 @@ __device__ __forceinline__ double exact_a_raw(const Raw8<DT>& r, uint32_t cw, in
     }
     const double g = static_cast<double>(__uint_as_float(bits));
     return __dadd_rn(g, __dadd_rn(__dmul_rn(static_cast<double>((cw >> (4 * i)) & 15u), ll.y), ll.x));
+}
+
+// ADAM_STATS + update of a coordinate held by exactly one window entry
+// (row r, entry e): window.cpp:28-46 with one term, optim.cpp:183-187, in the
+// reference's fp64 operation order. Out of line for the bf16-θ screen below.
+template <class KT>
+__device__ __noinline__ void exact_update(const StepArgs* pp, int64_t base, const unsigned char* gwv, int e,
+                                          int r, int idx) {
+    const StepArgs& p = *pp;
+    const double v = ld_t<KT::VDT>(gwv, e);
+    const double th = ld_t<KT::PDT>(p.params, base + idx);
+    const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r], v)), p.scale1);
+    const double vhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w2[r], __dmul_rn(v, v))), p.scale2);
+    const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+    st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
+}
+
+// bf16 θ: the fp32 estimate x32 = θ - lr32 * c1 v / (eps32 + |v| c2) is within
+// |lr u| 2^-20.6 + |x| 2^-24 of the fp64 result x (9 fp32 roundings of at most
+// 2^-24 and a 2-ulp division, against < 2^-49 for the fp64 chain). With
+// |lr u| <= 2^(e+4) (e = exponent of x32) that is < 86 fp32 ulps of x32's
+// binade (172 across a binade edge), so when the 16 bits below the bf16
+// mantissa are more than 512 ulps from the rounding midpoint 0x8000, x and x32
+// round to the same bf16. Everything else takes exact_update.
+template <class KT>
+__device__ __forceinline__ void update_unique(const StepArgs& p, int64_t base, const unsigned char* gwv, int e,
+                                              int r, int idx) {
+    if constexpr (KT::PDT == BF16 && KT::VDT != F64) {
+        uint16_t* th16 = static_cast<uint16_t*>(p.params) + base + idx;
+        const float th = __uint_as_float(static_cast<uint32_t>(*th16) << 16);
+        const float v = KT::VDT == BF16
+                            ? __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(gwv)[e]) << 16)
+                            : reinterpret_cast<const float*>(gwv)[e];
+        const float den = __fmaf_rn(fabsf(v), p.c2[r], p.eps32);
+        const float u = __fdividef(p.c1[r] * v, den);
+        const float x = __fmaf_rn(-p.lr32, u, th);
+        const uint32_t xb = __float_as_uint(x);
+        const uint32_t ex = (xb >> 23) & 0xFFu;
+        const int mid = static_cast<int>(xb & 0xFFFFu) - 0x8000;
+        const bool ok = ex >= 27u && ex <= 227u && den < 0x1p120f &&
+                        fabsf(p.lr32 * u) <= __uint_as_float((ex + 4u) << 23) && (mid > 512 || mid < -512);
+        if (ok) *th16 = static_cast<uint16_t>((xb + 0x7FFFu + ((xb >> 16) & 1u)) >> 16);
+        else exact_update<KT>(&p, base, gwv, e, r, idx);
+    } else {
+        const double v = ld_t<KT::VDT>(gwv, e);
+        const double th = ld_t<KT::PDT>(p.params, base + idx);
+        const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r], v)), p.scale1);
+        const double vhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w2[r], __dmul_rn(v, v))), p.scale2);
+        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+        st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
+    }
 }
 
 template <class KT>
@@ -1341,51 +1393,47 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     __syncwarp();
 
     // ---- ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) ----
+    // Entry t = row r (physical slot) * k_b + position pos; each lane walks
+    // t = lane, lane + 32, ... with (r, pos) advanced incrementally.
     const int nent = filled * kb;
-    const float inv_kb = 1.0f / static_cast<float>(kb);
-    for (int t = lane; t < nent; t += 32) {
-        const int r = row_of(t, kb, inv_kb);
-        const int idx = gwi[r * kbs + (t - r * kb)];
-        const uint32_t bit = 1u << (idx & 31);
-        if (atomicOr(&s_seen[idx >> 5], bit) & bit) atomicOr(&s_dup[idx >> 5], bit);
+    int r0 = 0, pos0 = lane;
+    while (pos0 >= kb) {
+        pos0 -= kb;
+        ++r0;
+    }
+    {
+        int r = r0, pos = pos0;
+        for (int t = lane; t < nent; t += 32) {
+            const int idx = gwi[r * kbs + pos];
+            const uint32_t bit = 1u << (idx & 31);
+            if (atomicOr(&s_seen[idx >> 5], bit) & bit) atomicOr(&s_dup[idx >> 5], bit);
+            pos += 32;
+            while (pos >= kb) {
+                pos -= kb;
+                ++r;
+            }
+        }
     }
     __syncwarp();
     int* dupl = reinterpret_cast<int*>(s_cval);
     int ndup = 0;
-    for (int t0 = 0; t0 < nent; t0 += 2 * 32) {
-        int idx[2], e[2], r[2];
-        bool mine[2];
-        double th[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int t = t0 + k * 32 + lane;
-            mine[k] = false;
-            r[k] = 0;
-            e[k] = 0;
-            idx[k] = 0;
-            bool dup = false;
-            if (t < nent) {
-                r[k] = row_of(t, kb, inv_kb);
-                e[k] = r[k] * kbs + (t - r[k] * kb);
-                idx[k] = gwi[e[k]];
-                dup = (s_dup[idx[k] >> 5] >> (idx[k] & 31)) & 1u;
-                mine[k] = !dup;
-            }
+    {
+        int r = r0, pos = pos0;
+        for (int t0 = 0; t0 < nent; t0 += 32) {
+            const bool act = t0 + lane < nent;
+            const int e = r * kbs + pos;
+            const int idx = act ? gwi[e] : 0;
+            const bool dup = act && ((s_dup[idx >> 5] >> (idx & 31)) & 1u);
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
             const int qd = ndup + __popc(bal & lanemask_lt());
-            if (dup && qd < kDupCap) dupl[qd] = (idx[k] << 16) | (r[k] << 8) | (t - r[k] * kb);
+            if (dup && qd < kDupCap) dupl[qd] = (idx << 16) | (r << 8) | pos;
             ndup += __popc(bal);
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) th[k] = mine[k] ? ld_t<KT::PDT>(p.params, base + idx[k]) : 0.0;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            if (!mine[k]) continue;
-            const double v = ld_t<KT::VDT>(gwv, e[k]);
-            const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r[k]], v)), p.scale1);
-            const double vhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w2[r[k]], __dmul_rn(v, v))), p.scale2);
-            const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
-            st_t<KT::PDT>(p.params, base + idx[k], __dsub_rn(th[k], __dmul_rn(p.lr, u)));
+            if (act && !dup) update_unique<KT>(p, base, gwv, e, r, idx);
+            pos += 32;
+            while (pos >= kb) {
+                pos -= kb;
+                ++r;
+            }
         }
     }
     __syncwarp();
@@ -1393,7 +1441,44 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         atomicAdd(p.dbg + 5, static_cast<unsigned>(ndup));
         if (ndup > kDupCap) atomicAdd(p.dbg + 4, 1u);
     }
-    dup_stats<KT, LLayout>(&p, ws, b, ndup, nent);
+    if (ndup <= 32) {
+        // Duplicated coordinates, one list entry per lane (list order = physical
+        // slot order): peers of a coordinate found with match.any, the lowest
+        // peer sums the terms in lane order (window.cpp:32-39) and updates θ.
+        const bool has = lane < ndup;
+        const int x = has ? dupl[lane] : 0;
+        const int idx = x >> 16, r = (x >> 8) & 0xFF, pos = x & 0xFF;
+        double t1 = 0.0, t2 = 0.0;
+        if (has) {
+            const double v = ld_t<KT::VDT>(gwv, r * kbs + pos);
+            t1 = __dmul_rn(p.w1[r], v);
+            t2 = __dmul_rn(p.w2[r], __dmul_rn(v, v));
+        }
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, has ? idx : -1 - lane);
+        const int cnt = has ? __popc(peers) : 0;
+        const int maxc = __reduce_max_sync(0xFFFFFFFFu, cnt);
+        uint32_t rem = peers;
+        double z1 = 0.0, z2 = 0.0;
+        for (int k = 0; k < maxc; ++k) {
+            const int src = rem ? __ffs(rem) - 1 : lane;
+            rem &= rem - 1;
+            const double a1 = __shfl_sync(0xFFFFFFFFu, t1, src);
+            const double a2 = __shfl_sync(0xFFFFFFFFu, t2, src);
+            if (k < cnt) {
+                z1 = __dadd_rn(z1, a1);
+                z2 = __dadd_rn(z2, a2);
+            }
+        }
+        if (has && (__ffs(peers) - 1) == lane) {
+            const double mhat = __dmul_rn(z1, p.scale1);
+            const double vhat = __dmul_rn(z2, p.scale2);
+            const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+            const double th = ld_t<KT::PDT>(p.params, base + idx);
+            st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
+        }
+    } else {
+        dup_stats<KT, LLayout>(&p, ws, b, ndup, nent);
+    }
 }
 
 template <class KT>
@@ -1412,7 +1497,8 @@ cudaError_t launch_kl(const StepArgs& a, cudaStream_t s) {
     X(BF16, BF16, BF16)   \
     X(F32, F32, BF16)     \
     X(F32, F32, F32)      \
-    X(BF16, F32, BF16)
+    X(BF16, F32, BF16)    \
+    X(BF16, BF16, F32)
 
 template <int LPB>
 cudaError_t launch_ldt(const StepArgs& a, cudaStream_t s) {

@@ -96,3 +96,17 @@ def test_lean_matches_exact_warp_kernel_at_scale():
     assert np.array_equal(wa.indices, wb.indices)
     assert np.array_equal(_bits(wa.values), _bits(wb.values))
     assert np.array_equal(_bits(_host(params["fast"])), _bits(_host(params["warp_exact"])))
+
+
+@pytest.mark.parametrize("lr,tscale", [(1e-3, 1.0), (0.5, 1.0), (1e-2, 2.0 ** -12), (1e-3, 0.0),
+                                       (1e-3, 2.0 ** -110), (1e-1, 2.0 ** 100)])
+def test_bf16_theta_update_screen(lr, tscale):
+    # the fp32 θ-update screen (|lr u| vs |θ|, rounding midpoints, θ = 0,
+    # exponents outside the screened range) must reproduce the fp64 update
+    d = 4096 * 4
+    th = oracle.synth(1, 0, 0, d) * tscale
+    run_parity(d, dict(lr=lr), gdt="bf16", pdt="bf16", vdt="bf16", steps=12, theta0=th)
+
+
+def test_bf16_theta_f32_window_values():
+    run_parity(4096 * 4, dict(lr=1e-2), gdt="bf16", pdt="bf16", vdt="f32", steps=12)

@@ -62,11 +62,14 @@ def make_engine(kernel, *args, **kw):
 
 
 def run_parity(d, hp, *, gdt="f32", pdt="f32", vdt="bf16", steps=12, levels=False, seed=42,
-               grad_fn=None, check_reference=None, lr=None, report_every=0, kernel="fast"):
+               grad_fn=None, check_reference=None, lr=None, report_every=0, kernel="fast",
+               theta0=None):
     torch = _torch()
     oracle.build()
     lr = hp.get("lr", 1e-3) if lr is None else lr
-    theta0 = oracle.synth(1, 0, 0, d, pdt)
+    if theta0 is None:
+        theta0 = oracle.synth(1, 0, 0, d, pdt)
+    theta0 = _host(_dev(np.asarray(theta0, np.float64), pdt))  # representable in the param dtype
     orc = oracle.Oracle(theta0, hp, param_dtype=pdt, value_dtype=vdt)
     ref = None
     if check_reference is None:
