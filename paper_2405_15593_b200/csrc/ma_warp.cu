@@ -132,9 +132,14 @@ __device__ __forceinline__ void widen8(const Raw8<DT>& r, double (&x)[8]) {
 // a += code·level + lo (quantize.cpp:164-178, optim.cpp:166-168): separate
 // multiply and add in fp64, no FMA.
 __device__ __forceinline__ void add_decoded8(double (&a)[8], uint32_t cw, double2 ll) {
+    const uint32_t ce = cw & 0x0F0F0F0Fu, co = (cw >> 4) & 0x0F0F0F0Fu;  // even / odd nibbles
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-        a[i] = __dadd_rn(a[i], __dadd_rn(__dmul_rn(static_cast<double>((cw >> (4 * i)) & 15u), ll.y), ll.x));
+    for (int k = 0; k < 4; ++k) {
+        const double c0 = static_cast<double>(__byte_perm(ce, 0u, 0x4440u | k));
+        const double c1 = static_cast<double>(__byte_perm(co, 0u, 0x4440u | k));
+        a[2 * k] = __dadd_rn(a[2 * k], __dadd_rn(__dmul_rn(c0, ll.y), ll.x));
+        a[2 * k + 1] = __dadd_rn(a[2 * k + 1], __dadd_rn(__dmul_rn(c1, ll.y), ll.x));
+    }
 }
 
 // a at one block-relative element (same arithmetic as pass 1).
@@ -963,33 +968,41 @@ __device__ __noinline__ void exact_update(const StepArgs* pp, int64_t base, cons
 // mantissa are more than 512 ulps from the rounding midpoint 0x8000, x and x32
 // round to the same bf16. Everything else takes exact_update.
 template <class KT>
-__device__ __forceinline__ void update_unique(const StepArgs& p, int64_t base, const unsigned char* gwv, int e,
-                                              int r, int idx) {
-    if constexpr (KT::PDT == BF16 && KT::VDT != F64) {
-        uint16_t* th16 = static_cast<uint16_t*>(p.params) + base + idx;
-        const float th = __uint_as_float(static_cast<uint32_t>(*th16) << 16);
-        const float v = KT::VDT == BF16
-                            ? __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(gwv)[e]) << 16)
-                            : reinterpret_cast<const float*>(gwv)[e];
-        const float den = __fmaf_rn(fabsf(v), p.c2[r], p.eps32);
-        const float u = __fdividef(p.c1[r] * v, den);
-        const float x = __fmaf_rn(-p.lr32, u, th);
-        const uint32_t xb = __float_as_uint(x);
-        const uint32_t ex = (xb >> 23) & 0xFFu;
-        const int mid = static_cast<int>(xb & 0xFFFFu) - 0x8000;
-        const bool ok = ex >= 27u && ex <= 227u && den < 0x1p120f &&
-                        fabsf(p.lr32 * u) <= __uint_as_float((ex + 4u) << 23) && (mid > 512 || mid < -512);
-        if (ok) *th16 = static_cast<uint16_t>((xb + 0x7FFFu + ((xb >> 16) & 1u)) >> 16);
-        else exact_update<KT>(&p, base, gwv, e, r, idx);
-    } else {
-        const double v = ld_t<KT::VDT>(gwv, e);
-        const double th = ld_t<KT::PDT>(p.params, base + idx);
-        const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r], v)), p.scale1);
-        const double vhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w2[r], __dmul_rn(v, v))), p.scale2);
-        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
-        st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
+struct UniqueUpd {
+    static constexpr bool kScreen = KT::PDT == BF16 && KT::VDT != F64;
+    float th = 0.0f, v = 0.0f;
+    __device__ __forceinline__ void load(const StepArgs& p, int64_t base, const unsigned char* gwv, int e, int idx) {
+        if constexpr (kScreen) {
+            th = __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(p.params)[base + idx]) << 16);
+            v = KT::VDT == BF16
+                    ? __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(gwv)[e]) << 16)
+                    : reinterpret_cast<const float*>(gwv)[e];
+        }
     }
-}
+    __device__ __forceinline__ void finish(const StepArgs& p, int64_t base, const unsigned char* gwv, int e, int r,
+                                           int idx) {
+        if constexpr (kScreen) {
+            const float den = __fmaf_rn(fabsf(v), p.c2[r], p.eps32);
+            const float u = __fdividef(p.c1[r] * v, den);
+            const float x = __fmaf_rn(-p.lr32, u, th);
+            const uint32_t xb = __float_as_uint(x);
+            const uint32_t ex = (xb >> 23) & 0xFFu;
+            const int mid = static_cast<int>(xb & 0xFFFFu) - 0x8000;
+            const bool ok = ex >= 27u && ex <= 227u && den < 0x1p120f &&
+                            fabsf(p.lr32 * u) <= __uint_as_float((ex + 4u) << 23) && (mid > 512 || mid < -512);
+            if (ok) static_cast<uint16_t*>(p.params)[base + idx] =
+                        static_cast<uint16_t>((xb + 0x7FFFu + ((xb >> 16) & 1u)) >> 16);
+            else exact_update<KT>(&p, base, gwv, e, r, idx);
+        } else {
+            const double vv = ld_t<KT::VDT>(gwv, e);
+            const double t = ld_t<KT::PDT>(p.params, base + idx);
+            const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r], vv)), p.scale1);
+            const double vhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w2[r], __dmul_rn(vv, vv))), p.scale2);
+            const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+            st_t<KT::PDT>(p.params, base + idx, __dsub_rn(t, __dmul_rn(p.lr, u)));
+        }
+    }
+};
 
 template <class KT>
 __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __grid_constant__ StepArgs p) {
@@ -1354,34 +1367,33 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             hi = oh > hi ? oh : hi;
         }
         // code = clamp(floor((r - lo) / level + 0.5)): t = (r - lo) * k with
-        // k = 15 / (hi - lo) to fp32 accuracy (relative error < 2^-21), read as
-        // an 18-bit fixed point from the low word of 2^34 + t + 0.5 + G 2^-18
-        // (one DFMA). |t - q| < 2^-16.5 = G / 2^18 with G = 8; fixed points
-        // within G of an integer take the IEEE quotient (quantize.cpp:51-53).
+        // k = 15 / (hi - lo) to fp32 accuracy (relative error < 2^-21). One DFMA
+        // forms 2^24 + t + 0.5 + G 2^-28, whose low word holds the code in bits
+        // 28..31 and a 28-bit fraction; |t - q| < 2^-16.5 < G 2^-28 (G = 2^13).
+        // A fraction within G of an integer sends the 8 codes to the IEEE
+        // quotient (quantize.cpp:51-53).
         const double rng = __dsub_rn(hi, lo);
-        uint32_t word = 0, bad = 0;
+        uint32_t word = 0;
         if (rng != 0.0) {
             const float r32 = __double2float_rn(rng);
-            bad = 0xFFu;
+            bool bad = true;
             if (r32 >= 0x1p-100f && r32 <= 0x1p100f) {
-                constexpr uint32_t G = 8;
                 const double k64 = static_cast<double>(__fdividef(15.0f, r32));
-                const double add = 0x1p34 + 0.5 + static_cast<double>(G) * 0x1p-18;
-                bad = 0;
+                const double add = 0x1p24 + 0.5 + 0x1p-15;
+                bad = false;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int i = 7; i >= 0; --i) {
                     const uint32_t y = static_cast<uint32_t>(__double_as_longlong(__fma_rn(__dsub_rn(a[i], lo), k64, add)));
-                    word |= ((y >> 18) & 15u) << (4 * i);
-                    bad |= static_cast<uint32_t>((y & 0x3FFFFu) < 2 * G) << i;
+                    word = __funnelshift_l(y, word, 4);
+                    bad |= (y << 4) < (2u << 17);  // fraction < 2G = 2^14 (of 2^28)
                 }
             }
             if (bad) {  // rare: the exact quotient
                 const double level = __ddiv_rn(rng, 15.0);
+                word = 0;
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if ((bad >> i) & 1u)
-                        word = (word & ~(15u << (4 * i))) | (exact_code_w(a[i], lo, level) << (4 * i));
-                if (p.dbg) atomicAdd(p.dbg + 1, __popc(bad));
+                for (int i = 7; i >= 0; --i) word = (word << 4) | exact_code_w(a[i], lo, level);
+                if (p.dbg) atomicAdd(p.dbg + 1, 8u);
             }
         }
         __stcs(reinterpret_cast<unsigned int*>(p.codes + ((base + e0) >> 1)), word);
@@ -1401,16 +1413,28 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         pos0 -= kb;
         ++r0;
     }
+    auto advance = [&](int& r, int& pos) {
+        pos += 32;
+        while (pos >= kb) {
+            pos -= kb;
+            ++r;
+        }
+    };
     {
         int r = r0, pos = pos0;
-        for (int t = lane; t < nent; t += 32) {
-            const int idx = gwi[r * kbs + pos];
-            const uint32_t bit = 1u << (idx & 31);
-            if (atomicOr(&s_seen[idx >> 5], bit) & bit) atomicOr(&s_dup[idx >> 5], bit);
-            pos += 32;
-            while (pos >= kb) {
-                pos -= kb;
-                ++r;
+        for (int t = lane; t < nent; t += 64) {
+            const int ea = r * kbs + pos;
+            advance(r, pos);
+            const bool hb = t + 32 < nent;
+            const int eb = r * kbs + pos;
+            advance(r, pos);
+            const int ia = gwi[ea];
+            const int ib = hb ? gwi[eb] : ia;
+            uint32_t bit = 1u << (ia & 31);
+            if (atomicOr(&s_seen[ia >> 5], bit) & bit) atomicOr(&s_dup[ia >> 5], bit);
+            if (hb) {
+                bit = 1u << (ib & 31);
+                if (atomicOr(&s_seen[ib >> 5], bit) & bit) atomicOr(&s_dup[ib >> 5], bit);
             }
         }
     }
@@ -1419,21 +1443,30 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     int ndup = 0;
     {
         int r = r0, pos = pos0;
-        for (int t0 = 0; t0 < nent; t0 += 32) {
-            const bool act = t0 + lane < nent;
-            const int e = r * kbs + pos;
-            const int idx = act ? gwi[e] : 0;
-            const bool dup = act && ((s_dup[idx >> 5] >> (idx & 31)) & 1u);
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
-            const int qd = ndup + __popc(bal & lanemask_lt());
-            if (dup && qd < kDupCap) dupl[qd] = (idx << 16) | (r << 8) | pos;
-            ndup += __popc(bal);
-            if (act && !dup) update_unique<KT>(p, base, gwv, e, r, idx);
-            pos += 32;
-            while (pos >= kb) {
-                pos -= kb;
-                ++r;
+        for (int t0 = 0; t0 < nent; t0 += 64) {
+            int e[2], idx[2], rr[2];
+            bool mine[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const bool act = t0 + 32 * k + lane < nent;
+                rr[k] = r;
+                e[k] = r * kbs + pos;
+                idx[k] = act ? gwi[e[k]] : 0;
+                const bool dup = act && ((s_dup[idx[k] >> 5] >> (idx[k] & 31)) & 1u);
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
+                const int qd = ndup + __popc(bal & lanemask_lt());
+                if (dup && qd < kDupCap) dupl[qd] = (idx[k] << 16) | (r << 8) | pos;
+                ndup += __popc(bal);
+                mine[k] = act && !dup;
+                advance(r, pos);
             }
+            UniqueUpd<KT> u[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                if (mine[k]) u[k].load(p, base, gwv, e[k], idx[k]);
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                if (mine[k]) u[k].finish(p, base, gwv, e[k], rr[k], idx[k]);
         }
     }
     __syncwarp();
