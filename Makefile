@@ -6,12 +6,12 @@
 NVCC     ?= /usr/local/cuda/bin/nvcc
 PKG      := paper_2405_15593_b200
 CSRC     := $(PKG)/csrc
-LIBDIR   := $(PKG)/lib
+LIBDIR   ?= $(PKG)/lib
 LIB      := $(LIBDIR)/libmicroadam_cuda.so
 # -fmad=false: no FMA contraction anywhere on device (bit-exact fp64 EF path).
 NVFLAGS  := -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
             -fmad=false -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
-            -Xcompiler -fvisibility=hidden -Xptxas -warn-spills
+            -Xcompiler -fvisibility=hidden -Xptxas -warn-spills $(EXTRA)
 SRCS     := $(CSRC)/ma_kernels.cu $(CSRC)/ma_fast.cu $(CSRC)/ma_warp.cu $(CSRC)/ma_capi.cu $(CSRC)/microadam_b200.cpp
 HDRS     := include/microadam_cuda.h include/ma_synth.h $(CSRC)/ma_internal.h $(CSRC)/ma_device.cuh $(CSRC)/ma_async.cuh $(CSRC)/microadam_b200.hpp
 

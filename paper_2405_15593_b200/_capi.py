@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libmicroadam_cuda.so")
+LIB_PATH = os.environ.get("MA_LIB_PATH") or os.path.join(HERE, "lib", "libmicroadam_cuda.so")
 
 # ma_status
 MA_OK, MA_ERR_INVALID_ARG, MA_ERR_DIM, MA_ERR_NONFINITE, MA_ERR_CUDA, MA_ERR_NCCL, \

@@ -1004,6 +1004,99 @@ struct UniqueUpd {
     }
 };
 
+// Duplicated coordinates beyond one warp's worth of list entries
+// (window.cpp:32-39: terms summed in physical slot order). The ordered entry
+// list is taken 32 entries at a time; match.any groups a coordinate's entries,
+// its lowest lane continues the coordinate's running sums (carried in smem
+// across chunks) in lane order; then one lane per coordinate applies the
+// update. Needs <= 64 distinct coordinates and an un-overflowed list; returns
+// false (nothing done) otherwise. Out of line: keeps the hot kernel's
+// register allocation untouched.
+template <class KT>
+__device__ __noinline__ bool dup_chunks(const StepArgs* pp, unsigned char* ws, int64_t b, int ndup) {
+    const StepArgs& p = *pp;
+    const LLayout L(KT::BUCKET);
+    constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
+    const int lane = threadIdx.x & 31;
+    const int kbs = p.kb_stride;
+    const int64_t base = b * kBlk;
+    const int64_t went = b * p.m * static_cast<int64_t>(kbs);
+    const unsigned char* gwv = static_cast<const unsigned char*>(p.win_val) + went * vsz;
+    const uint32_t* s_dup = reinterpret_cast<const uint32_t*>(ws + L.dup);
+    const int* dupl = reinterpret_cast<const int*>(ws + L.cval);
+    if (ndup > kDupCap) return false;
+    uint32_t dv[4];
+    int loc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        dv[k] = s_dup[lane * 4 + k];
+        loc += __popc(dv[k]);
+    }
+    int ndupc;
+    int run = warp_excl_scan(loc, lane, ndupc);
+    if (ndupc > 64) return false;
+    int* s_dpref = reinterpret_cast<int*>(ws + L.wpref);  // the claim bits of dup_stats are not needed
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        s_dpref[lane * 4 + k] = run;
+        run += __popc(dv[k]);
+    }
+    double2* zz = reinterpret_cast<double2*>(ws + L.llf);  // pass-2 tables are dead
+    int16_t* zc = reinterpret_cast<int16_t*>(ws + L.ll);
+    for (int i = lane; i < ndupc; i += 32) zz[i] = make_double2(0.0, 0.0);
+    __syncwarp();
+    for (int c0 = 0; c0 < ndup; c0 += 32) {
+        const bool has = c0 + lane < ndup;
+        const int x = has ? dupl[c0 + lane] : 0;
+        const int idx = x >> 16, r = (x >> 8) & 0xFF, pos = x & 0xFF;
+        double t1 = 0.0, t2 = 0.0;
+        int id = 0;
+        if (has) {
+            const double v = ld_t<KT::VDT>(gwv, r * kbs + pos);
+            t1 = __dmul_rn(p.w1[r], v);
+            t2 = __dmul_rn(p.w2[r], __dmul_rn(v, v));
+            id = s_dpref[idx >> 5] + __popc(s_dup[idx >> 5] & ((1u << (idx & 31)) - 1u));
+        }
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, has ? idx : -1 - lane);
+        const int cnt = has ? __popc(peers) : 0;
+        const int maxc = __reduce_max_sync(0xFFFFFFFFu, cnt);
+        const bool leader = has && (__ffs(peers) - 1) == lane;
+        double z1 = 0.0, z2 = 0.0;
+        if (leader) {
+            const double2 zc0 = zz[id];
+            z1 = zc0.x;
+            z2 = zc0.y;
+        }
+        uint32_t rem = peers;
+        for (int k = 0; k < maxc; ++k) {
+            const int src = rem ? __ffs(rem) - 1 : lane;
+            rem &= rem - 1;
+            const double a1 = __shfl_sync(0xFFFFFFFFu, t1, src);
+            const double a2 = __shfl_sync(0xFFFFFFFFu, t2, src);
+            if (k < cnt) {
+                z1 = __dadd_rn(z1, a1);
+                z2 = __dadd_rn(z2, a2);
+            }
+        }
+        if (leader) {
+            zz[id] = make_double2(z1, z2);
+            zc[id] = static_cast<int16_t>(idx);
+        }
+        __syncwarp();
+    }
+    for (int i = lane; i < ndupc; i += 32) {
+        const int idx = zc[i];
+        const double2 z = zz[i];
+        const double mhat = __dmul_rn(z.x, p.scale1);
+        const double vhat = __dmul_rn(z.y, p.scale2);
+        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+        const double th = ld_t<KT::PDT>(p.params, base + idx);
+        st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
+    }
+    __syncwarp();
+    return true;
+}
+
 template <class KT>
 __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __grid_constant__ StepArgs p) {
     constexpr int BUCKET = KT::BUCKET, LPB = KT::LPB;
@@ -1509,7 +1602,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             const double th = ld_t<KT::PDT>(p.params, base + idx);
             st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
         }
-    } else {
+    } else if (!dup_chunks<KT>(&p, ws, b, ndup)) {
         dup_stats<KT, LLayout>(&p, ws, b, ndup, nent);
     }
 }

@@ -110,3 +110,18 @@ def test_bf16_theta_update_screen(lr, tscale):
 
 def test_bf16_theta_f32_window_values():
     run_parity(4096 * 4, dict(lr=1e-2), gdt="bf16", pdt="bf16", vdt="f32", steps=12)
+
+
+@pytest.mark.parametrize("per_block,pdt", [(5, "bf16"), (5, "f32"), (20, "bf16"), (60, "bf16")])
+def test_duplicate_coordinates_chunked(per_block, pdt):
+    # a few coordinates per block win every step: 32 < duplicate entries <= 256
+    # with <= 64 coordinates (chunked match.any path), and beyond (fallback)
+    d = 4096 * 6
+    rng = np.random.default_rng(per_block)
+    spikes = np.concatenate([b * 4096 + rng.choice(4096, per_block, replace=False) for b in range(6)])
+
+    def g(s):
+        x = oracle.synth(17, s, 0, d)
+        x[spikes] += 40.0 + s
+        return x
+    run_parity(d, dict(lr=1e-2, window=12), gdt="bf16", pdt=pdt, vdt="bf16", steps=16, grad_fn=g)
