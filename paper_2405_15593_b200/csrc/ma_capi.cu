@@ -452,7 +452,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     alloc(reinterpret_cast<void**>(&h->d_report), ma::kReportFields * sizeof(double));
     alloc(reinterpret_cast<void**>(&h->d_thresh), size_t(nb) * sizeof(uint32_t));
     const char* dbg = std::getenv("MA_DEBUG_COUNTERS");
-    if (dbg && dbg[0] == '1') alloc(reinterpret_cast<void**>(&h->d_dbg), 8 * sizeof(unsigned));
+    if (dbg && dbg[0] == '1') alloc(reinterpret_cast<void**>(&h->d_dbg), 32 * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         free_handle(h);
@@ -704,12 +704,21 @@ int64_t ma_kernel_launches(const ma_handle* h) { return h ? h->launches : 0; }
 ma_status ma_debug_counters(ma_handle* h, int64_t* out, int n) {
     if (!h || !out || n < 0) return fail(MA_ERR_INVALID_ARG, "bad argument");
     DeviceGuard g(h->device);
-    unsigned v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned v[32] = {};
     if (h->d_dbg) {
         MA_CUDA(cudaDeviceSynchronize());
         MA_CUDA(cudaMemcpy(v, h->d_dbg, sizeof(v), cudaMemcpyDeviceToHost));
     }
-    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+    // [0, 8): event counters; [8, 20): per-phase warp cycles (MA_LEAN_PROF builds)
+    for (int i = 0; i < n && i < 20; ++i) {
+        if (i < 8) {
+            out[i] = v[i];
+        } else {
+            unsigned long long c;
+            std::memcpy(&c, reinterpret_cast<const unsigned char*>(v) + 32 + 8 * (i - 8), sizeof(c));
+            out[i] = static_cast<int64_t>(c);
+        }
+    }
     return MA_OK;
 }
 

@@ -870,6 +870,24 @@ constexpr int dtype_key_w(int g, int p, int v) { return g * 9 + p * 3 + v; }
 // ===========================================================================
 
 constexpr float kTwo23 = 8388608.0f;
+#ifndef MA_LEAN_CAPL
+#define MA_LEAN_CAPL 4  // lean kernel: exact-stage candidate slots per lane
+#endif
+#ifndef MA_LEAN_L1PF
+#define MA_LEAN_L1PF 0  // L1 prefetch of θ / window rows at the start of ADAM_STATS
+#endif
+#ifndef MA_LEAN_PROF
+#define MA_LEAN_PROF 0  // per-phase warp clock64 accumulation into dbg[8..] (profiling builds only)
+#endif
+#ifndef MA_LEAN_SB
+#define MA_LEAN_SB 2  // ADAM_STATS: window entries per lane with loads in flight
+#endif
+#ifndef MA_LEAN_TARGET
+#define MA_LEAN_TARGET 64  // lean kernel: carried-threshold target hit count
+#endif
+constexpr int kLCapL = MA_LEAN_CAPL;
+constexpr int kLCap = 32 * kLCapL;
+constexpr int kLTarget = MA_LEAN_TARGET;
 
 // Per-warp shared-memory carve-up of the lean kernel (bytes).
 struct LLayout {
@@ -884,8 +902,8 @@ struct LLayout {
         wpref = uint32_t(o); o = align_up(o + kBlk / 8, 16);    // member list; word prefix; seen bits
         dup = uint32_t(o);   o = align_up(o + kBlk / 8, 16);
         cval = uint32_t(o);  // candidates; radix histogram; bucket (lo, hi) keys; duplicate list
-        o = align_up(o + (size_t(kCap) * 8 > nbk * 16 ? size_t(kCap) * 8 : nbk * 16), 16);
-        cidx = uint32_t(o);  o = align_up(o + kCap * 2, 16);
+        o = align_up(o + (size_t(kLCap) * 8 > nbk * 16 ? size_t(kLCap) * 8 : nbk * 16), 16);
+        cidx = uint32_t(o);  o = align_up(o + kLCap * 2, 16);
         misc = uint32_t(o);  o = align_up(o + 16 * 4, 16);
         total = uint32_t(align_up(o, 128));
     }
@@ -1097,6 +1115,23 @@ __device__ __noinline__ bool dup_chunks(const StepArgs* pp, unsigned char* ws, i
     return true;
 }
 
+#if MA_LEAN_PROF
+// Adds the cycles since the previous mark to phase counter k-1 (dbg[8..] as u64).
+__device__ __forceinline__ void prof_mark(const StepArgs& p, int k) {
+    __shared__ long long t_prev[kWarps];
+    const int w = threadIdx.x >> 5;
+    __syncwarp();
+    const long long t = clock64();
+    if ((threadIdx.x & 31) == 0) {
+        if (k > 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(p.dbg + 8) + (k - 1),
+                      static_cast<unsigned long long>(t - t_prev[w]));
+        t_prev[w] = t;
+    }
+    __syncwarp();
+}
+#endif
+
 template <class KT>
 __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __grid_constant__ StepArgs p) {
     constexpr int BUCKET = KT::BUCKET, LPB = KT::LPB;
@@ -1108,6 +1143,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t bl = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
     if (bl >= p.block_count) return;
+#if MA_LEAN_PROF
+    if (p.dbg) prof_mark(p, 0);
+#endif
     const int64_t b = p.block_offset + bl;
     const int64_t base = b * kBlk;
     const LLayout L(BUCKET);
@@ -1155,6 +1193,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     }
     __syncwarp();
 
+#if MA_LEAN_PROF
+    if (p.dbg) prof_mark(p, 1);
+#endif
     // ---- pass 1: fp32 screen of a = g + decode(EF) against the carried threshold ----
     uint32_t cm0 = 0, cm1 = 0, cm2 = 0, cm3 = 0;
     {
@@ -1195,12 +1236,15 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         }
     };
 
+#if MA_LEAN_PROF
+    if (p.dbg) prof_mark(p, 2);
+#endif
     // ---- block Top-K (compress.cpp:39-53, 73-85) ----
     // Candidates: a superset of the keys >= base16 (key16 units) whose exact
     // values sit in s_cval / s_cidx; floor16: every key16 >= floor16 is a candidate.
     int ncand = -1;
     uint32_t base16 = T, floor16 = T;
-    if (T != 0 && cnt > kCap && cnt <= kRefineMax) {
+    if (T != 0 && cnt > kLCap && cnt <= kRefineMax) {
         // Overfull screen: refine from the hit mask (key16 histogram of the
         // exact hits at or above T) instead of re-reading the block.
         uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.cval);
@@ -1222,7 +1266,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         if (ok) {
             const int d = 31 - __clz(ok);
             const int n = __shfl_sync(0xFFFFFFFFu, sfx, d);
-            if (n <= kCap) {
+            if (n <= kLCap) {
                 const uint32_t T1 = T + static_cast<uint32_t>(d);
                 if (lane == 0) s_misc[4] = 0;
                 __syncwarp();
@@ -1240,7 +1284,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             }
         }
         if (p.dbg && lane == 0) atomicAdd(p.dbg + 6, 1u);
-    } else if (T != 0 && cnt >= kb && cnt <= kCap) {
+    } else if (T != 0 && cnt >= kb && cnt <= kLCap) {
         int total;
         int pos = warp_excl_scan(nmine, lane, total);
         for_hits([&](int e) {
@@ -1252,10 +1296,10 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         __syncwarp();
     }
     // 31-bit high words of the candidates' |a| keys (bits 62..32), 0 = empty slot
-    uint32_t kh[kCapL];
+    uint32_t kh[kLCapL];
     auto load_keys = [&]() {
 #pragma unroll
-        for (int s = 0; s < kCapL; ++s) {
+        for (int s = 0; s < kLCapL; ++s) {
             const int q = lane + 32 * s;
             kh[s] = q < ncand ? hi_key(s_cval[q]) : 0u;
         }
@@ -1263,7 +1307,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     auto count_ge = [&](uint32_t v) {
         int c = 0;
 #pragma unroll
-        for (int s = 0; s < kCapL; ++s) c += kh[s] >= v;
+        for (int s = 0; s < kLCapL; ++s) c += kh[s] >= v;
         return __reduce_add_sync(0xFFFFFFFFu, c);
     };
     load_keys();
@@ -1272,7 +1316,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         ncand = slow_select<KT, LLayout>(&p, ws, b);
         if (p.dbg && lane == 0) {
             atomicAdd(p.dbg + 2, 1u);
-            if (cnt > kCap) atomicAdd(p.dbg + 3, 1u);
+            if (cnt > kLCap) atomicAdd(p.dbg + 3, 1u);
         }
         if (ncand >= 0) {
             const uint32_t ph = static_cast<uint32_t>(s_misc[0]);  // prefix bits 62..32
@@ -1285,7 +1329,10 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     uint32_t next_t;
     uint32_t selc = 0;
     if (ncand >= 0) {
-        const uint32_t kmax = __reduce_max_sync(0xFFFFFFFFu, max(max(kh[0], kh[1]), max(kh[2], kh[3])));
+        uint32_t kml = 0;
+#pragma unroll
+        for (int s = 0; s < kLCapL; ++s) kml = max(kml, kh[s]);
+        const uint32_t kmax = __reduce_max_sync(0xFFFFFFFFu, kml);
         if (p.check_finite && kmax >= 0x7FF00000u && lane == 0) atomicOr(p.flag, 1u);  // inf/NaN in g or a
         // Bisection for a high word lo with count(lo) >= kb > count(hi), stopping
         // early once count(lo) == kb (then the keys >= lo are the selection).
@@ -1301,7 +1348,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             }
         }
 #pragma unroll
-        for (int s = 0; s < kCapL; ++s)
+        for (int s = 0; s < kLCapL; ++s)
             if (kh[s] > lo || (clo == kb && kh[s] == lo)) selc |= 1u << s;
         if (clo != kb) {
             // lo is the k_b-th high word and ties on it: rank the tied keys on the
@@ -1309,7 +1356,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             const int need = kb - count_ge(lo + 1);
             int nm = 0;
 #pragma unroll
-            for (int s = 0; s < kCapL; ++s) {
+            for (int s = 0; s < kLCapL; ++s) {
                 const bool mem = kh[s] == lo && lane + 32 * s < ncand;
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mem);
                 if (mem) s_memb[nm + __popc(bal & lanemask_lt())] = static_cast<int16_t>(lane + 32 * s);
@@ -1317,7 +1364,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             }
             __syncwarp();
 #pragma unroll
-            for (int s = 0; s < kCapL; ++s) {
+            for (int s = 0; s < kLCapL; ++s) {
                 const int q = lane + 32 * s;
                 if (kh[s] == lo && q < ncand) {
                     const uint64_t kq = key_of(s_cval[q]);
@@ -1335,7 +1382,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             if (p.dbg && lane == 0) atomicAdd(p.dbg + 7, 1u);
         }
 #pragma unroll
-        for (int s = 0; s < kCapL; ++s)
+        for (int s = 0; s < kLCapL; ++s)
             if ((selc >> s) & 1u) {
                 const int e = s_cidx[lane + 32 * s];
                 atomicOr(&s_sel[e >> 5], 1u << (e & 31));
@@ -1343,8 +1390,8 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         // next threshold (the exact kernel's rule): the largest key16 t in
         // [floor16, lo16] whose candidate count reaches `want`
         const int planned = T ? static_cast<int>(tstate >> 16) : 0;
-        int want = planned ? (kTargetHits * planned) / max(cnt, 1) : kTargetHits;
-        want = min(max(want, kb + (kb >> 2)), kCap - (kCap >> 2));
+        int want = planned ? (kLTarget * planned) / max(cnt, 1) : kLTarget;
+        want = min(max(want, kb + (kb >> 2)), kLCap - (kLCap >> 2));
         const uint32_t lo16 = lo >> 16;
         const uint32_t fl = min(floor16, lo16);
         uint32_t t;
@@ -1377,6 +1424,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     if (lane == 0) p.thresh[b] = (next_t & 0xFFFFu) ? next_t : (next_t | 1u);
     __syncwarp();
 
+#if MA_LEAN_PROF
+    if (p.dbg) prof_mark(p, 3);
+#endif
     // ---- window row `slot` (window.cpp:14-26): ascending positions ----
     {
         uint32_t wv[4];
@@ -1398,7 +1448,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     const int64_t row0 = static_cast<int64_t>(slot) * kbs;
     if (ncand >= 0) {
 #pragma unroll
-        for (int s = 0; s < kCapL; ++s)
+        for (int s = 0; s < kLCapL; ++s)
             if ((selc >> s) & 1u) {
                 const int q = lane + 32 * s;
                 const int e = s_cidx[q];
@@ -1422,6 +1472,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     __threadfence_block();
     __syncwarp();
 
+#if MA_LEAN_PROF
+    if (p.dbg) prof_mark(p, 4);
+#endif
     // ---- pass 2: residual (compress.cpp:95-102) + 4-bit re-quantization
     //      (quantize.cpp:15-24, 42-55, 102-114, 142-162), exact fp64 ----
 #pragma unroll 1
@@ -1497,7 +1550,23 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     for (int k = 0; k < 4; ++k) s_seen[lane * 4 + k] = 0;
     __syncwarp();
 
+#if MA_LEAN_PROF
+    if (p.dbg) prof_mark(p, 5);
+#endif
     // ---- ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) ----
+#if MA_LEAN_L1PF
+    {   // pull the block's θ lines and window rows into L1 while the bitmaps are built
+        const unsigned char* tp = static_cast<const unsigned char*>(p.params) + base * psz;
+        for (int o = lane * 128; o < kBlk * psz; o += 32 * 128)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + o));
+        const int rb = m * kbs * (2 + vsz);
+        for (int o = lane * 128; o < m * kbs * 2; o += 32 * 128)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const unsigned char*>(gwi) + o));
+        for (int o = lane * 128; o < m * kbs * vsz; o += 32 * 128)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(gwv + o));
+        (void)rb;
+    }
+#endif
     // Entry t = row r (physical slot) * k_b + position pos; each lane walks
     // t = lane, lane + 32, ... with (r, pos) advanced incrementally.
     const int nent = filled * kb;
@@ -1532,33 +1601,39 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         }
     }
     __syncwarp();
+#if MA_LEAN_PROF
+    if (p.dbg) prof_mark(p, 6);
+#endif
     int* dupl = reinterpret_cast<int*>(s_cval);
     int ndup = 0;
     {
         int r = r0, pos = pos0;
-        for (int t0 = 0; t0 < nent; t0 += 64) {
-            int e[2], idx[2], rr[2];
-            bool mine[2];
+        constexpr int SB = MA_LEAN_SB;  // entries per lane in flight
+        for (int t0 = 0; t0 < nent; t0 += 32 * SB) {
+            int e[SB], idx[SB], rr[SB], ps[SB];
+            bool act[SB], mine[SB];
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const bool act = t0 + 32 * k + lane < nent;
+            for (int k = 0; k < SB; ++k) {
+                act[k] = t0 + 32 * k + lane < nent;
                 rr[k] = r;
+                ps[k] = pos;
                 e[k] = r * kbs + pos;
-                idx[k] = act ? gwi[e[k]] : 0;
-                const bool dup = act && ((s_dup[idx[k] >> 5] >> (idx[k] & 31)) & 1u);
-                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
-                const int qd = ndup + __popc(bal & lanemask_lt());
-                if (dup && qd < kDupCap) dupl[qd] = (idx[k] << 16) | (r << 8) | pos;
-                ndup += __popc(bal);
-                mine[k] = act && !dup;
+                idx[k] = act[k] ? gwi[e[k]] : 0;
                 advance(r, pos);
             }
-            UniqueUpd<KT> u[2];
+            UniqueUpd<KT> u[SB];
 #pragma unroll
-            for (int k = 0; k < 2; ++k)
+            for (int k = 0; k < SB; ++k) {
+                const bool dup = act[k] && ((s_dup[idx[k] >> 5] >> (idx[k] & 31)) & 1u);
+                mine[k] = act[k] && !dup;
                 if (mine[k]) u[k].load(p, base, gwv, e[k], idx[k]);
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
+                const int qd = ndup + __popc(bal & lanemask_lt());
+                if (dup && qd < kDupCap) dupl[qd] = (idx[k] << 16) | (rr[k] << 8) | ps[k];
+                ndup += __popc(bal);
+            }
 #pragma unroll
-            for (int k = 0; k < 2; ++k)
+            for (int k = 0; k < SB; ++k)
                 if (mine[k]) u[k].finish(p, base, gwv, e[k], rr[k], idx[k]);
         }
     }
@@ -1567,6 +1642,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         atomicAdd(p.dbg + 5, static_cast<unsigned>(ndup));
         if (ndup > kDupCap) atomicAdd(p.dbg + 4, 1u);
     }
+#if MA_LEAN_PROF
+    if (p.dbg) prof_mark(p, 7);
+#endif
     if (ndup <= 32) {
         // Duplicated coordinates, one list entry per lane (list order = physical
         // slot order): peers of a coordinate found with match.any, the lowest
@@ -1605,6 +1683,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     } else if (!dup_chunks<KT>(&p, ws, b, ndup)) {
         dup_stats<KT, LLayout>(&p, ws, b, ndup, nent);
     }
+#if MA_LEAN_PROF
+    if (p.dbg) prof_mark(p, 8);
+#endif
 }
 
 template <class KT>

@@ -247,12 +247,13 @@ class _Handle:
 
     def debug_counters(self) -> dict:
         """Fast-kernel diagnostics (needs MA_DEBUG_COUNTERS=1 at creation)."""
-        out = (C.c_int64 * 7)()
-        _ok(lib().ma_debug_counters(self._h, out, 7))
+        out = (C.c_int64 * 20)()
+        _ok(lib().ma_debug_counters(self._h, out, 20))
         return {"select_fallback_blocks": out[0], "exact_quotient_elems": out[1],
                 "threshold_misses": out[2], "threshold_too_low": out[3],
                 "dup_list_overflow_blocks": out[4], "dup_entries": out[5],
-                "threshold_refinements": out[6]}
+                "threshold_refinements": out[6], "tie_ranks": out[7],
+                "phase_cycles": list(out[8:20])}
 
 
 _TORCH_DTYPE_NAMES = {"torch.float64": "f64", "torch.float32": "f32", "torch.bfloat16": "bf16"}
