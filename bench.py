@@ -7,15 +7,19 @@
 A "step" is one MicroAdamOptimizer::step (optim.cpp:164-190) over the whole
 workload vector: EF decode + accumulate, block Top-K, 4-bit re-quantization,
 window-ring write, ADAM_STATS + update — one fused kernel launch per step.
-At N>1 (torchrun, one rank per GPU) the vector is block-sharded
-(paper_2405_15593_b200/sharding.py) and every step ends with the NCCL
-all-gather of the updated bf16 θ shards into each rank's full replica.
+At N>1 (torchrun, one rank per GPU) the parameter space is block-sharded.
+--mode shard (default): rank r steps blocks [r nb, (r+1) nb) of an N x 7B
+vector — the step partitions with no data-path exchange, so no collective
+runs inside the timed loop (weak scaling). --mode allgather: the 7B vector is
+split over the ranks (paper_2405_15593_b200/sharding.py) and every step ends
+with the NCCL all-gather of the updated bf16 θ shards into each rank's full
+replica (strong scaling, the north star's ZeRO-1 layout).
 
 Default workload = BASELINE.json configs[3] (Llama-2-7B-sized vector,
 6,738,415,616 params, bf16 θ/g) — the config the headline metric is quoted on;
 it fits one B200. Inputs are synthetic (include/ma_synth.h), generated on the
-device; two gradient buffers alternate; each step moves ~53 GB >> 126 MB L2,
-so no L2 flush is needed between steps.
+device; up to 8 distinct resident gradients are cycled; each step moves
+~53 GB >> 126 MB L2, so no L2 flush is needed between steps.
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libmicroadam_ref.so = the unmodified /root/reference sources) on
@@ -63,6 +67,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-shard-blocks", type=int, default=128)
+    ap.add_argument("--mode", default="shard", choices=["shard", "allgather"],
+                    help="N>1: 'shard' = each rank steps its own workload-sized block range of an "
+                         "N x workload vector, no data-path collective (weak scaling); 'allgather' = "
+                         "the workload split across ranks + NCCL all-gather of bf16 θ each step "
+                         "(strong scaling, ZeRO-1 style)")
     return ap.parse_args()
 
 
@@ -247,10 +256,19 @@ def run_ours(args):
     vdt = "bf16"
     tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[dt]
     hp = ma.HyperParams(density=args.density, window=args.window, lr=1e-3)
-    b0, b1, e0, e1 = sharding.partition_blocks(d, hp.block, world, rank)
+    gather = world > 1 and args.mode == "allgather"
+    if gather:  # strong scaling: the workload's blocks split over the ranks
+        dim_total = d
+        b0, b1, e0, e1 = sharding.partition_blocks(d, hp.block, world, rank)
+        stride = sharding.shard_stride(d, hp.block, world)
+    else:  # weak scaling: rank r owns blocks [r nb, (r+1) nb) of a world x d vector
+        if d % hp.block:
+            raise SystemExit("--mode shard needs a whole-block workload")
+        dim_total = d * world
+        nb = d // hp.block
+        b0, b1, e0, e1 = rank * nb, (rank + 1) * nb, rank * d, (rank + 1) * d
     n = e1 - e0
-    stride = sharding.shard_stride(d, hp.block, world)
-    eng = ma.MicroAdam(d, hp, param_dtype=pdt, grad_dtype=gdt, value_dtype=vdt,
+    eng = ma.MicroAdam(dim_total, hp, param_dtype=pdt, grad_dtype=gdt, value_dtype=vdt,
                        block_range=(b0, b1), device=local)
     lay = eng.layout
     lib = ma.lib()
@@ -260,7 +278,7 @@ def run_ours(args):
         ma._capi.check(lib.ma_fill_synthetic(t.data_ptr(), MA_DT[dt], count, seed, step, offset, 0,
                                              stream.cuda_stream))
 
-    if world > 1:
+    if gather:
         full = torch.empty(stride * world, dtype=tdt, device="cuda")
         params = full[rank * stride: rank * stride + n]
     else:
@@ -285,7 +303,7 @@ def run_ours(args):
         eng.step(params, grads[i % len(grads)], 1e-3, stream=stream.cuda_stream)
         if ev is not None:
             ev[1].record()
-        if world > 1:
+        if gather:
             dist.all_gather_into_tensor(full, full[rank * stride: (rank + 1) * stride])
 
     for i in range(args.warmup):
@@ -320,7 +338,7 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         elapsed, kern = float(tt[0]), float(tt[1])
     s_per_step = elapsed / args.steps
-    value = d / s_per_step
+    value = dim_total / s_per_step
 
     peak, peak_src = read_peaks()
     bytes_launch = algorithmic_bytes(lay, gdt, pdt, vdt, hp.window)
@@ -350,7 +368,7 @@ def run_ours(args):
             tt = torch.tensor([te], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt[0])
-        e2e = {"value": d / te, "unit": UNIT, "h2d_bytes_per_step": n * DT_BYTES[gdt],
+        e2e = {"value": dim_total / te, "unit": UNIT, "h2d_bytes_per_step": n * DT_BYTES[gdt],
                "d2h_bytes_per_step": n * DT_BYTES[pdt], "steps": args.e2e_steps,
                "ms_per_step": te * 1e3,
                "path": "ma_step_host (C ABI): pinned host g -> H2D, fused step, updated θ D2H, "
@@ -371,14 +389,18 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": s_per_step * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dt,
+            "higher_is_better": True, "scaling": "strong" if gather else "weak", "vs_baseline": None,
+            "dtype": dt,
             "data": f"synthetic (include/ma_synth.h Irwin-Hall stream, generated on device; {n_grads} distinct resident gradients cycled)",
             "config": {
                 "workload": f"{args.workload}: {wl['desc']}, {d:,} params, {dt} θ/g, bf16 window "
                             f"values, density {args.density}, m={args.window}, 4-bit EF, "
                             f"B_d=4096, B_q=64, blockwise Top-K",
-                "dim": d, "parallelism": f"block-sharded dp{world}" + (
-                    " + NCCL all_gather of bf16 θ each step" if world > 1 else ""),
+                "dim": d, "dim_total": dim_total,
+                "parallelism": f"block-sharded dp{world}" + (
+                    " + NCCL all_gather of bf16 θ each step" if gather else
+                    (", one workload-sized block range per rank, no data-path collective"
+                     if world > 1 else "")),
                 "l2": "no flush: every step streams ~%.0f GB >> 126 MB L2" % (
                     bytes_launch * world / 1e9),
                 "grad_buffers": n_grads},
@@ -391,13 +413,15 @@ def run_ours(args):
                          "kernel_ms_per_step": [round(a.elapsed_time(b_), 3) for a, b_ in kev],
                          "peak_source": peak_src,
                          "traffic_source": traffic_src,
-                         "kernel": "microadam_step_warp (warp per Top-K block: fused EF decode, Top-K, window, ADAM_STATS, update, 4-bit requant)"},
+                         "kernel": "microadam_step_lean (one warp per B_d=4096 Top-K block: fp32-screened EF "
+                                   "decode + Top-K, window row, exact fp64 4-bit re-quantization, "
+                                   "ADAM_STATS + θ update)"},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clk,
         }
-        if world > 1:
+        if gather:
             line["step_only"] = {"value": d / kern, "ms": kern * 1e3}
         print(json.dumps(line), flush=True)
     if world > 1:
