@@ -173,6 +173,17 @@ MA_API ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double
                          const int64_t* win_indices /* m*row_width */,
                          const double* win_values /* m*row_width */);
 
+/* save_checkpoint / load_checkpoint (checkpoint.hpp:28-33, checkpoint.cpp:50-140):
+ * the reference's MADM v1 file, written from / restored into this handle's
+ * state. params (param_dtype, dim elements) is a device pointer when
+ * params_on_device != 0, else a host pointer; on load it receives θ (may be
+ * NULL to skip). θ and window values are stored as f64 (exact widening), the
+ * EF as packed codes + fp64 (lo, hi). Whole-vector handles only
+ * (MA_ERR_UNSUPPORTED for shards and lossless buffers). Note: the reference
+ * loader itself rejects dim > 2^32 (checkpoint.cpp:101). */
+MA_API ma_status ma_save_checkpoint(ma_handle* h, const void* params, int32_t params_on_device, const char* path);
+MA_API ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_device, const char* path);
+
 /* For ma_step_host: replace the device copy of θ from a host buffer. */
 MA_API ma_status ma_set_params(ma_handle* h, const void* h_params);
 

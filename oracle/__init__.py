@@ -157,11 +157,27 @@ def ref_lib():
         L.ref_adam_stats.restype = C.c_int
         L.ref_adam_stats.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, _i64, _f64,
                                      C.c_double, C.c_int, _f64]
+        L.ref_save_checkpoint.restype = C.c_int
+        L.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_load_checkpoint.restype = C.c_int
+        L.ref_load_checkpoint.argtypes = [C.c_char_p, _i64, C.c_void_p]
         L.ref_time_shards.restype = C.c_double
         L.ref_time_shards.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int64,
                                       C.c_int64, C.c_double, C.c_int64, _f64]
         _rlib = L
     return _rlib
+
+
+def ref_load_checkpoint(path: str, dim: int | None = None):
+    """The reference's own load_checkpoint (checkpoint.cpp:88-140): raises
+    ValueError on what the reference rejects; returns (header dict, θ or None)."""
+    L = ref_lib()
+    out = np.zeros(6, np.int64)
+    theta = np.zeros(dim) if dim else None
+    if L.ref_load_checkpoint(os.fsencode(path), out, theta.ctypes.data if theta is not None else None) != 0:
+        raise ValueError(L.ref_last_error().decode())
+    keys = ("dim", "step", "capacity", "row_width", "head", "filled")
+    return dict(zip(keys, (int(x) for x in out))), theta
 
 
 class State:
@@ -230,6 +246,11 @@ class Oracle:
     def _arr(self, ptr, n, dtype):
         return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
 
+    def save_checkpoint(self, path: str) -> None:
+        """The reference's own save_checkpoint (checkpoint.cpp:50-86)."""
+        if self.L.ref_save_checkpoint(self.h, os.fsencode(path)) != 0:
+            raise ValueError(self.L.ref_last_error().decode())
+
     def state(self) -> State:
         L, h = self.L, self.h
         s, hd, f = C.c_int64(), C.c_int64(), C.c_int64()
@@ -283,6 +304,11 @@ class Reference:
             raise ValueError(self.L.ref_last_error().decode())
         return {"grad_norm": rep[0], "error_norm": rep[1], "empirical_q": rep[2],
                 "update_nnz": int(rep[3])}
+
+    def save_checkpoint(self, path: str) -> None:
+        """The reference's own save_checkpoint (checkpoint.cpp:50-86)."""
+        if self.L.ref_save_checkpoint(self.h, os.fsencode(path)) != 0:
+            raise ValueError(self.L.ref_last_error().decode())
 
     def state(self) -> State:
         L, h = self.L, self.h

@@ -1,5 +1,5 @@
 // ref_shim.cpp — extern "C" wrapper around the UNMODIFIED reference sources
-// (/root/reference/proj/src/{compress,quantize,window,problems,optim}.cpp),
+// (/root/reference/proj/src/{compress,quantize,window,problems,optim,checkpoint}.cpp),
 // compiled by oracle/Makefile into oracle/_ref/libmicroadam_ref.so.
 //
 // TEST INFRASTRUCTURE ONLY: used by tests/ to pin the C restatement
@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../include/ma_synth.h"
+#include "microadam/checkpoint.hpp"
 #include "microadam/compress.hpp"
 #include "microadam/optim.hpp"
 #include "microadam/quantize.hpp"
@@ -105,6 +106,25 @@ void* ref_create(int64_t dim, const double* theta0, double beta1, double beta2, 
 }
 
 void ref_destroy(void* h) { delete static_cast<MicroAdamOptimizer*>(h); }
+
+// ---- save_checkpoint / load_checkpoint (checkpoint.hpp:28-33) ----
+int ref_save_checkpoint(void* h, const char* path) {
+    return guarded([&] { save_checkpoint(path, *static_cast<MicroAdamOptimizer*>(h)); });
+}
+
+// Loads with the reference loader; out: dim, step, capacity, row_width, head, filled.
+int ref_load_checkpoint(const char* path, int64_t* out6, double* theta /* dim, may be NULL */) {
+    return guarded([&] {
+        Checkpoint cp = load_checkpoint(path);
+        out6[0] = cp.dim;
+        out6[1] = cp.step;
+        out6[2] = cp.capacity;
+        out6[3] = cp.row_width;
+        out6[4] = cp.head;
+        out6[5] = cp.filled;
+        if (theta) std::memcpy(theta, cp.theta.data(), cp.theta.size() * sizeof(double));
+    });
+}
 
 int ref_step(void* h, const double* grad, int64_t n, double* report5) {
     auto* o = static_cast<MicroAdamOptimizer*>(h);

@@ -693,6 +693,174 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
     return MA_OK;
 }
 
+// ---------------------------------------------------------------------------
+// MADM v1 checkpoints (checkpoint.cpp:50-140): the reference's on-disk format,
+// written from / restored into device state. Little-endian fields: "MADM",
+// version 1, lossless flag, dim, step, θ as f64, window header (capacity,
+// row_width, head, filled), rows 0..filled-1 (stamp, int64 indices, f64
+// values), then bits, bucket, num_buckets, (lo, hi) per bucket, code bytes.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct CkptFile {
+    std::FILE* f = nullptr;
+    ~CkptFile() {
+        if (f) std::fclose(f);
+    }
+};
+
+bool put_bytes(std::FILE* f, const void* p, size_t n) { return std::fwrite(p, 1, n, f) == n; }
+bool put_i64(std::FILE* f, int64_t v) {
+    unsigned char b[8];
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(static_cast<uint64_t>(v) >> (8 * i));
+    return put_bytes(f, b, 8);
+}
+bool get_bytes(std::FILE* f, void* p, size_t n) { return std::fread(p, 1, n, f) == n; }
+bool get_i64(std::FILE* f, int64_t* v) {
+    unsigned char b[8];
+    if (!get_bytes(f, b, 8)) return false;
+    uint64_t u = 0;
+    for (int i = 0; i < 8; ++i) u |= static_cast<uint64_t>(b[i]) << (8 * i);
+    *v = static_cast<int64_t>(u);
+    return true;
+}
+// f64 arrays: the host is little-endian (x86-64 / aarch64), as the format.
+bool put_f64s(std::FILE* f, const double* v, size_t n) { return put_bytes(f, v, n * 8); }
+bool get_f64s(std::FILE* f, double* v, size_t n) { return get_bytes(f, v, n * 8); }
+
+constexpr size_t kCkptChunk = size_t(1) << 22;  // elements per θ staging chunk
+
+}  // namespace
+
+ma_status ma_save_checkpoint(ma_handle* h, const void* params, int32_t params_on_device, const char* path) {
+    if (!h || !params || !path) return fail(MA_ERR_INVALID_ARG, "null argument");
+    const Shape& s = h->shape;
+    if (s.dim != s.dim_global) return fail(MA_ERR_UNSUPPORTED, "checkpoint: sharded handles are not supported");
+    DeviceGuard g(h->device);
+    MA_CUDA(cudaDeviceSynchronize());
+    CkptFile cf;
+    cf.f = std::fopen(path, "wb");
+    if (!cf.f) return fail(MA_ERR_INVALID_ARG, std::string("checkpoint: cannot open ") + path + " for writing");
+    std::FILE* f = cf.f;
+    const int64_t m = h->cfg.hp.window;
+    const unsigned char head8[6] = {'M', 'A', 'D', 'M', 1, 0};  // magic, version, lossless = 0
+    bool ok = put_bytes(f, head8, 6) && put_i64(f, s.dim) && put_i64(f, h->step);
+    // θ (optim.hpp params()) widened to f64
+    const int pdt = h->cfg.param_dtype;
+    const size_t psz = dtype_size(pdt);
+    std::vector<unsigned char> raw;
+    std::vector<double> wide;
+    for (int64_t i0 = 0; ok && i0 < s.dim; i0 += int64_t(kCkptChunk)) {
+        const size_t n = size_t(std::min<int64_t>(int64_t(kCkptChunk), s.dim - i0));
+        raw.resize(n * psz);
+        const unsigned char* src = static_cast<const unsigned char*>(params) + size_t(i0) * psz;
+        if (params_on_device) MA_CUDA(cudaMemcpy(raw.data(), src, n * psz, cudaMemcpyDeviceToHost));
+        else std::memcpy(raw.data(), src, n * psz);
+        wide.resize(n);
+        for (size_t i = 0; i < n; ++i) wide[i] = widen(raw.data(), pdt, i);
+        ok = put_f64s(f, wide.data(), n);
+    }
+    ok = ok && put_i64(f, m) && put_i64(f, s.row_width) && put_i64(f, h->head) && put_i64(f, h->filled);
+    std::vector<int64_t> idx(static_cast<size_t>(s.row_width));
+    std::vector<double> val(static_cast<size_t>(s.row_width));
+    for (int64_t r = 0; ok && r < h->filled; ++r) {
+        ma_status st = ma_read_window_row(h, r, idx.data(), val.data());
+        if (st != MA_OK) return st;
+        ok = put_i64(f, h->stamps[size_t(r)]) && put_bytes(f, idx.data(), idx.size() * 8) &&
+             put_f64s(f, val.data(), val.size());
+    }
+    std::vector<uint8_t> codes(static_cast<size_t>(s.code_bytes));
+    std::vector<double> lo(static_cast<size_t>(s.nbuckets)), hi(static_cast<size_t>(s.nbuckets));
+    ma_status st = ma_read_error_buffer(h, codes.data(), lo.data(), hi.data());
+    if (st != MA_OK) return st;
+    const unsigned char bits = static_cast<unsigned char>(h->cfg.hp.bits);
+    ok = ok && put_bytes(f, &bits, 1) && put_i64(f, s.bucket) && put_i64(f, s.nbuckets);
+    for (int64_t q = 0; ok && q < s.nbuckets; ++q)
+        ok = put_f64s(f, &lo[size_t(q)], 1) && put_f64s(f, &hi[size_t(q)], 1);
+    ok = ok && put_i64(f, s.code_bytes) && put_bytes(f, codes.data(), codes.size());
+    if (!ok || std::fflush(f) != 0) return fail(MA_ERR_INVALID_ARG, std::string("checkpoint: write failed for ") + path);
+    return MA_OK;
+}
+
+ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_device, const char* path) {
+    if (!h || !path) return fail(MA_ERR_INVALID_ARG, "null argument");
+    const Shape& s = h->shape;
+    if (s.dim != s.dim_global) return fail(MA_ERR_UNSUPPORTED, "checkpoint: sharded handles are not supported");
+    DeviceGuard g(h->device);
+    CkptFile cf;
+    cf.f = std::fopen(path, "rb");
+    if (!cf.f) return fail(MA_ERR_INVALID_ARG, std::string("checkpoint: cannot open ") + path);
+    std::FILE* f = cf.f;
+    unsigned char head8[6];
+    if (!get_bytes(f, head8, 6)) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    if (std::memcmp(head8, "MADM", 4) != 0) return fail(MA_ERR_INVALID_ARG, "checkpoint: bad magic");
+    if (head8[4] != 1) return fail(MA_ERR_INVALID_ARG, "checkpoint: unsupported version");
+    if (head8[5] != 0) return fail(MA_ERR_UNSUPPORTED, "checkpoint: lossless error buffers are not supported on device");
+    int64_t dim = 0, step = 0, cap = 0, rw = 0, head = 0, filled = 0;
+    if (!get_i64(f, &dim) || !get_i64(f, &step)) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    if (dim != s.dim) return fail(MA_ERR_DIM, "checkpoint: dimension differs from the optimizer's");
+    const int pdt = h->cfg.param_dtype;
+    const size_t psz = dtype_size(pdt);
+    std::vector<double> wide;
+    std::vector<unsigned char> raw;
+    for (int64_t i0 = 0; i0 < dim; i0 += int64_t(kCkptChunk)) {
+        const size_t n = size_t(std::min<int64_t>(int64_t(kCkptChunk), dim - i0));
+        wide.resize(n);
+        if (!get_f64s(f, wide.data(), n)) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+        if (!params) continue;
+        raw.resize(n * psz);
+        for (size_t i = 0; i < n; ++i) {
+            if (pdt == MA_F64) {
+                std::memcpy(&raw[i * 8], &wide[i], 8);
+            } else if (pdt == MA_F32) {
+                const float x = float(wide[i]);
+                std::memcpy(&raw[i * 4], &x, 4);
+            } else {  // bf16: values written from a bf16 θ are exact; others round to nearest even
+                const float x = float(wide[i]);
+                uint32_t u;
+                std::memcpy(&u, &x, 4);
+                const uint16_t b = uint16_t((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+                std::memcpy(&raw[i * 2], &b, 2);
+            }
+        }
+        unsigned char* dst = static_cast<unsigned char*>(params) + size_t(i0) * psz;
+        if (params_on_device) MA_CUDA(cudaMemcpy(dst, raw.data(), raw.size(), cudaMemcpyHostToDevice));
+        else std::memcpy(dst, raw.data(), raw.size());
+    }
+    if (!get_i64(f, &cap) || !get_i64(f, &rw) || !get_i64(f, &head) || !get_i64(f, &filled))
+        return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    const int64_t m = h->cfg.hp.window;
+    if (cap != m || rw != s.row_width || filled < 0 || filled > cap || head < 0 || head >= cap)
+        return fail(MA_ERR_INVALID_ARG, "checkpoint: window header does not match the optimizer");
+    std::vector<int64_t> stamps(static_cast<size_t>(m), 0), idx(static_cast<size_t>(m * rw), 0);
+    std::vector<double> val(static_cast<size_t>(m * rw), 0.0);
+    for (int64_t r = 0; r < filled; ++r) {
+        if (!get_i64(f, &stamps[size_t(r)]) || !get_bytes(f, &idx[size_t(r * rw)], size_t(rw) * 8) ||
+            !get_f64s(f, &val[size_t(r * rw)], size_t(rw)))
+            return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    }
+    unsigned char bits = 0;
+    int64_t bucket = 0, nbk = 0, nbytes = 0;
+    if (!get_bytes(f, &bits, 1) || !get_i64(f, &bucket) || !get_i64(f, &nbk))
+        return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    if (bits != h->cfg.hp.bits || bucket != s.bucket || nbk != s.nbuckets)
+        return fail(MA_ERR_INVALID_ARG, "checkpoint: bucket count mismatch");
+    std::vector<double> lo(static_cast<size_t>(nbk)), hi(static_cast<size_t>(nbk));
+    for (int64_t q = 0; q < nbk; ++q)
+        if (!get_f64s(f, &lo[size_t(q)], 1) || !get_f64s(f, &hi[size_t(q)], 1))
+            return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    if (!get_i64(f, &nbytes) || nbytes != s.code_bytes)
+        return fail(MA_ERR_INVALID_ARG, "checkpoint: code length mismatch");
+    std::vector<uint8_t> codes(static_cast<size_t>(nbytes));
+    if (!get_bytes(f, codes.data(), codes.size())) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    // rows >= filled are unwritten (stamp 0): ma_write_state zero-fills them
+    ma_status st = ma_write_state(h, codes.data(), lo.data(), hi.data(), step, head, stamps.data(), idx.data(),
+                                  val.data());
+    if (st != MA_OK) return st;
+    if (params && !params_on_device) h->theta_valid = false;  // ma_step_host re-uploads θ
+    return MA_OK;
+}
+
 ma_status ma_get_layout(const ma_handle* h, ma_layout_info* out) {
     if (!h || !out) return fail(MA_ERR_INVALID_ARG, "null argument");
     fill_layout(h->shape, h->cfg, out);

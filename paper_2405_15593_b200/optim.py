@@ -19,6 +19,7 @@ torch is used only for device memory and streams.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 from typing import Optional
@@ -333,6 +334,30 @@ class MicroAdam(_Handle):
 
     def step_count(self) -> int:
         return self.counters()[0]
+
+    def save_checkpoint(self, path: str, params) -> None:
+        """save_checkpoint (checkpoint.cpp:50-86): the reference's MADM v1 file
+        from this engine's state and θ (a CUDA tensor of the param dtype, or a
+        host numpy array / CPU tensor)."""
+        on_dev, ptr = _buffer(params)
+        _ok(lib().ma_save_checkpoint(self._h, ptr, on_dev, os.fsencode(path)))
+
+    def load_checkpoint(self, path: str, params=None) -> None:
+        """Restore state (and θ into `params` when given) from a MADM v1 file
+        (checkpoint.cpp:88-140 format), e.g. one written by the reference."""
+        on_dev, ptr = _buffer(params) if params is not None else (0, None)
+        _ok(lib().ma_load_checkpoint(self._h, ptr, on_dev, os.fsencode(path)))
+
+
+def _buffer(x):
+    """(on_device, pointer) of a CUDA tensor, CPU tensor or numpy array."""
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise InvalidArgument("checkpoint: expected a contiguous array")
+        return 0, x.ctypes.data
+    if not x.is_contiguous():
+        raise InvalidArgument("checkpoint: expected a contiguous tensor")
+    return (1 if x.is_cuda else 0), x.data_ptr()
 
 
 class MicroAdamOptimizer(_Handle):
