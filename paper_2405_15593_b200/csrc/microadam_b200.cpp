@@ -205,4 +205,20 @@ int64_t MicroAdamOptimizer::step_count() const {
     return s;
 }
 
+void MicroAdam::save_checkpoint(const std::string& path, const void* d_params) const {
+    check(ma_save_checkpoint(h_, d_params, 1, path.c_str()));
+}
+
+void MicroAdam::load_checkpoint(const std::string& path, void* d_params) {
+    check(ma_load_checkpoint(h_, d_params, 1, path.c_str()));
+}
+
+void save_checkpoint(const std::string& path, const MicroAdamOptimizer& opt) {
+    check(ma_save_checkpoint(opt.handle(), opt.params().data(), 0, path.c_str()));
+}
+
+void load_checkpoint(const std::string& path, MicroAdamOptimizer& opt) {
+    check(ma_load_checkpoint(opt.handle(), opt.mutable_params().data(), 0, path.c_str()));
+}
+
 }  // namespace microadam_b200

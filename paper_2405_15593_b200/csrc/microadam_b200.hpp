@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <optional>
 #include <string_view>
+#include <string>
 #include <vector>
 
 #include "../../include/microadam_cuda.h"
@@ -122,6 +123,9 @@ public:
     GradientWindow window() const;
     QuantizedErrorBuffer error_buffer() const;
     ma_handle* handle() const { return h_; }
+    // MADM v1 checkpoint of this engine + its device θ (checkpoint.cpp:50-140)
+    void save_checkpoint(const std::string& path, const void* d_params) const;
+    void load_checkpoint(const std::string& path, void* d_params /* nullable */);
 
 private:
     ma_handle* h_ = nullptr;
@@ -148,6 +152,8 @@ public:
     const SparseSelection& last_selection() const { return last_sel_; }
     int64_t step_count() const;
     const HyperParams& hyper() const { return hp_; }
+    ma_handle* handle() const { return h_; }
+    Vec& mutable_params() { return theta_; }
 
 private:
     Vec theta_;
@@ -155,6 +161,11 @@ private:
     ma_handle* h_ = nullptr;
     SparseSelection last_sel_;
 };
+
+// save_checkpoint(path, opt) / resume (checkpoint.hpp:28-33): the reference's
+// MADM v1 file; byte-identical to the reference's for the same state.
+void save_checkpoint(const std::string& path, const MicroAdamOptimizer& opt);
+void load_checkpoint(const std::string& path, MicroAdamOptimizer& opt);
 
 }  // namespace microadam_b200
 #pragma GCC visibility pop

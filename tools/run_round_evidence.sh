@@ -1,6 +1,9 @@
 set -x
+mkdir -p gpurun_out
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/r1_tests.log 2>&1; tail -2 gpurun_out/r1_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1_smoke.log 2>&1; tail -2 gpurun_out/r1_smoke.log
 timeout 900 python bench.py > gpurun_out/r1_bench.json 2> gpurun_out/r1_bench.err; tail -c 3000 gpurun_out/r1_bench.json
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r1_bench_ref.json 2> gpurun_out/r1_bench_ref.err; tail -c 1500 gpurun_out/r1_bench_ref.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r1_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r1_launch_bench.log 2>&1
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:microadam_step_warp -s 6 -c 1 -o gpurun_out/r1_full7b python bench.py --steps 2 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/r1_full7b.log 2>&1
-ls -la gpurun_out | tail -5
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:microadam_step_lean -s 6 -c 1 -o gpurun_out/r1_full7b -f python bench.py --steps 2 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/r1_full7b.log 2>&1
+ls -la gpurun_out | tail -8
