@@ -18,8 +18,9 @@ replica (strong scaling, the north star's ZeRO-1 layout).
 Default workload = BASELINE.json configs[3] (Llama-2-7B-sized vector,
 6,738,415,616 params, bf16 θ/g) — the config the headline metric is quoted on;
 it fits one B200. Inputs are synthetic (include/ma_synth.h), generated on the
-device; up to 8 distinct resident gradients are cycled; each step moves
-~53 GB >> 126 MB L2, so no L2 flush is needed between steps.
+device; every step reads a gradient no earlier step saw (a shifted window of
+one of up to 8 resident buffers); each step moves ~53 GB >> 126 MB L2, so no
+L2 flush is needed between steps.
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libmicroadam_ref.so = the unmodified /root/reference sources) on
@@ -285,22 +286,30 @@ def run_ours(args):
         full = None
         params = torch.empty(n, dtype=tdt, device="cuda")
     fill(params, 1, 0, e0, n)
-    # Distinct resident gradients, as many as HBM allows (<= 8, >= 2): a short
-    # repeating gradient sequence would make the EF accumulator grow linearly,
-    # which real (non-repeating) gradients do not do.
+    # Every step gets a gradient no earlier step saw: up to 8 resident buffers
+    # (as many as HBM allows, >= 2), each SHIFT elements longer than the shard,
+    # and step i reads buffer i % B at offset (i // B) * STEP8 * 8 elements.
+    # Re-feeding an identical gradient every B steps (B < m) would make the
+    # window and the EF see exact repeats, which real training never produces.
+    SHIFT = 64 * 4096
+    STEP8 = 1283  # offset step in units of 8 elements (16-byte aligned for bf16)
     free, _ = torch.cuda.mem_get_info()
-    gbytes = n * DT_BYTES[gdt]
-    reserve = 2 * gbytes + (8 << 30)  # e2e staging (θ + g copies) + headroom
+    gbytes = (n + SHIFT) * DT_BYTES[gdt]
+    reserve = 2 * n * DT_BYTES[gdt] + (8 << 30)  # e2e staging (θ + g copies) + headroom
     n_grads = int(max(2, min(8, args.steps + args.warmup, (free - reserve) // gbytes)))
-    grads = [torch.empty(n, dtype=tdt, device="cuda") for _ in range(n_grads)]
+    grads = [torch.empty(n + SHIFT, dtype=tdt, device="cuda") for _ in range(n_grads)]
     for i, g in enumerate(grads):
-        fill(g, 42, i + 1, e0, n)
+        fill(g, 42, i + 1, e0, n + SHIFT)
     torch.cuda.synchronize()
+
+    def grad_view(i):
+        off = ((i // n_grads) * STEP8 * 8) % SHIFT
+        return grads[i % n_grads][off: off + n]
 
     def one_step(i, ev=None):
         if ev is not None:
             ev[0].record()
-        eng.step(params, grads[i % len(grads)], 1e-3, stream=stream.cuda_stream)
+        eng.step(params, grad_view(i), 1e-3, stream=stream.cuda_stream)
         if ev is not None:
             ev[1].record()
         if gather:
@@ -351,8 +360,8 @@ def run_ours(args):
         h_params = torch.empty(n, dtype=tdt, pin_memory=True)
         h_grads = [torch.empty(n, dtype=tdt, pin_memory=True) for _ in range(2)]
         h_params.copy_(params)
-        for hg, g in zip(h_grads, grads):
-            hg.copy_(g)
+        for k, hg in enumerate(h_grads):
+            hg.copy_(grad_view(k))
         del grads
         torch.cuda.empty_cache()
         eng.set_params(h_params)
@@ -391,7 +400,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": s_per_step * 1e3,
             "higher_is_better": True, "scaling": "strong" if gather else "weak", "vs_baseline": None,
             "dtype": dt,
-            "data": f"synthetic (include/ma_synth.h Irwin-Hall stream, generated on device; {n_grads} distinct resident gradients cycled)",
+            "data": f"synthetic (include/ma_synth.h Irwin-Hall stream, generated on device; step i reads "
+                    f"a shifted window of resident buffer i % {n_grads}, so no step repeats a gradient)",
             "config": {
                 "workload": f"{args.workload}: {wl['desc']}, {d:,} params, {dt} θ/g, bf16 window "
                             f"values, density {args.density}, m={args.window}, 4-bit EF, "
