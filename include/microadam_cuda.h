@@ -184,6 +184,29 @@ MA_API ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double
 MA_API ma_status ma_save_checkpoint(ma_handle* h, const void* params, int32_t params_on_device, const char* path);
 MA_API ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_device, const char* path);
 
+/* Sparse parameter propagation: MicroAdamOptimizer::step
+ * (optim.cpp:164-190) split so data-parallel ranks exchange the new window rows
+ * (int16 index + value per selected entry, ~0.04 B/param) instead of θ. Every
+ * rank holds a whole-vector handle and a θ replica; per step:
+ *   ma_step_front  on its block range [block_begin, block_end): EF decode, Top-K,
+ *                  window row (also copied to d_stage_idx / d_stage_val, layout
+ *                  [block_end - block_begin][kb_stride], int16 / value dtype),
+ *                  EF re-quantization; advances the window counters. d_grads
+ *                  holds the gradient of that block range only.
+ *   (all-gather the stage buffers across ranks, e.g. ncclAllGather)
+ *   ma_scatter_rows puts the gathered rows of [block_begin, block_end) into the
+ *                  window ring at this step's slot.
+ *   ma_step_stats  ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187)
+ *                  over all blocks into d_params (the rank's θ replica).
+ * Whole 4096-blocks, B_q = 64, flag/off finiteness, lean-kernel dtypes;
+ * front(all) + stats(all) is bit-identical to ma_step. MA_ERR_STATE if the
+ * calls are out of order. */
+MA_API ma_status ma_step_front(ma_handle* h, const void* d_grads, int64_t block_begin, int64_t block_end,
+                        void* d_stage_idx, void* d_stage_val, void* stream);
+MA_API ma_status ma_scatter_rows(ma_handle* h, const void* d_rows_idx, const void* d_rows_val,
+                          int64_t block_begin, int64_t block_end, void* stream);
+MA_API ma_status ma_step_stats(ma_handle* h, void* d_params, double lr, void* stream);
+
 /* For ma_step_host: replace the device copy of θ from a host buffer. */
 MA_API ma_status ma_set_params(ma_handle* h, const void* h_params);
 

@@ -26,7 +26,7 @@ EXPORTED = [
     "ma_step", "ma_step_host", "ma_sync", "ma_get_counters", "ma_read_error_buffer",
     "ma_read_window_row", "ma_write_state", "ma_set_params", "ma_get_layout",
     "ma_kernel_launches", "ma_last_error", "ma_version", "ma_fill_synthetic", "ma_debug_counters",
-    "ma_save_checkpoint", "ma_load_checkpoint",
+    "ma_save_checkpoint", "ma_load_checkpoint", "ma_step_front", "ma_scatter_rows", "ma_step_stats",
 ]
 
 
@@ -97,6 +97,9 @@ def lib():
     L.ma_write_state.argtypes = [vp, vp, vp, vp, C.c_int64, C.c_int64, vp, vp, vp]
     L.ma_set_params.argtypes = [vp, vp]
     L.ma_save_checkpoint.argtypes = [vp, vp, C.c_int32, C.c_char_p]
+    L.ma_step_front.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp, vp]
+    L.ma_scatter_rows.argtypes = [vp, vp, vp, C.c_int64, C.c_int64, vp]
+    L.ma_step_stats.argtypes = [vp, vp, C.c_double, vp]
     L.ma_load_checkpoint.argtypes = [vp, vp, C.c_int32, C.c_char_p]
     L.ma_get_layout.argtypes = [vp, P(Layout)]
     L.ma_kernel_launches.argtypes = [vp]

@@ -180,6 +180,8 @@ struct ma_handle {
     cudaStream_t host_stream = nullptr;
     cudaStream_t last_stream = nullptr;
     int64_t launches = 0;
+    // sparse propagation: the step's kernel arguments between ma_step_front and ma_step_stats
+    ma::StepArgs* pending = nullptr;
 };
 
 namespace {
@@ -212,6 +214,7 @@ void free_handle(ma_handle* h) {
     cudaFree(h->d_theta);
     cudaFree(h->d_gstage);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
+    delete h->pending;
     delete h;
 }
 
@@ -858,6 +861,90 @@ ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_devic
                                   val.data());
     if (st != MA_OK) return st;
     if (params && !params_on_device) h->theta_valid = false;  // ma_step_host re-uploads θ
+    return MA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Sparse parameter propagation: ma_step split into a
+// sharded front (EF decode, Top-K, window row, EF re-quantization over a block
+// range), a row exchange, and ADAM_STATS + update replicated over all blocks,
+// so ranks exchange only the new window rows (4·k_b/B_d ≈ 0.04 B/param)
+// instead of θ. front(all) + stats(all) is bit-identical to ma_step.
+// ---------------------------------------------------------------------------
+ma_status ma_step_front(ma_handle* h, const void* d_grads, int64_t block_begin, int64_t block_end,
+                        void* d_stage_idx, void* d_stage_val, void* stream) {
+    if (!h || !d_grads || !d_stage_idx || !d_stage_val) return fail(MA_ERR_INVALID_ARG, "null argument");
+    const Shape& s = h->shape;
+    const int64_t nb = s.b1 - s.b0;
+    if (block_begin < 0 || block_end > nb || block_begin >= block_end)
+        return fail(MA_ERR_INVALID_ARG, "step_front: block range outside the handle");
+    if (s.dim % s.block != 0 || !h->warp)
+        return fail(MA_ERR_UNSUPPORTED, "step_front: needs whole 4096-blocks and the warp kernel");
+    if (h->cfg.finite_mode == MA_FINITE_STRICT)
+        return fail(MA_ERR_UNSUPPORTED, "step_front: strict finiteness needs the fused step");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ma::StepArgs a;
+    base_args(h, &a);
+    if (!ma::lean_phase_ok(a)) return fail(MA_ERR_UNSUPPORTED, "step_front: dtype/bucket not on the lean kernel");
+    const size_t gsz = dtype_size(h->cfg.grad_dtype);
+    // the kernel addresses g by handle element index; the caller's buffer starts at block_begin
+    a.grads = static_cast<const unsigned char*>(d_grads) - size_t(block_begin * s.block) * gsz;
+    a.params = nullptr;
+    a.lr = h->cfg.hp.lr;
+    a.lr32 = static_cast<float>(a.lr);
+    push_and_weights(h, &a);
+    a.block_offset = block_begin;
+    a.block_count = block_end - block_begin;
+    a.stage_idx = static_cast<int16_t*>(d_stage_idx);
+    a.stage_val = d_stage_val;
+    a.stage_b0 = block_begin;
+    MA_CUDA(ma::launch_step_lean_phase(a, 1, st));
+    ++h->launches;
+    if (!h->pending) h->pending = new ma::StepArgs;
+    *h->pending = a;
+    h->last_stream = st;
+    return MA_OK;
+}
+
+ma_status ma_scatter_rows(ma_handle* h, const void* d_rows_idx, const void* d_rows_val, int64_t block_begin,
+                          int64_t block_end, void* stream) {
+    if (!h || !d_rows_idx || !d_rows_val) return fail(MA_ERR_INVALID_ARG, "null argument");
+    if (!h->pending) return fail(MA_ERR_STATE, "scatter_rows: no ma_step_front in flight");
+    const Shape& s = h->shape;
+    const int64_t nb = s.b1 - s.b0, m = h->cfg.hp.window, kbs = s.kb_stride;
+    if (block_begin < 0 || block_end > nb || block_begin >= block_end)
+        return fail(MA_ERR_INVALID_ARG, "scatter_rows: block range outside the handle");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t slot = h->pending->slot;
+    const size_t vsz = dtype_size(h->cfg.value_dtype);
+    const size_t rows = size_t(block_end - block_begin);
+    MA_CUDA(cudaMemcpy2DAsync(h->d_win_idx + (block_begin * m + slot) * kbs, size_t(m * kbs) * 2, d_rows_idx,
+                              size_t(kbs) * 2, size_t(kbs) * 2, rows, cudaMemcpyDeviceToDevice, st));
+    MA_CUDA(cudaMemcpy2DAsync(static_cast<unsigned char*>(h->d_win_val) + size_t((block_begin * m + slot) * kbs) * vsz,
+                              size_t(m * kbs) * vsz, d_rows_val, size_t(kbs) * vsz, size_t(kbs) * vsz, rows,
+                              cudaMemcpyDeviceToDevice, st));
+    return MA_OK;
+}
+
+ma_status ma_step_stats(ma_handle* h, void* d_params, double lr, void* stream) {
+    if (!h || !d_params) return fail(MA_ERR_INVALID_ARG, "null argument");
+    if (!h->pending) return fail(MA_ERR_STATE, "step_stats: no ma_step_front in flight");
+    if (!(lr > 0.0)) return fail(MA_ERR_INVALID_ARG, "step: lr must be > 0");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ma::StepArgs a = *h->pending;
+    a.params = d_params;
+    a.lr = lr;
+    a.lr32 = static_cast<float>(lr);
+    a.block_offset = 0;
+    a.block_count = h->shape.b1 - h->shape.b0;
+    MA_CUDA(ma::launch_step_lean_phase(a, 2, st));
+    ++h->launches;
+    delete h->pending;
+    h->pending = nullptr;
+    h->last_stream = st;
     return MA_OK;
 }
 

@@ -44,6 +44,11 @@ struct StepArgs {
     float c1[kMaxWindow];
     float c2[kMaxWindow];
     float eps32, lr32;
+    // sparse-propagation front (lean kernel PH = 1): new rows also go to
+    // stage_*[(b - stage_b0) * kb_stride + pos]
+    int16_t* stage_idx;
+    void* stage_val;
+    int64_t stage_b0;
 };
 
 struct Variant {
@@ -71,6 +76,9 @@ bool warp_path_ok(int block, int bucket, int kb, int m, int kb_stride, int g_dty
                   int v_dtype);
 size_t warp_smem_bytes(int bucket);
 cudaError_t launch_step_warp(const StepArgs& a, cudaStream_t s);
+// Lean kernel split for sparse parameter propagation (ph 1 = front, 2 = stats).
+bool lean_phase_ok(const StepArgs& a);
+cudaError_t launch_step_lean_phase(const StepArgs& a, int ph, cudaStream_t s);
 cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int* flag,
                                cudaStream_t s);
 cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double* out5,

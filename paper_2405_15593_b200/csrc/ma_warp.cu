@@ -1132,7 +1132,9 @@ __device__ __forceinline__ void prof_mark(const StepArgs& p, int k) {
 }
 #endif
 
-template <class KT>
+// PH: 3 = the fused step; 1 = front only (EF decode, Top-K, window row + stage
+// copy, EF re-quantization); 2 = ADAM_STATS + update only (sparse propagation).
+template <class KT, int PH = 3>
 __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __grid_constant__ StepArgs p) {
     constexpr int BUCKET = KT::BUCKET, LPB = KT::LPB;
     constexpr int gsz = KT::GDT == F32 ? 4 : 2;
@@ -1165,6 +1167,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     int16_t* gwi = p.win_idx + went;
     unsigned char* gwv = static_cast<unsigned char*>(p.win_val) + went * vsz;
 
+    if constexpr (PH & 1) {
     if (lane == 0) {
         prefetch_l2_keep(static_cast<const unsigned char*>(p.grads) + base * gsz, kBlk * gsz);
         prefetch_l2_keep(p.codes + base / 2, kBlk / 2);
@@ -1455,6 +1458,11 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
                 const int pos = s_wpref[e >> 5] + __popc(s_sel[e >> 5] & ((1u << (e & 31)) - 1u));
                 gwi[row0 + pos] = static_cast<int16_t>(e);
                 st_t<KT::VDT>(gwv, row0 + pos, s_cval[q]);
+                if constexpr (PH == 1) {
+                    const int64_t so = (b - p.stage_b0) * kbs + pos;
+                    p.stage_idx[so] = static_cast<int16_t>(e);
+                    st_t<KT::VDT>(p.stage_val, so, s_cval[q]);
+                }
             }
     } else {
         for (int w = lane; w < kBlk / 32; w += 32) {
@@ -1464,7 +1472,13 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
                 const int e = w * 32 + __ffs(bits) - 1;
                 bits &= bits - 1;
                 gwi[row0 + pos] = static_cast<int16_t>(e);
-                st_t<KT::VDT>(gwv, row0 + pos, recompute_a<KT>(p, base, s_ll, e));
+                const double av = recompute_a<KT>(p, base, s_ll, e);
+                st_t<KT::VDT>(gwv, row0 + pos, av);
+                if constexpr (PH == 1) {
+                    const int64_t so = (b - p.stage_b0) * kbs + pos;
+                    p.stage_idx[so] = static_cast<int16_t>(e);
+                    st_t<KT::VDT>(p.stage_val, so, av);
+                }
                 ++pos;
             }
         }
@@ -1480,7 +1494,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
 #pragma unroll 1
     for (int j = 0; j < kIter; ++j) {
         const int e0 = j * 256 + lane * 8;
-        if (j == kIter / 2 && lane == 0) {
+        if ((PH & 2) && j == kIter / 2 && lane == 0) {
             prefetch_l2(gwi, uint32_t(m * kbs * 2));
             prefetch_l2(gwv, uint32_t(m * kbs * vsz));
             prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
@@ -1549,6 +1563,21 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
 #pragma unroll
     for (int k = 0; k < 4; ++k) s_seen[lane * 4 + k] = 0;
     __syncwarp();
+    }  // PH & 1
+    if constexpr (PH == 2) {
+        if (lane == 0) {
+            prefetch_l2(gwi, uint32_t(m * kbs * 2));
+            prefetch_l2(gwv, uint32_t(m * kbs * vsz));
+            prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            s_seen[lane * 4 + k] = 0;
+            s_dup[lane * 4 + k] = 0;
+        }
+        __syncwarp();
+    }
+    if constexpr (PH & 2) {
 
 #if MA_LEAN_PROF
     if (p.dbg) prof_mark(p, 5);
@@ -1683,15 +1712,16 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     } else if (!dup_chunks<KT>(&p, ws, b, ndup)) {
         dup_stats<KT, LLayout>(&p, ws, b, ndup, nent);
     }
+    }  // PH & 2
 #if MA_LEAN_PROF
     if (p.dbg) prof_mark(p, 8);
 #endif
 }
 
-template <class KT>
+template <class KT, int PH = 3>
 cudaError_t launch_kl(const StepArgs& a, cudaStream_t s) {
     const size_t smem = size_t(kWarps) * LLayout(KT::BUCKET).total;
-    auto k = microadam_step_lean<KT>;
+    auto k = microadam_step_lean<KT, PH>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem));
     if (err != cudaSuccess) return err;
@@ -1767,6 +1797,23 @@ bool warp_path_ok(int block, int bucket, int kb, int m, int kb_stride, int g, in
 }
 
 size_t warp_smem_bytes(int bucket) { return size_t(kWarps) * WLayout(bucket).total; }
+
+// Sparse-propagation phases of the lean kernel (B_q = 64): ph = 1 front, 2 stats.
+bool lean_phase_ok(const StepArgs& a) { return lean_ok(a) && a.bucket == 64; }
+
+cudaError_t launch_step_lean_phase(const StepArgs& a, int ph, cudaStream_t s) {
+    if (a.block_count <= 0) return cudaSuccess;
+    if (!lean_phase_ok(a)) return cudaErrorInvalidConfiguration;
+    switch (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype)) {
+#define MA_CASE(G_, P_, V_)                                                        \
+        case dtype_key_w(G_, P_, V_):                                              \
+            return ph == 1 ? launch_kl<KW<8, G_, P_, V_, false>, 1>(a, s)          \
+                           : launch_kl<KW<8, G_, P_, V_, false>, 2>(a, s);
+        MA_LEAN_DTYPES(MA_CASE)
+#undef MA_CASE
+        default: return cudaErrorInvalidConfiguration;
+    }
+}
 
 cudaError_t launch_step_warp(const StepArgs& a, cudaStream_t s) {
     if (a.block_count <= 0) return cudaSuccess;

@@ -335,6 +335,37 @@ class MicroAdam(_Handle):
     def step_count(self) -> int:
         return self.counters()[0]
 
+    # -- sparse parameter propagation (ma_step_front / ma_scatter_rows / ma_step_stats) --
+    def stage_buffers(self, nblocks: int):
+        """Device (idx, values) stage buffers for `nblocks` blocks' window rows."""
+        import torch
+        kbs = self.layout.kb_stride
+        vt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[self.value_dtype]
+        return (torch.empty(nblocks * kbs, dtype=torch.int16, device=f"cuda:{self.device}"),
+                torch.empty(nblocks * kbs, dtype=vt, device=f"cuda:{self.device}"))
+
+    def _stream(self, stream):
+        if stream is None:
+            import torch
+            return torch.cuda.current_stream(self.device).cuda_stream
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+
+    def step_front(self, grads, block_begin: int, block_end: int, stage, stream=None) -> None:
+        """EF decode, Top-K, window row (also into `stage`) and EF re-quantization
+        for blocks [block_begin, block_end); `grads` covers exactly that range."""
+        _ok(lib().ma_step_front(self._h, grads.data_ptr(), block_begin, block_end, stage[0].data_ptr(),
+                                stage[1].data_ptr(), C.c_void_p(self._stream(stream))))
+
+    def scatter_rows(self, rows, block_begin: int, block_end: int, stream=None) -> None:
+        """Put the (gathered) rows of blocks [block_begin, block_end) into this step's window slot."""
+        _ok(lib().ma_scatter_rows(self._h, rows[0].data_ptr(), rows[1].data_ptr(), block_begin, block_end,
+                                  C.c_void_p(self._stream(stream))))
+
+    def step_stats(self, params, lr: Optional[float] = None, stream=None) -> None:
+        """ADAM_STATS + θ update over all blocks into `params` (this rank's replica)."""
+        _ok(lib().ma_step_stats(self._h, self._ptr(params, self.param_dtype, "params"),
+                                self.hp.lr if lr is None else lr, C.c_void_p(self._stream(stream))))
+
     def save_checkpoint(self, path: str, params) -> None:
         """save_checkpoint (checkpoint.cpp:50-86): the reference's MADM v1 file
         from this engine's state and θ (a CUDA tensor of the param dtype, or a
