@@ -68,11 +68,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-shard-blocks", type=int, default=128)
-    ap.add_argument("--mode", default="shard", choices=["shard", "allgather"],
+    ap.add_argument("--mode", default="shard", choices=["shard", "allgather", "sparse"],
                     help="N>1: 'shard' = each rank steps its own workload-sized block range of an "
                          "N x workload vector, no data-path collective (weak scaling); 'allgather' = "
                          "the workload split across ranks + NCCL all-gather of bf16 θ each step "
-                         "(strong scaling, ZeRO-1 style)")
+                         "(strong scaling, ZeRO-1 style); 'sparse' = the workload split across ranks "
+                         "for the EF / Top-K front, NCCL all-gather of the new window rows only, "
+                         "ADAM_STATS + update replicated on every rank's θ (strong scaling)")
     return ap.parse_args()
 
 
@@ -258,7 +260,14 @@ def run_ours(args):
     tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[dt]
     hp = ma.HyperParams(density=args.density, window=args.window, lr=1e-3)
     gather = world > 1 and args.mode == "allgather"
-    if gather:  # strong scaling: the workload's blocks split over the ranks
+    sparse = args.mode == "sparse"
+    if sparse:  # strong scaling, window-row exchange: a whole-vector handle per rank
+        if d % hp.block:
+            raise SystemExit("--mode sparse needs a whole-block workload")
+        dim_total = d
+        b0, b1, e0, e1 = sharding.partition_blocks(d, hp.block, world, rank)
+        stride = sharding.shard_stride(d, hp.block, world)
+    elif gather:  # strong scaling: the workload's blocks split over the ranks
         dim_total = d
         b0, b1, e0, e1 = sharding.partition_blocks(d, hp.block, world, rank)
         stride = sharding.shard_stride(d, hp.block, world)
@@ -270,7 +279,7 @@ def run_ours(args):
         b0, b1, e0, e1 = rank * nb, (rank + 1) * nb, rank * d, (rank + 1) * d
     n = e1 - e0
     eng = ma.MicroAdam(dim_total, hp, param_dtype=pdt, grad_dtype=gdt, value_dtype=vdt,
-                       block_range=(b0, b1), device=local)
+                       block_range=(0, -1) if sparse else (b0, b1), device=local)
     lay = eng.layout
     lib = ma.lib()
     stream = torch.cuda.current_stream()
@@ -279,13 +288,19 @@ def run_ours(args):
         ma._capi.check(lib.ma_fill_synthetic(t.data_ptr(), MA_DT[dt], count, seed, step, offset, 0,
                                              stream.cuda_stream))
 
-    if gather:
+    if sparse:  # every rank holds the full θ replica; rows travel, θ does not
+        full = None
+        params = torch.empty(d, dtype=tdt, device="cuda")
+        sblk = stride // hp.block  # blocks per rank (padded)
+        stage = eng.stage_buffers(sblk)
+        rows = eng.stage_buffers(sblk * world)
+    elif gather:
         full = torch.empty(stride * world, dtype=tdt, device="cuda")
         params = full[rank * stride: rank * stride + n]
     else:
         full = None
         params = torch.empty(n, dtype=tdt, device="cuda")
-    fill(params, 1, 0, e0, n)
+    fill(params, 1, 0, 0 if sparse else e0, params.numel())
     # Every step gets a gradient no earlier step saw: up to 8 resident buffers
     # (as many as HBM allows, >= 2), each SHIFT elements longer than the shard,
     # and step i reads buffer i % B at offset (i // B) * STEP8 * 8 elements.
@@ -306,10 +321,20 @@ def run_ours(args):
         off = ((i // n_grads) * STEP8 * 8) % SHIFT
         return grads[i % n_grads][off: off + n]
 
+    nb_all = d // hp.block
+
     def one_step(i, ev=None):
         if ev is not None:
             ev[0].record()
-        eng.step(params, grad_view(i), 1e-3, stream=stream.cuda_stream)
+        if sparse:
+            eng.step_front(grad_view(i), b0, b1, stage, stream=stream.cuda_stream)
+            if world > 1:
+                dist.all_gather_into_tensor(rows[0], stage[0])
+                dist.all_gather_into_tensor(rows[1], stage[1])
+                eng.scatter_rows(rows, 0, nb_all, stream=stream.cuda_stream)
+            eng.step_stats(params, 1e-3, stream=stream.cuda_stream)
+        else:
+            eng.step(params, grad_view(i), 1e-3, stream=stream.cuda_stream)
         if ev is not None:
             ev[1].record()
         if gather:
@@ -356,7 +381,7 @@ def run_ours(args):
 
     # ---- end to end through the reference-facing host path (ma_step_host) ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not (sparse and world > 1):
         h_params = torch.empty(n, dtype=tdt, pin_memory=True)
         h_grads = [torch.empty(n, dtype=tdt, pin_memory=True) for _ in range(2)]
         h_params.copy_(params)
@@ -398,7 +423,8 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": s_per_step * 1e3,
-            "higher_is_better": True, "scaling": "strong" if gather else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if (gather or sparse) else "weak",
+            "vs_baseline": None,
             "dtype": dt,
             "data": f"synthetic (include/ma_synth.h Irwin-Hall stream, generated on device; step i reads "
                     f"a shifted window of resident buffer i % {n_grads}, so no step repeats a gradient)",
@@ -409,6 +435,8 @@ def run_ours(args):
                 "dim": d, "dim_total": dim_total,
                 "parallelism": f"block-sharded dp{world}" + (
                     " + NCCL all_gather of bf16 θ each step" if gather else
+                    (" EF/Top-K front + NCCL all_gather of the new window rows, ADAM_STATS + update "
+                     "replicated on each rank's θ" if sparse else None) or
                     (", one workload-sized block range per rank, no data-path collective"
                      if world > 1 else "")),
                 "l2": "no flush: every step streams ~%.0f GB >> 126 MB L2" % (
