@@ -49,6 +49,7 @@ struct Shape {
     int64_t bucket = 0, nbuckets = 0, bucket0 = 0;
     int64_t code_bytes = 0;
     int64_t kb_stride = 0;
+    bool global = false;     // global Top-K over d > kMaxBlock (ma_global.cu)
 };
 
 // HyperParams::validate (optim.cpp:7-21) — same checks, same order.
@@ -108,8 +109,18 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
                              : static_cast<int64_t>(std::ceil(hp.density * static_cast<double>(dim)));
         s.per_block_k = k < 1 ? 1 : (k > dim ? dim : k);
     }
-    if (s.block > ma::kMaxBlock)
-        return fail(MA_ERR_UNSUPPORTED, "block (or global-mode dim) > 8192 not supported on device");
+    if (!cfg->blockwise && s.block > ma::kMaxBlock) {
+        // Global Top-K over the whole vector (compress.cpp:66-71): ma_global.cu
+        if (dim >= (int64_t(1) << 31))
+            return fail(MA_ERR_UNSUPPORTED, "global mode: dim >= 2^31 not supported on device");
+        if (4096 % hp.bucket != 0)
+            return fail(MA_ERR_UNSUPPORTED, "global mode on device needs bucket | 4096");
+        if (b0 != 0 || (b1 >= 0 && b1 != 1))
+            return fail(MA_ERR_UNSUPPORTED, "global mode cannot be block-sharded");
+        s.global = true;
+    } else if (s.block > ma::kMaxBlock) {
+        return fail(MA_ERR_UNSUPPORTED, "block > 8192 not supported on device");
+    }
     s.nblocks_global = (dim + s.block - 1) / s.block;
     if (s.nblocks_global > 1 && (s.block % hp.bucket != 0 || s.block % 2 != 0))
         return fail(MA_ERR_UNSUPPORTED,
@@ -170,6 +181,13 @@ struct ma_handle {
     double* d_report = nullptr;
     uint32_t* d_thresh = nullptr;
     unsigned int* d_dbg = nullptr;  // diagnostics counters (MA_DEBUG_COUNTERS=1)
+    // global Top-K mode buffers (ma_global.cu)
+    double* g_level = nullptr;
+    uint16_t* g_selbits = nullptr;
+    uint32_t* g_hist = nullptr;
+    int2* g_cnt = nullptr;
+    int2* g_selinfo = nullptr;
+    double* g_z = nullptr;
     // host counters (window.hpp:10-33)
     int64_t step = 0, head = 0, filled = 0;
     std::vector<int64_t> stamps;
@@ -213,6 +231,12 @@ void free_handle(ma_handle* h) {
     cudaFree(h->d_dbg);
     cudaFree(h->d_theta);
     cudaFree(h->d_gstage);
+    cudaFree(h->g_level);
+    cudaFree(h->g_selbits);
+    cudaFree(h->g_hist);
+    cudaFree(h->g_cnt);
+    cudaFree(h->g_selinfo);
+    cudaFree(h->g_z);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
     delete h->pending;
     delete h;
@@ -321,6 +345,104 @@ ma_status strict_prescan(ma_handle* h, const void* d_grads, cudaStream_t st) {
     return MA_OK;
 }
 
+// Global Top-K step (ma_global.cu): host-driven radix select of the k-th
+// largest |a| key, then emit / re-quantize / ADAM_STATS / update kernels.
+ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, double lr, cudaStream_t st,
+                          ma_step_report* report) {
+    const Shape& s = h->shape;
+    ma::StepArgs a;
+    base_args(h, &a);
+    push_and_weights(h, &a);
+    ma::GlobalArgs g{};
+    g.grads = d_grads;
+    g.params = d_params;
+    g.codes = h->d_codes;
+    g.meta = h->d_meta;
+    g.level = h->g_level;
+    g.win_idx = reinterpret_cast<int32_t*>(h->d_win_idx);
+    g.win_val = h->d_win_val;
+    g.selbits = h->g_selbits;
+    g.hist = h->g_hist;
+    g.cnt = h->g_cnt;
+    g.sel_info = h->g_selinfo;
+    g.z1 = h->g_z;
+    g.z2 = h->g_z + s.dim;
+    g.partials = report ? h->d_partials : nullptr;
+    g.flag = h->d_flag;
+    g.dim = s.dim;
+    g.nbuckets = s.nbuckets;
+    g.bucket = s.bucket;
+    g.k = s.per_block_k;
+    g.row_stride = s.kb_stride;
+    g.slot = a.slot;
+    g.g_dtype = h->cfg.grad_dtype;
+    g.p_dtype = h->cfg.param_dtype;
+    g.v_dtype = h->cfg.value_dtype;
+    g.check_finite = a.check_finite;
+    g.eps = a.eps;
+    g.lr = lr;
+    g.scale1 = a.scale1;
+    g.scale2 = a.scale2;
+    MA_CUDA(ma::g_launch_levels(g, st));
+    // exact k-th largest key: 11-bit digits from bit 62 down, then 8 bits
+    static const int kShift[6] = {52, 41, 30, 19, 8, 0};
+    uint64_t prefix = 0, pmask = 0;
+    int64_t need = s.per_block_k;
+    std::vector<uint32_t> hist(2048);
+    for (int pass = 0; pass < 6; ++pass) {
+        const int shift = kShift[pass], nbins = pass == 5 ? 256 : 2048;
+        MA_CUDA(ma::g_launch_hist(g, shift, nbins, prefix, pmask, st));
+        MA_CUDA(cudaMemcpyAsync(hist.data(), h->g_hist, size_t(nbins) * 4, cudaMemcpyDeviceToHost, st));
+        MA_CUDA(cudaStreamSynchronize(st));
+        int64_t above = 0;
+        int d = nbins - 1;
+        for (; d > 0; --d) {
+            if (above + int64_t(hist[size_t(d)]) >= need) break;
+            above += hist[size_t(d)];
+        }
+        need -= above;
+        prefix |= uint64_t(d) << shift;
+        pmask |= uint64_t(nbins - 1) << shift;
+        h->launches += 1;
+    }
+    g.kstar = prefix;  // the k-th largest key; `need` of its ties are selected
+    const int64_t nch = ma::global_chunks(s.dim);
+    MA_CUDA(ma::g_launch_count(g, st));
+    std::vector<int2> cnt(static_cast<size_t>(nch)), info(static_cast<size_t>(nch));
+    MA_CUDA(cudaMemcpyAsync(cnt.data(), h->g_cnt, cnt.size() * sizeof(int2), cudaMemcpyDeviceToHost, st));
+    MA_CUDA(cudaStreamSynchronize(st));
+    int64_t off = 0, ties = need;
+    for (int64_t c = 0; c < nch; ++c) {  // ties go to the lowest indices (compress.cpp:43-48)
+        const int64_t take = std::min<int64_t>(ties, cnt[size_t(c)].y);
+        info[size_t(c)] = make_int2(int(off), int(take));
+        off += cnt[size_t(c)].x + take;
+        ties -= take;
+    }
+    if (off != s.per_block_k) return fail(MA_ERR_CUDA, "global select: row count mismatch");
+    MA_CUDA(cudaMemcpyAsync(h->g_selinfo, info.data(), info.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    MA_CUDA(ma::g_launch_emit(g, st));
+    MA_CUDA(ma::g_launch_requant(g, st));
+    MA_CUDA(cudaMemsetAsync(h->g_z, 0, size_t(s.dim) * 2 * sizeof(double), st));
+    for (int64_t r = 0; r < h->filled; ++r) MA_CUDA(ma::g_launch_stats_row(g, int(r), a.w1[r], a.w2[r], st));
+    MA_CUDA(ma::g_launch_update(g, st));
+    h->launches += 5 + h->filled;
+    h->last_stream = st;
+    if (report) {
+        MA_CUDA(ma::launch_report_reduce(h->d_partials, nch, h->d_report, st));
+        ++h->launches;
+        double r[ma::kReportFields];
+        MA_CUDA(cudaMemcpyAsync(r, h->d_report, sizeof(r), cudaMemcpyDeviceToHost, st));
+        MA_CUDA(cudaStreamSynchronize(st));
+        const double na = std::sqrt(r[1]);
+        report->grad_norm = std::sqrt(r[0]);
+        report->empirical_q = na > 0.0 ? std::sqrt(r[2]) / na : 0.0;
+        report->error_norm = std::sqrt(r[3]);
+        report->update_nnz = static_cast<int64_t>(r[4]);
+        report->loss = 0.0;
+    }
+    return MA_OK;
+}
+
 ma_status run_step(ma_handle* h, void* d_params, const void* d_grads, double lr, cudaStream_t st,
                    ma_step_report* report) {
     if (!(lr > 0.0)) return fail(MA_ERR_INVALID_ARG, "step: lr must be > 0");
@@ -329,6 +451,7 @@ ma_status run_step(ma_handle* h, void* d_params, const void* d_grads, double lr,
         ma_status s = strict_prescan(h, d_grads, st);
         if (s != MA_OK) return s;
     }
+    if (h->shape.global) return run_step_global(h, d_params, d_grads, lr, st, report);
     ma::StepArgs a;
     base_args(h, &a);
     a.grads = d_grads;
@@ -437,6 +560,10 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     const char* warp_exact = std::getenv("MA_WARP_EXACT");
     h->warp_exact = warp_exact && warp_exact[0] == '1';
     if (!h->fast) h->variant = h->tail_variant;
+    if (s.global) {
+        h->fast = h->warp = false;
+        smem = ma::global_requant_smem(s.bucket);
+    }
     if (smem > size_t(smem_max)) {
         delete h;
         return fail(MA_ERR_UNSUPPORTED, "block/window shape needs more shared memory than one SM has");
@@ -448,10 +575,20 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     };
     alloc(reinterpret_cast<void**>(&h->d_codes), size_t(s.code_bytes));
     alloc(reinterpret_cast<void**>(&h->d_meta), size_t(s.nbuckets) * sizeof(double2));
-    alloc(reinterpret_cast<void**>(&h->d_win_idx), went * sizeof(int16_t));
+    alloc(reinterpret_cast<void**>(&h->d_win_idx), went * (s.global ? sizeof(int32_t) : sizeof(int16_t)));
+    if (s.global) {
+        const int64_t nch = ma::global_chunks(s.dim);
+        alloc(reinterpret_cast<void**>(&h->g_level), size_t(s.nbuckets) * sizeof(double));
+        alloc(reinterpret_cast<void**>(&h->g_selbits), size_t(nch) * 256 * sizeof(uint16_t));
+        alloc(reinterpret_cast<void**>(&h->g_hist), 2048 * sizeof(uint32_t));
+        alloc(reinterpret_cast<void**>(&h->g_cnt), size_t(nch) * sizeof(int2));
+        alloc(reinterpret_cast<void**>(&h->g_selinfo), size_t(nch) * sizeof(int2));
+        alloc(reinterpret_cast<void**>(&h->g_z), size_t(s.dim) * 2 * sizeof(double));
+    }
     alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));
     alloc(reinterpret_cast<void**>(&h->d_flag), sizeof(unsigned));
-    alloc(reinterpret_cast<void**>(&h->d_partials), size_t(nb) * ma::kReportFields * sizeof(double));
+    alloc(reinterpret_cast<void**>(&h->d_partials),
+          size_t(s.global ? ma::global_chunks(s.dim) : nb) * ma::kReportFields * sizeof(double));
     alloc(reinterpret_cast<void**>(&h->d_report), ma::kReportFields * sizeof(double));
     alloc(reinterpret_cast<void**>(&h->d_thresh), size_t(nb) * sizeof(uint32_t));
     const char* dbg = std::getenv("MA_DEBUG_COUNTERS");
@@ -618,6 +755,19 @@ ma_status ma_read_window_row(ma_handle* h, int64_t slot, int64_t* indices, doubl
     const Shape& s = h->shape;
     const int64_t nb = s.b1 - s.b0, m = h->cfg.hp.window, kbs = s.kb_stride;
     const size_t vsz = dtype_size(h->cfg.value_dtype);
+    if (s.global) {  // [m][kb_stride] int32 global indices
+        std::vector<int32_t> gi(static_cast<size_t>(s.row_width));
+        std::vector<unsigned char> gv(size_t(s.row_width) * vsz);
+        MA_CUDA(cudaMemcpy(gi.data(), reinterpret_cast<const int32_t*>(h->d_win_idx) + slot * kbs,
+                           gi.size() * 4, cudaMemcpyDeviceToHost));
+        MA_CUDA(cudaMemcpy(gv.data(), static_cast<const char*>(h->d_win_val) + size_t(slot * kbs) * vsz, gv.size(),
+                           cudaMemcpyDeviceToHost));
+        for (int64_t j = 0; j < s.row_width; ++j) {
+            if (indices) indices[j] = gi[size_t(j)];
+            if (values) values[j] = widen(gv.data(), h->cfg.value_dtype, size_t(j));
+        }
+        return MA_OK;
+    }
     // Strided 2-D copy of just this slot: one row of kb_stride per block.
     std::vector<int16_t> idx(size_t(nb * kbs));
     std::vector<unsigned char> val(size_t(nb * kbs) * vsz);
@@ -656,6 +806,39 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
     const int64_t nb = s.b1 - s.b0, kbs = s.kb_stride;
     const int vdt = h->cfg.value_dtype;
     const size_t vsz = dtype_size(vdt);
+    auto put_val = [&](unsigned char* dst, double v) {
+        if (vdt == MA_F64) {
+            std::memcpy(dst, &v, 8);
+        } else if (vdt == MA_F32) {
+            const float f = float(v);
+            std::memcpy(dst, &f, 4);
+        } else {
+            const float f = float(v);  // caller passes bf16-representable values
+            uint32_t u;
+            std::memcpy(&u, &f, 4);
+            const uint16_t hb = uint16_t(u >> 16);
+            std::memcpy(dst, &hb, 2);
+        }
+    };
+    if (s.global) {
+        std::vector<int32_t> gi(static_cast<size_t>(m * kbs), 0);
+        std::vector<unsigned char> gv(size_t(m * kbs) * vsz, 0);
+        for (int64_t r = 0; r < m; ++r)
+            for (int64_t j = 0; j < s.row_width; ++j) {
+                const int64_t idx = win_indices[r * s.row_width + j];
+                if (stamps[r] != 0 && (idx < 0 || idx >= s.dim))
+                    return fail(MA_ERR_INVALID_ARG, "window index outside the vector");
+                gi[size_t(r * kbs + j)] = int32_t(idx < 0 ? 0 : idx);
+                put_val(&gv[size_t(r * kbs + j) * vsz], win_values[r * s.row_width + j]);
+            }
+        MA_CUDA(cudaMemcpy(h->d_win_idx, gi.data(), gi.size() * 4, cudaMemcpyHostToDevice));
+        MA_CUDA(cudaMemcpy(h->d_win_val, gv.data(), gv.size(), cudaMemcpyHostToDevice));
+        h->step = step;
+        h->head = head;
+        h->filled = step < m ? step : m;
+        std::memcpy(h->stamps.data(), stamps, size_t(m) * sizeof(int64_t));
+        return MA_OK;
+    }
     std::vector<int16_t> idx(size_t(nb * m * kbs), 0);
     std::vector<unsigned char> val(size_t(nb * m * kbs) * vsz, 0);
     for (int64_t r = 0; r < m; ++r) {

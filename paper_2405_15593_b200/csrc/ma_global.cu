@@ -1,0 +1,328 @@
+// ma_global.cu — global Top-K mode (MicroAdamOptimizer with blockwise = false,
+// the reference's default: topk_global, compress.cpp:66-71) for d > 8192.
+//
+// Correctness-first pipeline over the whole vector, every decision in the
+// reference's fp64 arithmetic (a = g + (c·level + lo), optim.cpp:166-168,
+// quantize.cpp:164-178):
+//   G0  per-bucket level = (hi - lo) / 15 of the current EF (quantize.cpp:7-13)
+//   G1  radix histograms of the 63-bit |a| keys, six digit passes driven from
+//       the host (11-bit digits, then 8): the exact k-th key K* and how many
+//       ties at K* the selection takes (compress.cpp:39-53: |a| desc, idx asc)
+//   G2  per 4096-chunk counts of keys > K* and == K*
+//   G3  emit: the selected entries in ascending index order at their global
+//       row positions (host prefix sums of G2), the selection bitmap
+//   G4  residual (compress.cpp:95-102) + bucket min/max + 4-bit codes by the
+//       IEEE quotient (quantize.cpp:15-24, 42-55, 102-114), StepReport sums
+//   G5  ADAM_STATS as window.cpp:28-46 does it: dense z1/z2 accumulated row by
+//       row in physical slot order (one launch per row; indices are unique
+//       within a row), then
+//   G6  the update θ -= lr · mhat / (eps + sqrt(vhat)) (optim.cpp:183-187) for
+//       every coordinate with a nonzero accumulator (u = 0 elsewhere).
+// Window rows: int32 global indices [m][row stride] + values.
+#include <math_constants.h>
+
+#include "ma_device.cuh"
+#include "ma_internal.h"
+
+namespace ma {
+namespace {
+
+using namespace dev;
+
+constexpr int kChunk = 4096;     // elements per CTA in G2/G3/G4
+constexpr int kThreads = 256;
+constexpr int kPer = kChunk / kThreads;  // 16 elements per thread (strided by 256)
+
+__device__ __forceinline__ double g_a(const GlobalArgs& p, int64_t i) {
+    const int64_t q = i / p.bucket;
+    const double lo = p.meta[q].x;
+    const uint32_t byte = p.codes[i >> 1];
+    const double c = static_cast<double>((byte >> ((i & 1) * 4)) & 15u);
+    const double e = __dadd_rn(__dmul_rn(c, p.level[q]), lo);
+    return __dadd_rn(ld_val(p.grads, p.g_dtype, i), e);
+}
+
+__global__ void g_levels(GlobalArgs p) {
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < p.nbuckets;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const double2 m = p.meta[q];
+        p.level[q] = m.x == m.y ? 0.0 : __ddiv_rn(__dsub_rn(m.y, m.x), 15.0);
+    }
+}
+
+// One radix digit: histogram of (key >> shift) & (nbins - 1) over keys whose
+// bits above the digit equal `prefix` (under `pmask`).
+__global__ void g_hist(GlobalArgs p, int shift, int nbins, uint64_t prefix, uint64_t pmask) {
+    __shared__ uint32_t h[2048];
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    bool bad = false;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < p.dim;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t k = key_of(g_a(p, i));
+        bad |= (k >> 52) >= 0x7FFu;  // inf / NaN (check_finite in topk_global)
+        if ((k & pmask) == prefix) atomicAdd(&h[(k >> shift) & uint64_t(nbins - 1)], 1u);
+    }
+    if (bad && p.check_finite) atomicOr(p.flag, 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x)
+        if (h[i]) atomicAdd(&p.hist[i], h[i]);
+}
+
+__device__ __forceinline__ int cta_excl_scan(int v, int* s_tmp, int& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = v;
+    for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += t;
+    }
+    if (lane == 31) s_tmp[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int x = lane < kThreads / 32 ? s_tmp[lane] : 0;
+        int xi = x;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, xi, off);
+            if (lane >= off) xi += t;
+        }
+        if (lane < kThreads / 32) s_tmp[lane] = xi - x;
+        if (lane == kThreads / 32 - 1) s_tmp[32] = xi;
+    }
+    __syncthreads();
+    total = s_tmp[32];
+    const int r = s_tmp[w] + incl - v;
+    __syncthreads();
+    return r;
+}
+
+// Counts of keys > K* and == K* per chunk.
+__global__ void g_count(GlobalArgs p) {
+    __shared__ int s_tmp[33];
+    const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+    int gt = 0, eq = 0;
+    for (int j = 0; j < kPer; ++j) {
+        const int64_t i = c0 + j * kThreads + threadIdx.x;
+        if (i >= p.dim) break;
+        const uint64_t k = key_of(g_a(p, i));
+        gt += k > p.kstar;
+        eq += k == p.kstar;
+    }
+    int tg, te;
+    cta_excl_scan(gt, s_tmp, tg);
+    cta_excl_scan(eq, s_tmp, te);
+    if (threadIdx.x == 0) p.cnt[blockIdx.x] = make_int2(tg, te);
+}
+
+// Selected entries of a chunk at their global row positions, ascending index.
+// Thread t owns the 16 consecutive elements [c0 + 16 t, c0 + 16 t + 16).
+__global__ void g_emit(GlobalArgs p) {
+    __shared__ int s_tmp[33];
+    const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+    const int64_t e0 = c0 + int64_t(threadIdx.x) * kPer;
+    const int2 cs = p.sel_info[blockIdx.x];  // (row offset, ties to take in this chunk)
+    uint32_t gtm = 0, eqm = 0;
+    double av[kPer];
+    for (int j = 0; j < kPer; ++j) {
+        av[j] = 0.0;
+        const int64_t i = e0 + j;
+        if (i >= p.dim) continue;
+        av[j] = g_a(p, i);
+        const uint64_t k = key_of(av[j]);
+        gtm |= static_cast<uint32_t>(k > p.kstar) << j;
+        eqm |= static_cast<uint32_t>(k == p.kstar) << j;
+    }
+    int te;
+    int tie_before = cta_excl_scan(__popc(eqm), s_tmp, te);
+    uint32_t selm = gtm;
+    for (int j = 0; j < kPer; ++j)
+        if ((eqm >> j) & 1u) {
+            if (tie_before < cs.y) selm |= 1u << j;
+            ++tie_before;
+        }
+    int tot;
+    int pos = cs.x + cta_excl_scan(__popc(selm), s_tmp, tot);
+    int32_t* ri = p.win_idx + int64_t(p.slot) * p.row_stride;
+    for (int j = 0; j < kPer; ++j)
+        if ((selm >> j) & 1u) {
+            ri[pos] = static_cast<int32_t>(e0 + j);
+            st_val(p.win_val, p.v_dtype, int64_t(p.slot) * p.row_stride + pos, av[j]);
+            ++pos;
+        }
+    if (e0 < p.dim) p.selbits[e0 / kPer] = static_cast<uint16_t>(selm);
+}
+
+// Residual, bucket (lo, hi), 4-bit codes by the IEEE quotient; report sums.
+__global__ void g_requant(GlobalArgs p) {
+    extern __shared__ double s_a[];  // kChunk residuals
+    __shared__ double s_red[kThreads / 32][4];
+    const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+    const int n = static_cast<int>(p.dim - c0 < kChunk ? p.dim - c0 : kChunk);
+    double rep[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = threadIdx.x; j < n; j += kThreads) {
+        const int64_t i = c0 + j;
+        const double a = g_a(p, i);
+        const bool sel = (p.selbits[i / kPer] >> (i % kPer)) & 1u;
+        const double r = sel ? 0.0 : a;
+        s_a[j] = r;
+        if (p.partials) {
+            const double g = ld_val(p.grads, p.g_dtype, i);
+            rep[0] += g * g;
+            rep[1] += a * a;
+            rep[2] += r * r;
+        }
+    }
+    __syncthreads();
+    // buckets inside this chunk (kChunk % bucket == 0): one thread per bucket
+    const int B = static_cast<int>(p.bucket);
+    double* s_lo = reinterpret_cast<double*>(s_a + kChunk);
+    double* s_lv = s_lo + kChunk / 1;  // room for up to kChunk buckets
+    for (int q = threadIdx.x; q * B < n; q += kThreads) {
+        const int j0 = q * B, j1 = j0 + B < n ? j0 + B : n;
+        double lo = s_a[j0], hi = s_a[j0];
+        for (int j = j0 + 1; j < j1; ++j) {
+            const double x = s_a[j];
+            lo = x < lo ? x : lo;
+            hi = x > hi ? x : hi;
+        }
+        const int64_t qg = c0 / B + q;
+        p.meta[qg] = make_double2(lo, hi);
+        s_lo[q] = lo;
+        s_lv[q] = lo == hi ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+    }
+    __syncthreads();
+    // codes: thread t packs bytes (2 elements each) of this chunk
+    for (int jb = threadIdx.x; jb * 2 < n; jb += kThreads) {
+        uint32_t byte = 0;
+        for (int h = 0; h < 2; ++h) {
+            const int j = jb * 2 + h;
+            if (j >= n) break;
+            const int q = j / B;
+            const double level = s_lv[q];
+            uint32_t c = 0;
+            if (level != 0.0) {
+                double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(s_a[j], s_lo[q]), level), 0.5));
+                f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+                c = static_cast<uint32_t>(f);
+            }
+            byte |= c << (4 * h);
+            if (p.partials) {
+                const double en = __dadd_rn(__dmul_rn(static_cast<double>(c), level), s_lo[q]);
+                rep[3] += en * en;
+            }
+        }
+        p.codes[(c0 >> 1) + jb] = static_cast<uint8_t>(byte);
+    }
+    if (p.partials) {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int f = 0; f < 4; ++f) {
+            for (int off = 16; off > 0; off >>= 1) rep[f] += __shfl_xor_sync(0xFFFFFFFFu, rep[f], off);
+            if (lane == 0) s_red[w][f] = rep[f];
+        }
+        __syncthreads();
+        if (threadIdx.x < 4) {
+            double s = 0.0;
+            for (int w2 = 0; w2 < kThreads / 32; ++w2) s += s_red[w2][threadIdx.x];
+            p.partials[int64_t(blockIdx.x) * kReportFields + threadIdx.x] = s;
+        }
+    }
+}
+
+// z[idx] += w · v (or w · v²) for one window row (window.cpp:37-41).
+__global__ void g_stats_row(GlobalArgs p, int r, double w1, double w2) {
+    const int32_t* ri = p.win_idx + int64_t(r) * p.row_stride;
+    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < p.k;
+         j += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t idx = ri[j];
+        const double v = ld_val(p.win_val, p.v_dtype, int64_t(r) * p.row_stride + j);
+        p.z1[idx] = __dadd_rn(p.z1[idx], __dmul_rn(w1, v));
+        p.z2[idx] = __dadd_rn(p.z2[idx], __dmul_rn(w2, __dmul_rn(v, v)));
+    }
+}
+
+// θ -= lr · (z1 s1) / (eps + sqrt(z2 s2)) where the accumulators are nonzero
+// (elsewhere u = 0 / (eps + 0) = 0 and θ is unchanged); nnz per chunk.
+__global__ void g_update(GlobalArgs p) {
+    __shared__ double s_red[kThreads / 32];
+    const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+    double nnz = 0.0;
+    for (int j = threadIdx.x; j < kChunk; j += kThreads) {
+        const int64_t i = c0 + j;
+        if (i >= p.dim) break;
+        const double z1 = p.z1[i], z2 = p.z2[i];
+        if (z1 == 0.0 && z2 == 0.0) continue;
+        const double mhat = __dmul_rn(z1, p.scale1);
+        const double vhat = __dmul_rn(z2, p.scale2);
+        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+        if (u != 0.0) nnz += 1.0;
+        const double th = ld_val(p.params, p.p_dtype, i);
+        st_val(p.params, p.p_dtype, i, __dsub_rn(th, __dmul_rn(p.lr, u)));
+    }
+    if (p.partials) {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int off = 16; off > 0; off >>= 1) nnz += __shfl_xor_sync(0xFFFFFFFFu, nnz, off);
+        if (lane == 0) s_red[w] = nnz;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w2 = 0; w2 < kThreads / 32; ++w2) s += s_red[w2];
+            p.partials[int64_t(blockIdx.x) * kReportFields + 4] = s;
+        }
+    }
+}
+
+unsigned grid_for(int64_t n, int per) {
+    const int64_t want = (n + per - 1) / per;
+    return static_cast<unsigned>(want < 148 * 16 ? (want > 0 ? want : 1) : 148 * 16);
+}
+
+}  // namespace
+
+int64_t global_chunks(int64_t dim) { return (dim + kChunk - 1) / kChunk; }
+
+size_t global_requant_smem(int64_t bucket) {
+    (void)bucket;
+    return size_t(kChunk) * 8 * 3;  // residuals + per-bucket lo + level (up to kChunk buckets)
+}
+
+cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s) {
+    g_levels<<<grid_for(a.nbuckets, 256), 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t g_launch_hist(const GlobalArgs& a, int shift, int nbins, uint64_t prefix, uint64_t pmask,
+                          cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(a.hist, 0, 2048 * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    g_hist<<<grid_for(a.dim, 256 * 16), 256, 0, s>>>(a, shift, nbins, prefix, pmask);
+    return cudaGetLastError();
+}
+
+cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s) {
+    g_count<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t g_launch_emit(const GlobalArgs& a, cudaStream_t s) {
+    g_emit<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s) {
+    const size_t smem = global_requant_smem(a.bucket);
+    cudaError_t e = cudaFuncSetAttribute(g_requant, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    g_requant<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t g_launch_stats_row(const GlobalArgs& a, int r, double w1, double w2, cudaStream_t s) {
+    g_stats_row<<<grid_for(a.k, 256 * 4), 256, 0, s>>>(a, r, w1, w2);
+    return cudaGetLastError();
+}
+
+cudaError_t g_launch_update(const GlobalArgs& a, cudaStream_t s) {
+    g_update<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace ma

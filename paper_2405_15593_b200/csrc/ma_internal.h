@@ -51,6 +51,39 @@ struct StepArgs {
     int64_t stage_b0;
 };
 
+// Global Top-K mode (ma_global.cu, blockwise = false with d > kMaxBlock).
+struct GlobalArgs {
+    const void* grads;
+    void* params;
+    uint8_t* codes;
+    double2* meta;
+    double* level;       // [nbuckets] level of the EF being decoded
+    int32_t* win_idx;    // [m][row_stride] global indices
+    void* win_val;       // [m][row_stride] values (v_dtype)
+    uint16_t* selbits;   // selection bits, 16 elements per word
+    uint32_t* hist;      // [2048] radix histogram
+    int2* cnt;           // [chunks] (keys > K*, keys == K*)
+    const int2* sel_info;  // [chunks] (row offset, ties taken)
+    double* z1;
+    double* z2;
+    double* partials;    // nullable: [chunks][kReportFields]
+    unsigned int* flag;
+    int64_t dim, nbuckets, bucket, k, row_stride;
+    uint64_t kstar;
+    int32_t slot, g_dtype, p_dtype, v_dtype, check_finite;
+    double eps, lr, scale1, scale2;
+};
+int64_t global_chunks(int64_t dim);
+size_t global_requant_smem(int64_t bucket);
+cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s);
+cudaError_t g_launch_hist(const GlobalArgs& a, int shift, int nbins, uint64_t prefix, uint64_t pmask,
+                          cudaStream_t s);
+cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s);
+cudaError_t g_launch_emit(const GlobalArgs& a, cudaStream_t s);
+cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s);
+cudaError_t g_launch_stats_row(const GlobalArgs& a, int r, double w1, double w2, cudaStream_t s);
+cudaError_t g_launch_update(const GlobalArgs& a, cudaStream_t s);
+
 struct Variant {
     int nt;   // threads per CTA
     int ept;  // elements per thread (even)

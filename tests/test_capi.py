@@ -158,3 +158,12 @@ def test_oracle_not_imported_by_product():
                 text = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "liboracle" not in text and "libmicroadam_ref" not in text, f
+
+
+def test_global_mode_shapes(ma):
+    # blockwise = false (the reference default) runs on device for any d < 2^31
+    # with bucket | 4096 (ma_global.cu); d <= 8192 stays a single block
+    assert _validate(ma, dim=100_000, blockwise=0) == ma._capi.MA_OK
+    assert _validate(ma, dim=5_000, blockwise=0, bucket=100) == ma._capi.MA_OK
+    assert _validate(ma, dim=100_000, blockwise=0, bucket=100) == ma._capi.MA_ERR_UNSUPPORTED
+    assert _validate(ma, dim=3_000_000_000, blockwise=0) == ma._capi.MA_ERR_UNSUPPORTED

@@ -1,0 +1,118 @@
+"""Global Top-K mode on the device for d > 8192 (SURVEY.md §8 a16 / §8(f)
+rank 4; the reference's default MicroAdamOptimizer(blockwise=false),
+topk_global compress.cpp:66-71).
+
+fp64 θ/g/window: bit-exact against the UNMODIFIED reference every step (θ, EF
+codes, bucket (lo, hi), window row). bf16/f32 dtypes: bit-exact against the
+composed oracle (block = d). Ties at the k-th key (16-level gradients) take
+the lowest indices; checkpoints are byte-identical to the reference's; the
+host drop-in class matches the reference's StepReport.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests.conftest import cuda_available
+from tests.test_gpu_parity import _bits, _dev, _host, _torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+needs_ref = pytest.mark.skipif(not oracle.reference_available(), reason="needs /root/reference")
+
+
+def _global_engine(d, hp, dt, vdt):
+    from paper_2405_15593_b200 import MicroAdam
+    return MicroAdam(d, hp, param_dtype=dt, grad_dtype=dt, value_dtype=vdt, blockwise=False)
+
+
+@needs_ref
+@pytest.mark.parametrize("d,hp,levels", [
+    (50_000, dict(lr=1e-2, window=4), False),
+    (100_003, dict(lr=1e-2, window=3, bucket=32), False),
+    (40_000, dict(lr=1e-2, window=5, k=777), True),   # 16-level grads: ties at K*
+])
+def test_global_fp64_matches_unmodified_reference(d, hp, levels):
+    torch = _torch()
+    th0 = oracle.synth(1, 0, 0, d)
+    ref = oracle.Reference(th0, hp, blockwise=False)
+    eng = _global_engine(d, hp, "f64", "f64")
+    p = _dev(th0, "f64")
+    for s in range(1, 8):
+        g = oracle.synth(42, s, 0, d, levels=levels)
+        ref.step(g)
+        eng.step(p, _dev(g, "f64"), hp["lr"])
+        torch.cuda.synchronize()
+        st = ref.state()
+        head = eng.counters()[1]
+        slot = (head + hp["window"] - 1) % hp["window"]
+        assert np.array_equal(eng.window().indices[slot], st.last_idx), f"selection @ {s}"
+        assert np.array_equal(eng.error_buffer().codes, st.codes), f"codes @ {s}"
+        assert np.array_equal(_bits(eng.error_buffer().lo), _bits(st.lo)), f"lo @ {s}"
+        assert np.array_equal(_bits(_host(p)), _bits(st.params)), f"θ @ {s}"
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_global_low_precision_matches_composed_oracle(dt):
+    d = 30_011
+    hp = dict(lr=1e-2, window=4, density=0.02)
+    torch = _torch()
+    th0 = _host(_dev(oracle.synth(1, 0, 0, d, dt), dt))
+    orc = oracle.Oracle(th0, dict(hp, block=d), param_dtype=dt, value_dtype="bf16")
+    eng = _global_engine(d, hp, dt, "bf16")
+    p = _dev(th0, dt)
+    for s in range(1, 8):
+        g = _host(_dev(oracle.synth(42, s, 0, d, dt), dt))
+        orc.step(g, hp["lr"])
+        eng.step(p, _dev(g, dt), hp["lr"])
+        torch.cuda.synchronize()
+        so = orc.state()
+        assert np.array_equal(eng.error_buffer().codes, so.codes), f"codes @ {s}"
+        assert np.array_equal(_bits(_host(p)), _bits(so.params)), f"θ @ {s}"
+        w = eng.window()
+        for r in range(eng.counters()[2]):
+            assert np.array_equal(w.indices[r], so.win_idx[r])
+            assert np.array_equal(_bits(w.values[r]), _bits(so.win_val[r]))
+
+
+@needs_ref
+def test_global_dropin_class_and_checkpoint_match_reference(tmp_path):
+    from paper_2405_15593_b200 import MicroAdamOptimizer
+    d, hp = 20_000, dict(lr=1e-2, window=3)
+    th0 = oracle.synth(1, 0, 0, d)
+    opt = MicroAdamOptimizer(th0, hp, blockwise=False)
+    ref = oracle.Reference(th0, hp, blockwise=False)
+    for s in range(1, 6):
+        g = oracle.synth(42, s, 0, d)
+        rep = opt.step(g)
+        rrep = ref.step(g)
+        assert np.array_equal(_bits(opt.params()), _bits(ref.state().params))
+        assert rep.update_nnz == rrep["update_nnz"]
+        assert abs(rep.grad_norm - rrep["grad_norm"]) <= 1e-12 * rrep["grad_norm"]
+        assert abs(rep.error_norm - rrep["error_norm"]) <= 1e-12 * max(rrep["error_norm"], 1e-300)
+    a, b = str(tmp_path / "ref.madm"), str(tmp_path / "dev.madm")
+    ref.save_checkpoint(a)
+    eng = _global_engine(d, hp, "f64", "f64")
+    p = _dev(th0, "f64")
+    for s in range(1, 6):
+        eng.step(p, _dev(oracle.synth(42, s, 0, d), "f64"), hp["lr"])
+    eng.synchronize()
+    eng.save_checkpoint(b, p)
+    assert open(a, "rb").read() == open(b, "rb").read()
+
+
+def test_global_mode_tie_heavy_f32():
+    # 16-level gradients (ties at the k-th key), m = 2, f32 window values
+    hp = dict(lr=1e-2, window=2, density=0.003)
+    d = 12_345
+    torch = _torch()
+    th0 = _host(_dev(oracle.synth(1, 0, 0, d, "f32"), "f32"))
+    orc = oracle.Oracle(th0, dict(hp, block=d), param_dtype="f32", value_dtype="f32")
+    eng = _global_engine(d, hp, "f32", "f32")
+    p = _dev(th0, "f32")
+    for s in range(1, 6):
+        g = _host(_dev(oracle.synth(5, s, 0, d, "f32", levels=True), "f32"))
+        orc.step(g, hp["lr"])
+        eng.step(p, _dev(g, "f32"), hp["lr"])
+    torch.cuda.synchronize()
+    so = orc.state()
+    assert np.array_equal(_bits(_host(p)), _bits(so.params))
+    assert np.array_equal(eng.error_buffer().codes, so.codes)
