@@ -393,3 +393,17 @@ def test_bf16_subnormal_window_values():
     # device vs the oracle's software RNE).
     run_parity(4096 * 3, dict(lr=1e-3), gdt="f64", pdt="f64", vdt="bf16", steps=5,
                grad_fn=lambda s: oracle.synth(5, s, 0, 4096 * 3) * 2.0 ** -133)
+
+
+def test_reference_side_adapter_drives_reference_run_loop():
+    """INTEGRATION.md's adapter, compiled against the unmodified reference
+    headers/sources (oracle/_ref/adapter_check), run through the reference's
+    own run() loop: every iterate bit-identical to the reference optimizer."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(oracle.__file__), "_ref", "adapter_check")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/adapter_check not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "adapter ok" in out.stdout
