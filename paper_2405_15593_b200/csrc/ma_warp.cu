@@ -873,9 +873,6 @@ constexpr float kTwo23 = 8388608.0f;
 #ifndef MA_LEAN_CAPL
 #define MA_LEAN_CAPL 4  // lean kernel: exact-stage candidate slots per lane
 #endif
-#ifndef MA_LEAN_L1PF
-#define MA_LEAN_L1PF 0  // L1 prefetch of θ / window rows at the start of ADAM_STATS
-#endif
 #ifndef MA_LEAN_PROF
 #define MA_LEAN_PROF 0  // per-phase warp clock64 accumulation into dbg[8..] (profiling builds only)
 #endif
@@ -1583,19 +1580,6 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     if (p.dbg) prof_mark(p, 5);
 #endif
     // ---- ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) ----
-#if MA_LEAN_L1PF
-    {   // pull the block's θ lines and window rows into L1 while the bitmaps are built
-        const unsigned char* tp = static_cast<const unsigned char*>(p.params) + base * psz;
-        for (int o = lane * 128; o < kBlk * psz; o += 32 * 128)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + o));
-        const int rb = m * kbs * (2 + vsz);
-        for (int o = lane * 128; o < m * kbs * 2; o += 32 * 128)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const unsigned char*>(gwi) + o));
-        for (int o = lane * 128; o < m * kbs * vsz; o += 32 * 128)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(gwv + o));
-        (void)rb;
-    }
-#endif
     // Entry t = row r (physical slot) * k_b + position pos; each lane walks
     // t = lane, lane + 32, ... with (r, pos) advanced incrementally.
     const int nent = filled * kb;
