@@ -79,7 +79,7 @@ typedef struct ma_hyperparams {
 typedef struct ma_config {
     ma_hyperparams hp;
     int32_t blockwise;      /* 1 (the device path); 0 = global Top-K, run as one block when d <= 8192 */
-    int32_t lossless_error; /* 0 (quantized EF); 1 unsupported on device */
+    int32_t lossless_error; /* 0 (quantized EF); 1 = dense fp64 residual (blockwise, generic kernel) */
     int32_t param_dtype;    /* ma_dtype of θ in device memory */
     int32_t grad_dtype;     /* ma_dtype of the gradient */
     int32_t value_dtype;    /* ma_dtype of window values (bf16 = the paper's layout) */
@@ -161,6 +161,12 @@ MA_API ma_status ma_get_counters(const ma_handle* h, int64_t* step, int64_t* hea
 /* error_buffer() (optim.cpp:155-158): packed codes (code_bytes) and per-bucket
  * (lo, hi) as fp64 (num_buckets each), host buffers, for the handle's range. */
 MA_API ma_status ma_read_error_buffer(ma_handle* h, uint8_t* codes, double* lo, double* hi);
+
+/* error_vector() (optim.cpp:160-162): the dense error feedback in fp64 (dim
+ * entries): the decoded 4-bit buffer, or the stored residual of a
+ * lossless_error engine (for which ma_read_error_buffer returns MA_ERR_STATE,
+ * like error_buffer() throwing std::logic_error, optim.cpp:155-158). */
+MA_API ma_status ma_read_error_vector(ma_handle* h, double* out);
 
 /* window().rows[slot] in the reference layout: row_width global int64 indices
  * (ascending) and values widened to fp64. Returns MA_ERR_INVALID_ARG for slot

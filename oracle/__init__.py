@@ -246,6 +246,12 @@ class Oracle:
     def _arr(self, ptr, n, dtype):
         return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
 
+    def error_vector(self) -> np.ndarray:
+        """error_vector() (optim.cpp:160-162)."""
+        out = np.zeros(self.dim)
+        self.L.ref_error_vector(self.h, out)
+        return out
+
     def save_checkpoint(self, path: str) -> None:
         """The reference's own save_checkpoint (checkpoint.cpp:50-86)."""
         if self.L.ref_save_checkpoint(self.h, os.fsencode(path)) != 0:
@@ -304,6 +310,12 @@ class Reference:
             raise ValueError(self.L.ref_last_error().decode())
         return {"grad_norm": rep[0], "error_norm": rep[1], "empirical_q": rep[2],
                 "update_nnz": int(rep[3])}
+
+    def error_vector(self) -> np.ndarray:
+        """error_vector() (optim.cpp:160-162)."""
+        out = np.zeros(self.dim)
+        self.L.ref_error_vector(self.h, out)
+        return out
 
     def save_checkpoint(self, path: str) -> None:
         """The reference's own save_checkpoint (checkpoint.cpp:50-86)."""

@@ -84,8 +84,6 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
         if (dt < MA_F64 || dt > MA_BF16) return fail(MA_ERR_INVALID_ARG, "unknown dtype");
     if (cfg->finite_mode < MA_FINITE_FLAG || cfg->finite_mode > MA_FINITE_OFF)
         return fail(MA_ERR_INVALID_ARG, "unknown finite_mode");
-    if (cfg->lossless_error)
-        return fail(MA_ERR_UNSUPPORTED, "lossless_error (dense EF test hook) is not on the device path");
     if (hp.bits != 4) return fail(MA_ERR_UNSUPPORTED, "device path implements bits = 4");
     if (hp.window > ma::kMaxWindow) return fail(MA_ERR_UNSUPPORTED, "window > 256 not supported on device");
 
@@ -117,6 +115,8 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
             return fail(MA_ERR_UNSUPPORTED, "global mode on device needs bucket | 4096");
         if (b0 != 0 || (b1 >= 0 && b1 != 1))
             return fail(MA_ERR_UNSUPPORTED, "global mode cannot be block-sharded");
+        if (cfg->lossless_error)
+            return fail(MA_ERR_UNSUPPORTED, "global mode with lossless_error is not on the device path");
         s.global = true;
     } else if (s.block > ma::kMaxBlock) {
         return fail(MA_ERR_UNSUPPORTED, "block > 8192 not supported on device");
@@ -188,6 +188,7 @@ struct ma_handle {
     int2* g_cnt = nullptr;
     int2* g_selinfo = nullptr;
     double* g_z = nullptr;
+    double* d_dense = nullptr;  // lossless error feedback (fp64 residual, dim elements)
     // host counters (window.hpp:10-33)
     int64_t step = 0, head = 0, filled = 0;
     std::vector<int64_t> stamps;
@@ -237,6 +238,7 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_cnt);
     cudaFree(h->g_selinfo);
     cudaFree(h->g_z);
+    cudaFree(h->d_dense);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
     delete h->pending;
     delete h;
@@ -292,6 +294,7 @@ void base_args(ma_handle* h, ma::StepArgs* a) {
     a->v_dtype = h->cfg.value_dtype;
     a->eps = h->cfg.hp.eps;
     a->force_exact = h->warp_exact ? 1 : 0;
+    a->dense = h->d_dense;
 }
 
 // Fast path: the persistent kernel takes the range's full blocks and the
@@ -564,6 +567,10 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         h->fast = h->warp = false;
         smem = ma::global_requant_smem(s.bucket);
     }
+    if (cfg->lossless_error) {  // dense fp64 EF: the generic kernel
+        h->fast = h->warp = false;
+        h->variant = h->tail_variant;
+    }
     if (smem > size_t(smem_max)) {
         delete h;
         return fail(MA_ERR_UNSUPPORTED, "block/window shape needs more shared memory than one SM has");
@@ -587,6 +594,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     }
     alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));
     alloc(reinterpret_cast<void**>(&h->d_flag), sizeof(unsigned));
+    if (cfg->lossless_error) alloc(reinterpret_cast<void**>(&h->d_dense), size_t(s.dim) * sizeof(double));
     alloc(reinterpret_cast<void**>(&h->d_partials),
           size_t(s.global ? ma::global_chunks(s.dim) : nb) * ma::kReportFields * sizeof(double));
     alloc(reinterpret_cast<void**>(&h->d_report), ma::kReportFields * sizeof(double));
@@ -722,6 +730,7 @@ ma_status ma_get_counters(const ma_handle* h, int64_t* step, int64_t* head, int6
 
 ma_status ma_read_error_buffer(ma_handle* h, uint8_t* codes, double* lo, double* hi) {
     if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
+    if (h->d_dense) return fail(MA_ERR_STATE, "error_buffer: engine uses dense error storage");
     DeviceGuard g(h->device);
     MA_CUDA(cudaDeviceSynchronize());
     if (codes) MA_CUDA(cudaMemcpy(codes, h->d_codes, size_t(h->shape.code_bytes), cudaMemcpyDeviceToHost));
@@ -746,6 +755,29 @@ double widen(const void* p, int dt, size_t i) {
     return double(f);
 }
 }  // namespace
+
+ma_status ma_read_error_vector(ma_handle* h, double* out) {
+    if (!h || !out) return fail(MA_ERR_INVALID_ARG, "null argument");
+    DeviceGuard g(h->device);
+    MA_CUDA(cudaDeviceSynchronize());
+    const Shape& s = h->shape;
+    if (h->d_dense) {
+        MA_CUDA(cudaMemcpy(out, h->d_dense, size_t(s.dim) * sizeof(double), cudaMemcpyDeviceToHost));
+        return MA_OK;
+    }
+    // QuantizedErrorBuffer::decode (quantize.cpp:164-178): c * level + lo
+    std::vector<uint8_t> codes(static_cast<size_t>(s.code_bytes));
+    std::vector<double2> meta(static_cast<size_t>(s.nbuckets));
+    MA_CUDA(cudaMemcpy(codes.data(), h->d_codes, codes.size(), cudaMemcpyDeviceToHost));
+    MA_CUDA(cudaMemcpy(meta.data(), h->d_meta, meta.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < s.dim; ++i) {
+        const double2 m = meta[size_t(i / s.bucket)];
+        const double level = m.x == m.y ? 0.0 : (m.y - m.x) / 15.0;
+        const double c = double((codes[size_t(i >> 1)] >> ((i & 1) * 4)) & 15u);
+        out[i] = c * level + m.x;
+    }
+    return MA_OK;
+}
 
 ma_status ma_read_window_row(ma_handle* h, int64_t slot, int64_t* indices, double* values) {
     if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
@@ -929,7 +961,7 @@ ma_status ma_save_checkpoint(ma_handle* h, const void* params, int32_t params_on
     if (!cf.f) return fail(MA_ERR_INVALID_ARG, std::string("checkpoint: cannot open ") + path + " for writing");
     std::FILE* f = cf.f;
     const int64_t m = h->cfg.hp.window;
-    const unsigned char head8[6] = {'M', 'A', 'D', 'M', 1, 0};  // magic, version, lossless = 0
+    const unsigned char head8[6] = {'M', 'A', 'D', 'M', 1, h->d_dense ? 1 : 0};  // magic, version, lossless
     bool ok = put_bytes(f, head8, 6) && put_i64(f, s.dim) && put_i64(f, h->step);
     // θ (optim.hpp params()) widened to f64
     const int pdt = h->cfg.param_dtype;
@@ -954,6 +986,15 @@ ma_status ma_save_checkpoint(ma_handle* h, const void* params, int32_t params_on
         if (st != MA_OK) return st;
         ok = put_i64(f, h->stamps[size_t(r)]) && put_bytes(f, idx.data(), idx.size() * 8) &&
              put_f64s(f, val.data(), val.size());
+    }
+    if (h->d_dense) {  // lossless: the dense error vector (checkpoint.cpp:72-73)
+        std::vector<double> ev(static_cast<size_t>(s.dim));
+        ma_status st = ma_read_error_vector(h, ev.data());
+        if (st != MA_OK) return st;
+        ok = ok && put_f64s(f, ev.data(), ev.size());
+        if (!ok || std::fflush(f) != 0)
+            return fail(MA_ERR_INVALID_ARG, std::string("checkpoint: write failed for ") + path);
+        return MA_OK;
     }
     std::vector<uint8_t> codes(static_cast<size_t>(s.code_bytes));
     std::vector<double> lo(static_cast<size_t>(s.nbuckets)), hi(static_cast<size_t>(s.nbuckets));
@@ -981,7 +1022,8 @@ ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_devic
     if (!get_bytes(f, head8, 6)) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
     if (std::memcmp(head8, "MADM", 4) != 0) return fail(MA_ERR_INVALID_ARG, "checkpoint: bad magic");
     if (head8[4] != 1) return fail(MA_ERR_INVALID_ARG, "checkpoint: unsupported version");
-    if (head8[5] != 0) return fail(MA_ERR_UNSUPPORTED, "checkpoint: lossless error buffers are not supported on device");
+    if ((head8[5] != 0) != (h->d_dense != nullptr))
+        return fail(MA_ERR_INVALID_ARG, "checkpoint: lossless flag does not match the optimizer");
     int64_t dim = 0, step = 0, cap = 0, rw = 0, head = 0, filled = 0;
     if (!get_i64(f, &dim) || !get_i64(f, &step)) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
     if (dim != s.dim) return fail(MA_ERR_DIM, "checkpoint: dimension differs from the optimizer's");
@@ -1024,6 +1066,18 @@ ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_devic
         if (!get_i64(f, &stamps[size_t(r)]) || !get_bytes(f, &idx[size_t(r * rw)], size_t(rw) * 8) ||
             !get_f64s(f, &val[size_t(r * rw)], size_t(rw)))
             return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    }
+    if (h->d_dense) {  // lossless: dense error vector, then the window state
+        std::vector<double> ev(static_cast<size_t>(dim));
+        if (!get_f64s(f, ev.data(), ev.size())) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+        MA_CUDA(cudaMemcpy(h->d_dense, ev.data(), ev.size() * sizeof(double), cudaMemcpyHostToDevice));
+        std::vector<uint8_t> zc(static_cast<size_t>(s.code_bytes), 0);
+        std::vector<double> z0(static_cast<size_t>(s.nbuckets), 0.0);
+        ma_status st = ma_write_state(h, zc.data(), z0.data(), z0.data(), step, head, stamps.data(), idx.data(),
+                                      val.data());
+        if (st != MA_OK) return st;
+        if (params && !params_on_device) h->theta_valid = false;
+        return MA_OK;
     }
     unsigned char bits = 0;
     int64_t bucket = 0, nbk = 0, nbytes = 0;

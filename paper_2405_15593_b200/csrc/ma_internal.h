@@ -49,6 +49,9 @@ struct StepArgs {
     int16_t* stage_idx;
     void* stage_val;
     int64_t stage_b0;
+    // lossless error feedback (MicroAdamOptimizer(..., lossless_error = true),
+    // optim.cpp:172-173): the residual kept dense in fp64 (generic kernel only)
+    double* dense;
 };
 
 // Global Top-K mode (ma_global.cu, blockwise = false with d > kMaxBlock).

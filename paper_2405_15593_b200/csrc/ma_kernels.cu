@@ -191,10 +191,10 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
                 ld_pair(p.grads, p.g_dtype, base + e, g0, g1);
             else
                 g0 = ld_val(p.grads, p.g_dtype, base + e);
-            const uint32_t byte = p.codes[(base + e) >> 1];
+            const uint32_t byte = p.dense ? 0u : p.codes[(base + e) >> 1];
             const int bA = e / bucket;
-            const double e0 =
-                __dadd_rn(__dmul_rn(static_cast<double>(byte & 15u), s_lvl[bA]), s_lo[bA]);
+            const double e0 = p.dense ? p.dense[base + e]
+                                      : __dadd_rn(__dmul_rn(static_cast<double>(byte & 15u), s_lvl[bA]), s_lo[bA]);
             a[2 * j] = __dadd_rn(g0, e0);
             valid |= 1u << (2 * j);
             bad |= !isfinite(g0) || !isfinite(a[2 * j]);
@@ -204,8 +204,8 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
             }
             if (two) {
                 const int bB = (e + 1) / bucket;
-                const double e1 =
-                    __dadd_rn(__dmul_rn(static_cast<double>(byte >> 4), s_lvl[bB]), s_lo[bB]);
+                const double e1 = p.dense ? p.dense[base + e + 1]
+                                          : __dadd_rn(__dmul_rn(static_cast<double>(byte >> 4), s_lvl[bB]), s_lo[bB]);
                 a[2 * j + 1] = __dadd_rn(g1, e1);
                 valid |= 1u << (2 * j + 1);
                 bad |= !isfinite(g1) || !isfinite(a[2 * j + 1]);
@@ -258,8 +258,15 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
     }
     __syncthreads();
 
+    // ---- lossless EF: the residual itself is the new error (optim.cpp:172-173) ----
+    if (p.dense) {
+        for (int i = tid; i < len; i += NT) {
+            p.dense[base + i] = s_a[i];
+            if (want_report) rep[3] += s_a[i] * s_a[i];
+        }
+    }
     // ---- P4: re-quantize the residual (quantize.cpp:15-24, 42-55, 142-162) ----
-    for (int bk = warp; bk < nbk; bk += NW) {
+    for (int bk = p.dense ? nbk : warp; bk < nbk; bk += NW) {
         const int s = bk * bucket;
         const int n = min(bucket, len - s);
         double lo = s_a[s], hi = s_a[s];
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
     __syncthreads();
 
     // ---- P5: nibble pack (quantize.cpp:102-114) ----
-    for (int i = tid; i < (len + 1) / 2; i += NT) {
+    for (int i = p.dense ? (len + 1) / 2 : tid; i < (len + 1) / 2; i += NT) {
         const uint32_t lo4 = s_code[2 * i];
         const uint32_t hi4 = (2 * i + 1 < len) ? s_code[2 * i + 1] : 0u;
         p.codes[(base >> 1) + i] = static_cast<uint8_t>(lo4 | (hi4 << 4));

@@ -162,6 +162,7 @@ MicroAdamOptimizer::MicroAdamOptimizer(Vec theta0, HyperParams hp, bool blockwis
     cfg.hp = hp_.to_c();
     cfg.blockwise = blockwise ? 1 : 0;
     cfg.lossless_error = lossless_error ? 1 : 0;
+    lossless_ = lossless_error;
     cfg.param_dtype = MA_F64;
     cfg.grad_dtype = MA_F64;
     cfg.value_dtype = MA_F64;
@@ -197,7 +198,11 @@ QuantizedErrorBuffer MicroAdamOptimizer::error_buffer() const {
     return read_error(h_, static_cast<int64_t>(theta_.size()), hp_);
 }
 
-Vec MicroAdamOptimizer::error_vector() const { return error_buffer().decode(); }
+Vec MicroAdamOptimizer::error_vector() const {  // optim.cpp:160-162
+    Vec out(theta_.size());
+    check(ma_read_error_vector(h_, out.data()));
+    return out;
+}
 
 int64_t MicroAdamOptimizer::step_count() const {
     int64_t s = 0;

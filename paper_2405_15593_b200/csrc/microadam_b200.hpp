@@ -147,7 +147,7 @@ public:
 
     GradientWindow window() const;
     QuantizedErrorBuffer error_buffer() const;
-    bool lossless() const { return false; }
+    bool lossless() const { return lossless_; }
     Vec error_vector() const;
     const SparseSelection& last_selection() const { return last_sel_; }
     int64_t step_count() const;
@@ -160,6 +160,7 @@ private:
     HyperParams hp_;
     ma_handle* h_ = nullptr;
     SparseSelection last_sel_;
+    bool lossless_ = false;
 };
 
 // save_checkpoint(path, opt) / resume (checkpoint.hpp:28-33): the reference's

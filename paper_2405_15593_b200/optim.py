@@ -428,13 +428,24 @@ class MicroAdamOptimizer(_Handle):
         return "microadam"
 
     def lossless(self) -> bool:
-        return False
+        return bool(self.cfg.lossless_error)
 
     def error_vector(self) -> np.ndarray:
-        return self.error_buffer().decode()
+        """error_vector() (optim.cpp:160-162): decoded EF, or the dense residual."""
+        out = np.zeros(self.layout.dim)
+        _ok(lib().ma_read_error_vector(self._h, out.ctypes.data))
+        return out
 
     def last_selection(self) -> SparseSelection:
         return self._last
+
+    def save_checkpoint(self, path: str) -> None:
+        """save_checkpoint(path, opt) (checkpoint.hpp:28-33): the MADM v1 file."""
+        _ok(lib().ma_save_checkpoint(self._h, self._theta.ctypes.data, 0, os.fsencode(path)))
+
+    def load_checkpoint(self, path: str) -> None:
+        """Resume from a MADM v1 file (θ into params(), state into the device)."""
+        _ok(lib().ma_load_checkpoint(self._h, self._theta.ctypes.data, 0, os.fsencode(path)))
 
     def step_count(self) -> int:
         return self.counters()[0]

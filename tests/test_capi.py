@@ -108,7 +108,8 @@ def test_k_exceeding_dim_rejected(ma):  # optim.cpp:23-26
 
 
 @pytest.mark.parametrize("kw", [dict(bits=8), dict(block=16384), dict(bucket=100),
-                                dict(block=4095), dict(lossless_error=1), dict(window=300)])
+                                dict(block=4095), dict(window=300),
+                                dict(lossless_error=1, blockwise=0)])
 def test_unsupported_device_shapes_are_explicit(ma, kw):
     assert _validate(ma, dim=100_000, **kw) == ma._capi.MA_ERR_UNSUPPORTED
 
@@ -167,3 +168,8 @@ def test_global_mode_shapes(ma):
     assert _validate(ma, dim=5_000, blockwise=0, bucket=100) == ma._capi.MA_OK
     assert _validate(ma, dim=100_000, blockwise=0, bucket=100) == ma._capi.MA_ERR_UNSUPPORTED
     assert _validate(ma, dim=3_000_000_000, blockwise=0) == ma._capi.MA_ERR_UNSUPPORTED
+
+
+def test_lossless_blockwise_is_supported(ma):
+    # MicroAdamOptimizer(..., lossless_error = true) (optim.hpp:103-104): dense fp64 EF
+    assert _validate(ma, dim=100_000, lossless_error=1) == ma._capi.MA_OK
