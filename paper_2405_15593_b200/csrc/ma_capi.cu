@@ -84,7 +84,7 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
         if (dt < MA_F64 || dt > MA_BF16) return fail(MA_ERR_INVALID_ARG, "unknown dtype");
     if (cfg->finite_mode < MA_FINITE_FLAG || cfg->finite_mode > MA_FINITE_OFF)
         return fail(MA_ERR_INVALID_ARG, "unknown finite_mode");
-    if (hp.bits != 4) return fail(MA_ERR_UNSUPPORTED, "device path implements bits = 4");
+    if (hp.bits > 8) return fail(MA_ERR_UNSUPPORTED, "device path implements bits <= 8");
     if (hp.window > ma::kMaxWindow) return fail(MA_ERR_UNSUPPORTED, "window > 256 not supported on device");
 
     Shape s;
@@ -117,6 +117,7 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
             return fail(MA_ERR_UNSUPPORTED, "global mode cannot be block-sharded");
         if (cfg->lossless_error)
             return fail(MA_ERR_UNSUPPORTED, "global mode with lossless_error is not on the device path");
+        if (hp.bits != 4) return fail(MA_ERR_UNSUPPORTED, "global mode on device implements bits = 4");
         s.global = true;
     } else if (s.block > ma::kMaxBlock) {
         return fail(MA_ERR_UNSUPPORTED, "block > 8192 not supported on device");
@@ -141,7 +142,11 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
     s.bucket = hp.bucket;
     s.bucket0 = s.elem0 / hp.bucket;
     s.nbuckets = (s.dim + hp.bucket - 1) / hp.bucket;
-    s.code_bytes = (s.dim * 4 + 7) / 8;
+    s.code_bytes = (s.dim * hp.bits + 7) / 8;
+    if (hp.bits != 4 && s.nblocks_global > 1 && (s.block * hp.bits) % 8 != 0)
+        return fail(MA_ERR_UNSUPPORTED, "bits != 4 needs block * bits to be a multiple of 8");
+    if (hp.bits != 4 && (s.elem0 * hp.bits) % 8 != 0)
+        return fail(MA_ERR_UNSUPPORTED, "bits != 4 shards must start on a byte boundary");
     s.kb_stride = (s.per_block_k + 7) / 8 * 8;
     *out = s;
     return MA_OK;
@@ -295,6 +300,7 @@ void base_args(ma_handle* h, ma::StepArgs* a) {
     a->eps = h->cfg.hp.eps;
     a->force_exact = h->warp_exact ? 1 : 0;
     a->dense = h->d_dense;
+    a->bits = static_cast<int32_t>(h->cfg.hp.bits);
 }
 
 // Fast path: the persistent kernel takes the range's full blocks and the
@@ -567,7 +573,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         h->fast = h->warp = false;
         smem = ma::global_requant_smem(s.bucket);
     }
-    if (cfg->lossless_error) {  // dense fp64 EF: the generic kernel
+    if (cfg->lossless_error || cfg->hp.bits != 4) {  // dense EF / other code widths: the generic kernel
         h->fast = h->warp = false;
         h->variant = h->tail_variant;
     }
@@ -770,10 +776,15 @@ ma_status ma_read_error_vector(ma_handle* h, double* out) {
     std::vector<double2> meta(static_cast<size_t>(s.nbuckets));
     MA_CUDA(cudaMemcpy(codes.data(), h->d_codes, codes.size(), cudaMemcpyDeviceToHost));
     MA_CUDA(cudaMemcpy(meta.data(), h->d_meta, meta.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+    const int bits = int(h->cfg.hp.bits);
+    const double max_code = double((1u << bits) - 1u);
     for (int64_t i = 0; i < s.dim; ++i) {
         const double2 m = meta[size_t(i / s.bucket)];
-        const double level = m.x == m.y ? 0.0 : (m.y - m.x) / 15.0;
-        const double c = double((codes[size_t(i >> 1)] >> ((i & 1) * 4)) & 15u);
+        const double level = m.x == m.y ? 0.0 : (m.y - m.x) / max_code;
+        const int64_t pos = i * bits;  // LSB-first bit stream (quantize.cpp:116-128)
+        uint32_t w = codes[size_t(pos >> 3)];
+        if ((pos & 7) + bits > 8) w |= uint32_t(codes[size_t((pos >> 3) + 1)]) << 8;
+        const double c = double((w >> (pos & 7)) & ((1u << bits) - 1u));
         out[i] = c * level + m.x;
     }
     return MA_OK;

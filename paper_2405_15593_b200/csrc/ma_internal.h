@@ -52,6 +52,8 @@ struct StepArgs {
     // lossless error feedback (MicroAdamOptimizer(..., lossless_error = true),
     // optim.cpp:172-173): the residual kept dense in fp64 (generic kernel only)
     double* dense;
+    int32_t bits;  // EF code width; the generic kernel handles 1..8, the others 4
+    int32_t pad1;
 };
 
 // Global Top-K mode (ma_global.cu, blockwise = false with d > kMaxBlock).

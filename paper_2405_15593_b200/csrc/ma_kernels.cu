@@ -66,6 +66,16 @@ struct SmemLayout {
 // Exclusive rank, in element order, of the flagged elements of the block.
 // Thread `tid` holds elements e = 2*(j*NT + tid) + p at register slot 2j+p, so
 // element order is (j, warp, lane, p). Returns the flagged total.
+// Code of element i in the LSB-first bit stream of width `bits` (quantize.cpp:116-128).
+__device__ __forceinline__ uint32_t read_code(const uint8_t* codes, int64_t i, int bits) {
+    const int64_t pos = i * bits;
+    const int64_t byte0 = pos >> 3;
+    const int sh = static_cast<int>(pos & 7);
+    uint32_t w = codes[byte0];
+    if (sh + bits > 8) w |= static_cast<uint32_t>(codes[byte0 + 1]) << 8;
+    return (w >> sh) & ((1u << bits) - 1u);
+}
+
 template <int NT, int EPT>
 __device__ __forceinline__ int block_rank(uint32_t flags, int (&rank)[EPT], int* scan) {
     constexpr int NW = NT / 32;
@@ -163,13 +173,15 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
     const int nbk = (len + bucket - 1) / bucket;
     const int64_t bk0 = base / bucket;
     const bool want_report = p.partials != nullptr;
+    const int bits = p.bits;
+    const double max_code = static_cast<double>((1u << bits) - 1u);  // QuantParams::max_code
     auto elem = [&](int i) { return 2 * ((i >> 1) * NT + tid) + (i & 1); };
 
     // ---- P0: old bucket grids (QuantParams ctor, quantize.cpp:7-13) ----
     for (int i = tid; i < nbk; i += NT) {
         const double2 mt = p.meta[bk0 + i];
         s_lo[i] = mt.x;
-        s_lvl[i] = (mt.x == mt.y) ? 0.0 : __ddiv_rn(__dsub_rn(mt.y, mt.x), 15.0);
+        s_lvl[i] = (mt.x == mt.y) ? 0.0 : __ddiv_rn(__dsub_rn(mt.y, mt.x), max_code);
     }
     for (int i = tid; i < len; i += NT) s_selm[i] = 0;
     __syncthreads();
@@ -191,10 +203,11 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
                 ld_pair(p.grads, p.g_dtype, base + e, g0, g1);
             else
                 g0 = ld_val(p.grads, p.g_dtype, base + e);
-            const uint32_t byte = p.dense ? 0u : p.codes[(base + e) >> 1];
+            const uint32_t byte = (p.dense || bits != 4) ? 0u : p.codes[(base + e) >> 1];
+            const uint32_t c0 = bits == 4 ? (byte & 15u) : (p.dense ? 0u : read_code(p.codes, base + e, bits));
             const int bA = e / bucket;
             const double e0 = p.dense ? p.dense[base + e]
-                                      : __dadd_rn(__dmul_rn(static_cast<double>(byte & 15u), s_lvl[bA]), s_lo[bA]);
+                                      : __dadd_rn(__dmul_rn(static_cast<double>(c0), s_lvl[bA]), s_lo[bA]);
             a[2 * j] = __dadd_rn(g0, e0);
             valid |= 1u << (2 * j);
             bad |= !isfinite(g0) || !isfinite(a[2 * j]);
@@ -204,8 +217,9 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
             }
             if (two) {
                 const int bB = (e + 1) / bucket;
+                const uint32_t c1 = bits == 4 ? (byte >> 4) : (p.dense ? 0u : read_code(p.codes, base + e + 1, bits));
                 const double e1 = p.dense ? p.dense[base + e + 1]
-                                          : __dadd_rn(__dmul_rn(static_cast<double>(byte >> 4), s_lvl[bB]), s_lo[bB]);
+                                          : __dadd_rn(__dmul_rn(static_cast<double>(c1), s_lvl[bB]), s_lo[bB]);
                 a[2 * j + 1] = __dadd_rn(g1, e1);
                 valid |= 1u << (2 * j + 1);
                 bad |= !isfinite(g1) || !isfinite(a[2 * j + 1]);
@@ -280,7 +294,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
             lo = fmin(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, off));
             hi = fmax(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, off));
         }
-        const double level = (lo == hi) ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+        const double level = (lo == hi) ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), max_code);
         if (lane == 0) p.meta[bk0 + bk] = make_double2(lo, hi);
         // Guarded reciprocal: floor((x-lo)*(1/level)+0.5) equals the exact
         // quotient's unless t lands within 7e-15 of an integer; such t take
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
                 double f = floor(t);
                 const double fr = __dsub_rn(t, f);
                 if (!fast || fr < 1e-12 || fr > 1.0 - 1e-12) f = floor(__dadd_rn(__ddiv_rn(d, level), 0.5));
-                f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+                f = f < 0.0 ? 0.0 : (f > max_code ? max_code : f);
                 c = static_cast<uint32_t>(f);
             }
             s_code[s + i] = static_cast<uint8_t>(c);
@@ -308,8 +322,22 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
     }
     __syncthreads();
 
-    // ---- P5: nibble pack (quantize.cpp:102-114) ----
-    for (int i = p.dense ? (len + 1) / 2 : tid; i < (len + 1) / 2; i += NT) {
+    // ---- P5: pack (quantize.cpp:102-114): LSB-first bit stream; the block
+    // starts on a byte boundary (block * bits % 8 == 0, checked at create) ----
+    if (!p.dense && bits != 4) {
+        const int nbytes = (len * bits + 7) / 8;
+        for (int jb = tid; jb < nbytes; jb += NT) {
+            uint32_t byte = 0;
+            const int b0 = jb * 8;
+            for (int i = b0 / bits; i < len && i * bits < b0 + 8; ++i) {
+                const int sh = i * bits - b0;  // bit position of code i relative to this byte
+                const uint32_t c = s_code[i];
+                byte |= sh >= 0 ? (c << sh) : (c >> -sh);
+            }
+            p.codes[(base * bits) / 8 + jb] = static_cast<uint8_t>(byte & 0xFFu);
+        }
+    }
+    for (int i = (p.dense || bits != 4) ? (len + 1) / 2 : tid; i < (len + 1) / 2; i += NT) {
         const uint32_t lo4 = s_code[2 * i];
         const uint32_t hi4 = (2 * i + 1 < len) ? s_code[2 * i + 1] : 0u;
         p.codes[(base >> 1) + i] = static_cast<uint8_t>(lo4 | (hi4 << 4));
