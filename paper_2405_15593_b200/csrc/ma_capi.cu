@@ -381,6 +381,8 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.dim = s.dim;
     g.nbuckets = s.nbuckets;
     g.bucket = s.bucket;
+    g.bucket_shift = 0;
+    while ((int64_t(1) << g.bucket_shift) < s.bucket) ++g.bucket_shift;
     g.k = s.per_block_k;
     g.row_stride = s.kb_stride;
     g.slot = a.slot;

@@ -34,7 +34,7 @@ constexpr int kThreads = 256;
 constexpr int kPer = kChunk / kThreads;  // 16 elements per thread (strided by 256)
 
 __device__ __forceinline__ double g_a(const GlobalArgs& p, int64_t i) {
-    const int64_t q = i / p.bucket;
+    const int64_t q = i >> p.bucket_shift;  // bucket | 4096: a power of two
     const double lo = p.meta[q].x;
     const uint32_t byte = p.codes[i >> 1];
     const double c = static_cast<double>((byte >> ((i & 1) * 4)) & 15u);
@@ -61,7 +61,12 @@ __global__ void g_hist(GlobalArgs p, int shift, int nbins, uint64_t prefix, uint
          i += int64_t(gridDim.x) * blockDim.x) {
         const uint64_t k = key_of(g_a(p, i));
         bad |= (k >> 52) >= 0x7FFu;  // inf / NaN (check_finite in topk_global)
-        if ((k & pmask) == prefix) atomicAdd(&h[(k >> shift) & uint64_t(nbins - 1)], 1u);
+        const bool in = (k & pmask) == prefix;
+        const int bin = in ? static_cast<int>((k >> shift) & uint64_t(nbins - 1)) : -1;
+        // one atomic per distinct bin per warp (keys crowd a few exponent bins)
+        const unsigned act = __activemask();
+        const unsigned peers = __match_any_sync(act, bin);
+        if (in && (__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&h[bin], __popc(peers));
     }
     if (bad && p.check_finite) atomicOr(p.flag, 1u);
     __syncthreads();
@@ -172,35 +177,67 @@ __global__ void g_requant(GlobalArgs p) {
         }
     }
     __syncthreads();
-    // buckets inside this chunk (kChunk % bucket == 0): one thread per bucket
+    // buckets inside this chunk (kChunk % bucket == 0): 8 threads per bucket
+    // reduce (lo, hi) (quant_params, quantize.cpp:15-24), one writes the grid
     const int B = static_cast<int>(p.bucket);
     double* s_lo = reinterpret_cast<double*>(s_a + kChunk);
     double* s_lv = s_lo + kChunk / 1;  // room for up to kChunk buckets
-    for (int q = threadIdx.x; q * B < n; q += kThreads) {
-        const int j0 = q * B, j1 = j0 + B < n ? j0 + B : n;
-        double lo = s_a[j0], hi = s_a[j0];
-        for (int j = j0 + 1; j < j1; ++j) {
-            const double x = s_a[j];
-            lo = x < lo ? x : lo;
-            hi = x > hi ? x : hi;
+    const int nq = (n + B - 1) / B;
+    for (int q0 = threadIdx.x / 8; q0 < ((nq + 31) / 32) * 32; q0 += kThreads / 8) {
+        const int q = q0, sub = threadIdx.x & 7;
+        double lo = 0.0, hi = 0.0;
+        bool any = false;
+        if (q < nq) {
+            const int j0 = q * B, j1 = j0 + B < n ? j0 + B : n;
+            for (int j = j0 + sub; j < j1; j += 8) {
+                const double x = s_a[j];
+                if (!any) {
+                    lo = hi = x;
+                    any = true;
+                } else {
+                    lo = x < lo ? x : lo;
+                    hi = x > hi ? x : hi;
+                }
+            }
         }
-        const int64_t qg = c0 / B + q;
-        p.meta[qg] = make_double2(lo, hi);
-        s_lo[q] = lo;
-        s_lv[q] = lo == hi ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+        for (int off = 1; off < 8; off <<= 1) {  // lanes of a bucket are 8 consecutive threads
+            const double ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
+            const double oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+            const bool oa = __shfl_xor_sync(0xFFFFFFFFu, any, off);
+            if (oa && (!any || ol < lo)) lo = ol;
+            if (oa && (!any || oh > hi)) hi = oh;
+            any = any || oa;
+        }
+        if (q < nq && sub == 0) {
+            p.meta[(c0 >> p.bucket_shift) + q] = make_double2(lo, hi);
+            s_lo[q] = lo;
+            s_lv[q] = lo == hi ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+        }
     }
     __syncthreads();
-    // codes: thread t packs bytes (2 elements each) of this chunk
+    // codes: thread t packs bytes (2 elements each); floor((x - lo) * (1/level) + 0.5)
+    // equals the IEEE quotient's unless it lands within 1e-12 of an integer,
+    // where the division decides (quantize.cpp:51-53)
     for (int jb = threadIdx.x; jb * 2 < n; jb += kThreads) {
         uint32_t byte = 0;
         for (int h = 0; h < 2; ++h) {
             const int j = jb * 2 + h;
             if (j >= n) break;
-            const int q = j / B;
+            const int q = j >> p.bucket_shift;
             const double level = s_lv[q];
             uint32_t c = 0;
             if (level != 0.0) {
-                double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(s_a[j], s_lo[q]), level), 0.5));
+                const double d = __dsub_rn(s_a[j], s_lo[q]);
+                const bool fast = level >= 0x1p-1000;
+                double f = 0.0;
+                if (fast) {
+                    const double t = __dadd_rn(__dmul_rn(d, __drcp_rn(level)), 0.5);
+                    f = floor(t);
+                    const double fr = __dsub_rn(t, f);
+                    if (fr < 1e-12 || fr > 1.0 - 1e-12) f = floor(__dadd_rn(__ddiv_rn(d, level), 0.5));
+                } else {
+                    f = floor(__dadd_rn(__ddiv_rn(d, level), 0.5));
+                }
                 f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
                 c = static_cast<uint32_t>(f);
             }

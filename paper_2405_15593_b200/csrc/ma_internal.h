@@ -75,7 +75,7 @@ struct GlobalArgs {
     unsigned int* flag;
     int64_t dim, nbuckets, bucket, k, row_stride;
     uint64_t kstar;
-    int32_t slot, g_dtype, p_dtype, v_dtype, check_finite;
+    int32_t slot, g_dtype, p_dtype, v_dtype, check_finite, bucket_shift;
     double eps, lr, scale1, scale2;
 };
 int64_t global_chunks(int64_t dim);
