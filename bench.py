@@ -271,12 +271,9 @@ def run_ours(args):
         dim_total = d
         b0, b1, e0, e1 = sharding.partition_blocks(d, hp.block, world, rank)
         stride = sharding.shard_stride(d, hp.block, world)
-    else:  # weak scaling: rank r owns blocks [r nb, (r+1) nb) of a world x d vector
-        if d % hp.block:
-            raise SystemExit("--mode shard needs a whole-block workload")
+    else:  # weak scaling: rank r owns ~1/N of the blocks of a world x d vector
         dim_total = d * world
-        nb = d // hp.block
-        b0, b1, e0, e1 = rank * nb, (rank + 1) * nb, rank * d, (rank + 1) * d
+        b0, b1, e0, e1 = sharding.partition_blocks(dim_total, hp.block, world, rank)
     n = e1 - e0
     eng = ma.MicroAdam(dim_total, hp, param_dtype=pdt, grad_dtype=gdt, value_dtype=vdt,
                        block_range=(0, -1) if sparse else (b0, b1), device=local)
