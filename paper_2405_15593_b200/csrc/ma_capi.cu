@@ -314,8 +314,8 @@ cudaError_t launch(ma_handle* h, ma::StepArgs& a, int64_t nblocks, cudaStream_t 
     if (nfull > 0) {
         a.block_count = nfull;
         const int64_t grid = std::min<int64_t>(nfull, h->persist_grid);
-        cudaError_t e = h->warp ? ma::launch_step_warp(a, st)
-                                : ma::launch_step_fast(a, h->variant, int(grid), st);
+        cudaError_t e = (h->warp && ma::warp_can_run(a)) ? ma::launch_step_warp(a, st)
+                                                        : ma::launch_step_fast(a, h->variant, int(grid), st);
         if (e != cudaSuccess) return e;
     }
     if (tail_partial) {

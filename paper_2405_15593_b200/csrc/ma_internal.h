@@ -114,6 +114,8 @@ bool warp_path_ok(int block, int bucket, int kb, int m, int kb_stride, int g_dty
                   int v_dtype);
 size_t warp_smem_bytes(int bucket);
 cudaError_t launch_step_warp(const StepArgs& a, cudaStream_t s);
+// Whether the warp kernels run this step (the exact one needs k_b <= 64).
+bool warp_can_run(const StepArgs& a);
 // Lean kernel split for sparse parameter propagation (ph 1 = front, 2 = stats).
 bool lean_phase_ok(const StepArgs& a);
 cudaError_t launch_step_lean_phase(const StepArgs& a, int ph, cudaStream_t s);

@@ -68,6 +68,7 @@ __device__ __forceinline__ void prefetch_l2_keep(const void* p, uint32_t bytes) 
 struct WLayout {
     uint32_t ll, sel, wpref, dup, cval, cidx, misc, total;
     __host__ __device__ WLayout() {}
+    __host__ __device__ WLayout(int bucket, int /*capl*/) : WLayout(bucket) {}
     __host__ __device__ explicit WLayout(int bucket) {
         size_t o = 0;
         ll = uint32_t(o);    o = align_up(o + size_t(kBlk / bucket) * 16, 16);  // (lo, level)
@@ -81,9 +82,10 @@ struct WLayout {
     }
 };
 
-template <int LPB_, int GDT_, int PDT_, int VDT_, bool REP_>
+template <int LPB_, int GDT_, int PDT_, int VDT_, bool REP_, int CAPL_ = 4>
 struct KW {
     static constexpr int LPB = LPB_, GDT = GDT_, PDT = PDT_, VDT = VDT_;
+    static constexpr int CAPL = CAPL_;  // lean kernel: exact-stage candidate slots per lane
     static constexpr int BUCKET = 8 * LPB_;
     static constexpr bool REPORT = REP_;
 };
@@ -205,7 +207,8 @@ __device__ __noinline__ uint32_t exact_code_w(double x, double lo, double level)
 template <class KT, class LAY>
 __device__ __noinline__ int slow_select(const StepArgs* pp, unsigned char* ws, int64_t b) {
     const StepArgs& p = *pp;
-    const LAY L(KT::BUCKET);
+    constexpr int kCapS = 32 * KT::CAPL;
+    const LAY L(KT::BUCKET, KT::CAPL);
     const int lane = threadIdx.x & 31;
     const int64_t base = b * kBlk;
     const double2* s_ll = reinterpret_cast<const double2*>(ws + L.ll);
@@ -268,11 +271,11 @@ __device__ __noinline__ int slow_select(const StepArgs* pp, unsigned char* ws, i
         prefix |= static_cast<uint64_t>(d) << sh;
         pmask |= uint64_t(127) << sh;
         __syncwarp();
-        if (above_total + binc <= kCap || sh == 0) break;
+        if (above_total + binc <= kCapS || sh == 0) break;
     }
     double* s_cval = reinterpret_cast<double*>(ws + L.cval);
     int16_t* s_cidx = reinterpret_cast<int16_t*>(ws + L.cidx);
-    if (above_total + binc <= kCap) {
+    if (above_total + binc <= kCapS) {
         // gather every key >= prefix (numeric) — exactly above_total + binc keys
         if (lane == 0) s_misc[2] = 0;
         __syncwarp();
@@ -334,7 +337,7 @@ template <class KT, class LAY>
 __device__ __noinline__ double dup_stats(const StepArgs* pp, unsigned char* ws, int64_t b, int ndup,
                                          int nent) {
     const StepArgs& p = *pp;
-    const LAY L(KT::BUCKET);
+    const LAY L(KT::BUCKET, KT::CAPL);
     const int lane = threadIdx.x & 31;
     const int kb = p.per_block_k, kbs = p.kb_stride, filled = p.filled;
     constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
@@ -890,13 +893,15 @@ constexpr int kLTarget = MA_LEAN_TARGET;
 struct LLayout {
     uint32_t ll, llf, sel, wpref, dup, cval, cidx, misc, total;
     __host__ __device__ LLayout() {}
-    __host__ __device__ explicit LLayout(int bucket) {
+    __host__ __device__ explicit LLayout(int bucket, int capl = kLCapL) {
         const size_t nbk = size_t(kBlk / bucket);
+        const size_t kLCap = size_t(32 * capl);
         size_t o = 0;
         ll = uint32_t(o);    o = align_up(o + nbk * 16, 16);     // exact (lo, level), fp64
         llf = uint32_t(o);   o = align_up(o + nbk * 16, 16);     // (lo32, level32, E_q, Tf_q)
         sel = uint32_t(o);   o = align_up(o + kBlk / 8, 16);
-        wpref = uint32_t(o); o = align_up(o + kBlk / 8, 16);    // member list; word prefix; seen bits
+        wpref = uint32_t(o);  // member list (int16 per candidate); word prefix; seen bits
+        o = align_up(o + (kLCap * 2 > size_t(kBlk / 8) ? kLCap * 2 : size_t(kBlk / 8)), 16);
         dup = uint32_t(o);   o = align_up(o + kBlk / 8, 16);
         cval = uint32_t(o);  // candidates; radix histogram; bucket (lo, hi) keys; duplicate list
         o = align_up(o + (size_t(kLCap) * 8 > nbk * 16 ? size_t(kLCap) * 8 : nbk * 16), 16);
@@ -1030,7 +1035,7 @@ struct UniqueUpd {
 template <class KT>
 __device__ __noinline__ bool dup_chunks(const StepArgs* pp, unsigned char* ws, int64_t b, int ndup) {
     const StepArgs& p = *pp;
-    const LLayout L(KT::BUCKET);
+    const LLayout L(KT::BUCKET, KT::CAPL);
     constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
     const int lane = threadIdx.x & 31;
     const int kbs = p.kb_stride;
@@ -1039,7 +1044,7 @@ __device__ __noinline__ bool dup_chunks(const StepArgs* pp, unsigned char* ws, i
     const unsigned char* gwv = static_cast<const unsigned char*>(p.win_val) + went * vsz;
     const uint32_t* s_dup = reinterpret_cast<const uint32_t*>(ws + L.dup);
     const int* dupl = reinterpret_cast<const int*>(ws + L.cval);
-    if (ndup > kDupCap) return false;
+    if (ndup > static_cast<int>((L.cidx - L.cval) / 4)) return false;  // the list overflowed
     uint32_t dv[4];
     int loc = 0;
 #pragma unroll
@@ -1049,66 +1054,74 @@ __device__ __noinline__ bool dup_chunks(const StepArgs* pp, unsigned char* ws, i
     }
     int ndupc;
     int run = warp_excl_scan(loc, lane, ndupc);
-    if (ndupc > 64) return false;
     int* s_dpref = reinterpret_cast<int*>(ws + L.wpref);  // the claim bits of dup_stats are not needed
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         s_dpref[lane * 4 + k] = run;
         run += __popc(dv[k]);
     }
-    double2* zz = reinterpret_cast<double2*>(ws + L.llf);  // pass-2 tables are dead
-    int16_t* zc = reinterpret_cast<int16_t*>(ws + L.ll);
-    for (int i = lane; i < ndupc; i += 32) zz[i] = make_double2(0.0, 0.0);
+    // running sums of up to zcap coordinates at a time (pass-2 tables are dead)
+    double2* zz = reinterpret_cast<double2*>(ws + L.ll);
+    int16_t* zc = reinterpret_cast<int16_t*>(ws + L.cidx);
+    const int zcap = min(static_cast<int>((L.cval - L.ll) / 16), static_cast<int>((L.misc - L.cidx) / 2));
     __syncwarp();
-    for (int c0 = 0; c0 < ndup; c0 += 32) {
-        const bool has = c0 + lane < ndup;
-        const int x = has ? dupl[c0 + lane] : 0;
-        const int idx = x >> 16, r = (x >> 8) & 0xFF, pos = x & 0xFF;
-        double t1 = 0.0, t2 = 0.0;
-        int id = 0;
-        if (has) {
-            const double v = ld_t<KT::VDT>(gwv, r * kbs + pos);
-            t1 = __dmul_rn(p.w1[r], v);
-            t2 = __dmul_rn(p.w2[r], __dmul_rn(v, v));
-            id = s_dpref[idx >> 5] + __popc(s_dup[idx >> 5] & ((1u << (idx & 31)) - 1u));
-        }
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, has ? idx : -1 - lane);
-        const int cnt = has ? __popc(peers) : 0;
-        const int maxc = __reduce_max_sync(0xFFFFFFFFu, cnt);
-        const bool leader = has && (__ffs(peers) - 1) == lane;
-        double z1 = 0.0, z2 = 0.0;
-        if (leader) {
-            const double2 zc0 = zz[id];
-            z1 = zc0.x;
-            z2 = zc0.y;
-        }
-        uint32_t rem = peers;
-        for (int k = 0; k < maxc; ++k) {
-            const int src = rem ? __ffs(rem) - 1 : lane;
-            rem &= rem - 1;
-            const double a1 = __shfl_sync(0xFFFFFFFFu, t1, src);
-            const double a2 = __shfl_sync(0xFFFFFFFFu, t2, src);
-            if (k < cnt) {
-                z1 = __dadd_rn(z1, a1);
-                z2 = __dadd_rn(z2, a2);
+    for (int id0 = 0; id0 < ndupc; id0 += zcap) {
+        const int nz = min(zcap, ndupc - id0);
+        for (int i = lane; i < nz; i += 32) zz[i] = make_double2(0.0, 0.0);
+        __syncwarp();
+        for (int c0 = 0; c0 < ndup; c0 += 32) {
+            bool has = c0 + lane < ndup;
+            const int x = has ? dupl[c0 + lane] : 0;
+            const int idx = x >> 16, r = (x >> 8) & 0xFF, pos = x & 0xFF;
+            int id = 0;
+            if (has) {
+                id = s_dpref[idx >> 5] + __popc(s_dup[idx >> 5] & ((1u << (idx & 31)) - 1u)) - id0;
+                has = id >= 0 && id < nz;
             }
+            double t1 = 0.0, t2 = 0.0;
+            if (has) {
+                const double v = ld_t<KT::VDT>(gwv, r * kbs + pos);
+                t1 = __dmul_rn(p.w1[r], v);
+                t2 = __dmul_rn(p.w2[r], __dmul_rn(v, v));
+            }
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, has ? idx : -1 - lane);
+            const int cnt = has ? __popc(peers) : 0;
+            const int maxc = __reduce_max_sync(0xFFFFFFFFu, cnt);
+            const bool leader = has && (__ffs(peers) - 1) == lane;
+            double z1 = 0.0, z2 = 0.0;
+            if (leader) {
+                const double2 zc0 = zz[id];
+                z1 = zc0.x;
+                z2 = zc0.y;
+            }
+            uint32_t rem = peers;
+            for (int k = 0; k < maxc; ++k) {
+                const int src = rem ? __ffs(rem) - 1 : lane;
+                rem &= rem - 1;
+                const double a1 = __shfl_sync(0xFFFFFFFFu, t1, src);
+                const double a2 = __shfl_sync(0xFFFFFFFFu, t2, src);
+                if (k < cnt) {
+                    z1 = __dadd_rn(z1, a1);
+                    z2 = __dadd_rn(z2, a2);
+                }
+            }
+            if (leader) {
+                zz[id] = make_double2(z1, z2);
+                zc[id] = static_cast<int16_t>(idx);
+            }
+            __syncwarp();
         }
-        if (leader) {
-            zz[id] = make_double2(z1, z2);
-            zc[id] = static_cast<int16_t>(idx);
+        for (int i = lane; i < nz; i += 32) {
+            const int idx = zc[i];
+            const double2 z = zz[i];
+            const double mhat = __dmul_rn(z.x, p.scale1);
+            const double vhat = __dmul_rn(z.y, p.scale2);
+            const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+            const double th = ld_t<KT::PDT>(p.params, base + idx);
+            st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
         }
         __syncwarp();
     }
-    for (int i = lane; i < ndupc; i += 32) {
-        const int idx = zc[i];
-        const double2 z = zz[i];
-        const double mhat = __dmul_rn(z.x, p.scale1);
-        const double vhat = __dmul_rn(z.y, p.scale2);
-        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
-        const double th = ld_t<KT::PDT>(p.params, base + idx);
-        st_t<KT::PDT>(p.params, base + idx, __dsub_rn(th, __dmul_rn(p.lr, u)));
-    }
-    __syncwarp();
     return true;
 }
 
@@ -1147,7 +1160,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
 #endif
     const int64_t b = p.block_offset + bl;
     const int64_t base = b * kBlk;
-    const LLayout L(BUCKET);
+    const LLayout L(BUCKET, KT::CAPL);
     unsigned char* ws = smem + warp * L.total;
     double2* s_ll = reinterpret_cast<double2*>(ws + L.ll);
     float4* s_llf = reinterpret_cast<float4*>(ws + L.llf);
@@ -1244,7 +1257,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     // values sit in s_cval / s_cidx; floor16: every key16 >= floor16 is a candidate.
     int ncand = -1;
     uint32_t base16 = T, floor16 = T;
-    if (T != 0 && cnt > kLCap && cnt <= kRefineMax) {
+    if (T != 0 && cnt > (32 * KT::CAPL) && cnt <= kRefineMax) {
         // Overfull screen: refine from the hit mask (key16 histogram of the
         // exact hits at or above T) instead of re-reading the block.
         uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.cval);
@@ -1266,7 +1279,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         if (ok) {
             const int d = 31 - __clz(ok);
             const int n = __shfl_sync(0xFFFFFFFFu, sfx, d);
-            if (n <= kLCap) {
+            if (n <= (32 * KT::CAPL)) {
                 const uint32_t T1 = T + static_cast<uint32_t>(d);
                 if (lane == 0) s_misc[4] = 0;
                 __syncwarp();
@@ -1284,7 +1297,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             }
         }
         if (p.dbg && lane == 0) atomicAdd(p.dbg + 6, 1u);
-    } else if (T != 0 && cnt >= kb && cnt <= kLCap) {
+    } else if (T != 0 && cnt >= kb && cnt <= (32 * KT::CAPL)) {
         int total;
         int pos = warp_excl_scan(nmine, lane, total);
         for_hits([&](int e) {
@@ -1296,10 +1309,10 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         __syncwarp();
     }
     // 31-bit high words of the candidates' |a| keys (bits 62..32), 0 = empty slot
-    uint32_t kh[kLCapL];
+    uint32_t kh[KT::CAPL];
     auto load_keys = [&]() {
 #pragma unroll
-        for (int s = 0; s < kLCapL; ++s) {
+        for (int s = 0; s < KT::CAPL; ++s) {
             const int q = lane + 32 * s;
             kh[s] = q < ncand ? hi_key(s_cval[q]) : 0u;
         }
@@ -1307,7 +1320,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     auto count_ge = [&](uint32_t v) {
         int c = 0;
 #pragma unroll
-        for (int s = 0; s < kLCapL; ++s) c += kh[s] >= v;
+        for (int s = 0; s < KT::CAPL; ++s) c += kh[s] >= v;
         return __reduce_add_sync(0xFFFFFFFFu, c);
     };
     load_keys();
@@ -1316,7 +1329,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         ncand = slow_select<KT, LLayout>(&p, ws, b);
         if (p.dbg && lane == 0) {
             atomicAdd(p.dbg + 2, 1u);
-            if (cnt > kLCap) atomicAdd(p.dbg + 3, 1u);
+            if (cnt > (32 * KT::CAPL)) atomicAdd(p.dbg + 3, 1u);
         }
         if (ncand >= 0) {
             const uint32_t ph = static_cast<uint32_t>(s_misc[0]);  // prefix bits 62..32
@@ -1331,7 +1344,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     if (ncand >= 0) {
         uint32_t kml = 0;
 #pragma unroll
-        for (int s = 0; s < kLCapL; ++s) kml = max(kml, kh[s]);
+        for (int s = 0; s < KT::CAPL; ++s) kml = max(kml, kh[s]);
         const uint32_t kmax = __reduce_max_sync(0xFFFFFFFFu, kml);
         if (p.check_finite && kmax >= 0x7FF00000u && lane == 0) atomicOr(p.flag, 1u);  // inf/NaN in g or a
         // Bisection for a high word lo with count(lo) >= kb > count(hi), stopping
@@ -1348,7 +1361,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             }
         }
 #pragma unroll
-        for (int s = 0; s < kLCapL; ++s)
+        for (int s = 0; s < KT::CAPL; ++s)
             if (kh[s] > lo || (clo == kb && kh[s] == lo)) selc |= 1u << s;
         if (clo != kb) {
             // lo is the k_b-th high word and ties on it: rank the tied keys on the
@@ -1356,7 +1369,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             const int need = kb - count_ge(lo + 1);
             int nm = 0;
 #pragma unroll
-            for (int s = 0; s < kLCapL; ++s) {
+            for (int s = 0; s < KT::CAPL; ++s) {
                 const bool mem = kh[s] == lo && lane + 32 * s < ncand;
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mem);
                 if (mem) s_memb[nm + __popc(bal & lanemask_lt())] = static_cast<int16_t>(lane + 32 * s);
@@ -1364,7 +1377,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             }
             __syncwarp();
 #pragma unroll
-            for (int s = 0; s < kLCapL; ++s) {
+            for (int s = 0; s < KT::CAPL; ++s) {
                 const int q = lane + 32 * s;
                 if (kh[s] == lo && q < ncand) {
                     const uint64_t kq = key_of(s_cval[q]);
@@ -1382,7 +1395,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             if (p.dbg && lane == 0) atomicAdd(p.dbg + 7, 1u);
         }
 #pragma unroll
-        for (int s = 0; s < kLCapL; ++s)
+        for (int s = 0; s < KT::CAPL; ++s)
             if ((selc >> s) & 1u) {
                 const int e = s_cidx[lane + 32 * s];
                 atomicOr(&s_sel[e >> 5], 1u << (e & 31));
@@ -1390,8 +1403,9 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
         // next threshold (the exact kernel's rule): the largest key16 t in
         // [floor16, lo16] whose candidate count reaches `want`
         const int planned = T ? static_cast<int>(tstate >> 16) : 0;
-        int want = planned ? (kLTarget * planned) / max(cnt, 1) : kLTarget;
-        want = min(max(want, kb + (kb >> 2)), kLCap - (kLCap >> 2));
+        const int target = max(kLTarget, kb + (kb >> 1));
+        int want = planned ? (target * planned) / max(cnt, 1) : target;
+        want = min(max(want, kb + (kb >> 2)), (32 * KT::CAPL) - ((32 * KT::CAPL) >> 2));
         const uint32_t lo16 = lo >> 16;
         const uint32_t fl = min(floor16, lo16);
         uint32_t t;
@@ -1448,7 +1462,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     const int64_t row0 = static_cast<int64_t>(slot) * kbs;
     if (ncand >= 0) {
 #pragma unroll
-        for (int s = 0; s < kLCapL; ++s)
+        for (int s = 0; s < KT::CAPL; ++s)
             if ((selc >> s) & 1u) {
                 const int q = lane + 32 * s;
                 const int e = s_cidx[q];
@@ -1642,7 +1656,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
                 if (mine[k]) u[k].load(p, base, gwv, e[k], idx[k]);
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
                 const int qd = ndup + __popc(bal & lanemask_lt());
-                if (dup && qd < kDupCap) dupl[qd] = (idx[k] << 16) | (rr[k] << 8) | ps[k];
+                if (dup && qd < static_cast<int>((L.cidx - L.cval) / 4)) dupl[qd] = (idx[k] << 16) | (rr[k] << 8) | ps[k];
                 ndup += __popc(bal);
             }
 #pragma unroll
@@ -1653,7 +1667,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     __syncwarp();
     if (p.dbg && lane == 0) {
         atomicAdd(p.dbg + 5, static_cast<unsigned>(ndup));
-        if (ndup > kDupCap) atomicAdd(p.dbg + 4, 1u);
+        if (ndup > static_cast<int>((L.cidx - L.cval) / 4)) atomicAdd(p.dbg + 4, 1u);
     }
 #if MA_LEAN_PROF
     if (p.dbg) prof_mark(p, 7);
@@ -1704,7 +1718,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
 
 template <class KT, int PH = 3>
 cudaError_t launch_kl(const StepArgs& a, cudaStream_t s) {
-    const size_t smem = size_t(kWarps) * LLayout(KT::BUCKET).total;
+    const size_t smem = size_t(kWarps) * LLayout(KT::BUCKET, KT::CAPL).total;
     auto k = microadam_step_lean<KT, PH>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem));
@@ -1721,11 +1735,17 @@ cudaError_t launch_kl(const StepArgs& a, cudaStream_t s) {
     X(BF16, F32, BF16)    \
     X(BF16, BF16, F32)
 
+// k_b <= 64: 4 candidate slots per lane; up to 256 (densities to 6.25%): 16.
+constexpr int kWideKb = 32 * 16 / 2;
+
 template <int LPB>
 cudaError_t launch_ldt(const StepArgs& a, cudaStream_t s) {
+    const bool wide = a.per_block_k > kCap / 2;
     switch (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype)) {
-#define MA_CASE(G_, P_, V_) \
-        case dtype_key_w(G_, P_, V_): return launch_kl<KW<LPB, G_, P_, V_, false>>(a, s);
+#define MA_CASE(G_, P_, V_)                                                              \
+        case dtype_key_w(G_, P_, V_):                                                    \
+            return wide ? launch_kl<KW<LPB, G_, P_, V_, false, 16>>(a, s)                \
+                        : launch_kl<KW<LPB, G_, P_, V_, false>>(a, s);
         MA_LEAN_DTYPES(MA_CASE)
 #undef MA_CASE
         default: return cudaErrorInvalidConfiguration;
@@ -1734,6 +1754,7 @@ cudaError_t launch_ldt(const StepArgs& a, cudaStream_t s) {
 
 bool lean_ok(const StepArgs& a) {
     if (a.partials || a.force_exact || (a.bucket != 32 && a.bucket != 64)) return false;
+    if (a.per_block_k > kWideKb) return false;
     switch (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype)) {
 #define MA_CASE(G_, P_, V_) case dtype_key_w(G_, P_, V_): return true;
         MA_LEAN_DTYPES(MA_CASE)
@@ -1769,7 +1790,7 @@ cudaError_t launch_wrep(const StepArgs& a, cudaStream_t s) {
 // Warp path: B_d = 4096, k_b <= 64 (candidates fit kCap), B_q in {16, 32, 64},
 // an instantiated dtype combo; window rows addressable with 16-bit offsets.
 bool warp_path_ok(int block, int bucket, int kb, int m, int kb_stride, int g, int p, int v) {
-    if (block != kBlk || kb < 1 || kb > kCap / 2) return false;
+    if (block != kBlk || kb < 1 || kb > kWideKb) return false;  // k_b > 64: lean kernel only
     if (bucket != 16 && bucket != 32 && bucket != 64) return false;
     if (m < 1 || m > kMaxWindow || m * kb_stride > 32768) return false;
     switch (dtype_key_w(g, p, v)) {
@@ -1783,7 +1804,7 @@ bool warp_path_ok(int block, int bucket, int kb, int m, int kb_stride, int g, in
 size_t warp_smem_bytes(int bucket) { return size_t(kWarps) * WLayout(bucket).total; }
 
 // Sparse-propagation phases of the lean kernel (B_q = 64): ph = 1 front, 2 stats.
-bool lean_phase_ok(const StepArgs& a) { return lean_ok(a) && a.bucket == 64; }
+bool lean_phase_ok(const StepArgs& a) { return lean_ok(a) && a.bucket == 64 && a.per_block_k <= kCap / 2; }
 
 cudaError_t launch_step_lean_phase(const StepArgs& a, int ph, cudaStream_t s) {
     if (a.block_count <= 0) return cudaSuccess;
@@ -1799,8 +1820,11 @@ cudaError_t launch_step_lean_phase(const StepArgs& a, int ph, cudaStream_t s) {
     }
 }
 
+bool warp_can_run(const StepArgs& a) { return lean_ok(a) || a.per_block_k <= kCap / 2; }
+
 cudaError_t launch_step_warp(const StepArgs& a, cudaStream_t s) {
     if (a.block_count <= 0) return cudaSuccess;
+    if (!warp_can_run(a)) return cudaErrorInvalidConfiguration;
     if ((a.block_count + kWarps - 1) / kWarps > 0x7FFFFFFFll) return cudaErrorInvalidConfiguration;
     if (lean_ok(a)) return a.bucket == 64 ? launch_ldt<8>(a, s) : launch_ldt<4>(a, s);
     return a.partials ? launch_wrep<true>(a, s) : launch_wrep<false>(a, s);
