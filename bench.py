@@ -2,7 +2,8 @@
 """Benchmark of the B200 MicroAdam optimizer step (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload llama2-7b|opt-1.3b|bert-110m|1m]
+                    [--workload llama2-7b|llama2-13b|opt-1.3b|bert-110m|1m]
+                    [--density D] [--window M] [--mode shard|allgather|sparse]
 
 A "step" is one MicroAdamOptimizer::step (optim.cpp:164-190) over the whole
 workload vector: EF decode + accumulate, block Top-K, 4-bit re-quantization,
@@ -47,6 +48,8 @@ UNIT = "params/s"
 WORKLOADS = {
     "llama2-7b": dict(dim=6_738_415_616, dtype="bf16",
                       desc="Llama-2-7B-sized flat vector (BASELINE configs[3])"),
+    "llama2-13b": dict(dim=13_015_864_320, dtype="bf16",
+                       desc="Llama-2-13B-sized flat vector (configs[4]; density / window sweep)"),
     "opt-1.3b": dict(dim=1_300_000_000, dtype="bf16", desc="OPT-1.3B-sized flat vector (configs[2])"),
     "bert-110m": dict(dim=110_000_000, dtype="f32", desc="BERT-base-sized flat vector (configs[1])"),
     "1m": dict(dim=1_000_000, dtype="f32", desc="synthetic 1M vector (configs[0])"),
