@@ -5,6 +5,8 @@
 // pow() weights (window.cpp:37,43 — computed here, on the host, exactly as the
 // reference does) and kernel launches. No exception crosses the ABI.
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -200,7 +202,15 @@ struct ma_handle {
     // host path (ma_step_host)
     void* d_theta = nullptr;
     void* d_gstage = nullptr;
+    // ma_step_host sparse θ return: window-entry θ values gathered on device,
+    // brought back with the ring indices (pinned), scattered by host threads
+    void* d_gath = nullptr;
+    int16_t* h_ring_idx = nullptr;
+    void* h_gath = nullptr;
     bool theta_valid = false;
+    // host buffer known to equal the device θ (the last ma_step_host output);
+    // the sparse θ return is only valid into that buffer
+    const void* host_synced = nullptr;
     cudaStream_t host_stream = nullptr;
     cudaStream_t last_stream = nullptr;
     int64_t launches = 0;
@@ -237,6 +247,9 @@ void free_handle(ma_handle* h) {
     cudaFree(h->d_dbg);
     cudaFree(h->d_theta);
     cudaFree(h->d_gstage);
+    cudaFree(h->d_gath);
+    if (h->h_ring_idx) cudaFreeHost(h->h_ring_idx);
+    if (h->h_gath) cudaFreeHost(h->h_gath);
     cudaFree(h->g_level);
     cudaFree(h->g_selbits);
     cudaFree(h->g_hist);
@@ -641,6 +654,7 @@ ma_status ma_set_params(ma_handle* h, const void* h_params) {
     if (!h->d_theta) MA_CUDA(cudaMalloc(&h->d_theta, pbytes));
     MA_CUDA(cudaMemcpy(h->d_theta, h_params, pbytes, cudaMemcpyHostToDevice));
     h->theta_valid = true;
+    h->host_synced = h_params;
     return MA_OK;
 }
 
@@ -664,10 +678,16 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
         if (r != MA_OK) return r;
         MA_CUDA(cudaMemcpyAsync(h_params, h->d_theta, size_t(s.dim) * psz, cudaMemcpyDeviceToHost, st));
         MA_CUDA(cudaStreamSynchronize(st));
+        h->host_synced = h_params;
         return ma_sync(h);
     }
     // Chunked pipeline: H2D grads of chunk c+1 overlaps the step of chunk c
-    // and the D2H of θ for chunk c-1 (two copy engines + SMs busy at once).
+    // and the return of θ for chunk c-1 (two copy engines + SMs busy at once).
+    // θ changes only at window coordinates (optim.cpp:183-187: u = 0 off the
+    // window), so unless MA_HOST_DENSE=1 the return is sparse: the window ring
+    // indices and the θ values gathered at them (4 bytes per window entry
+    // against 2 per parameter for bf16 θ), scattered into h_params by host
+    // threads as each chunk lands.
     ma::StepArgs a;
     base_args(h, &a);
     a.grads = h->d_gstage;
@@ -676,16 +696,29 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
     a.lr32 = static_cast<float>(lr);
     push_and_weights(h, &a);
     const int64_t nb = s.b1 - s.b0;
+    const int64_t m = h->cfg.hp.window, kbs = s.kb_stride;
+    const char* dense_env = std::getenv("MA_HOST_DENSE");
+    const bool sparse_ret =
+        !s.global && h->host_synced == h_params && !(dense_env && dense_env[0] == '1');
+    const size_t ring_n = size_t(nb) * size_t(m) * size_t(kbs);
+    if (sparse_ret && !h->d_gath) {
+        MA_CUDA(cudaMalloc(&h->d_gath, ring_n * psz));
+        MA_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->h_ring_idx), ring_n * sizeof(int16_t)));
+        MA_CUDA(cudaMallocHost(&h->h_gath, ring_n * psz));
+    }
     const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(64) << 20) / (s.block * int64_t(gsz)));
     const int64_t nchunks = (nb + chunk_blocks - 1) / chunk_blocks;
-    std::vector<cudaEvent_t> up(static_cast<size_t>(nchunks)), done(static_cast<size_t>(nchunks));
+    std::vector<cudaEvent_t> up(static_cast<size_t>(nchunks)), done(static_cast<size_t>(nchunks)),
+        back(static_cast<size_t>(nchunks));
     static thread_local cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     if (!s_h2d) MA_CUDA(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
     if (!s_d2h) MA_CUDA(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
     for (int64_t c = 0; c < nchunks; ++c) {
         MA_CUDA(cudaEventCreateWithFlags(&up[size_t(c)], cudaEventDisableTiming));
         MA_CUDA(cudaEventCreateWithFlags(&done[size_t(c)], cudaEventDisableTiming));
+        MA_CUDA(cudaEventCreateWithFlags(&back[size_t(c)], cudaEventDisableTiming));
     }
+    const int filled = static_cast<int>(h->filled);
     for (int64_t c = 0; c < nchunks; ++c) {
         const int64_t cb0 = c * chunk_blocks, cb1 = std::min(nb, cb0 + chunk_blocks);
         const int64_t e0 = cb0 * s.block, e1 = std::min(s.dim, cb1 * s.block);
@@ -697,19 +730,78 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
         a.block_offset = cb0;
         MA_CUDA(launch(h, a, cb1 - cb0, st));
         ++h->launches;
+        if (sparse_ret) {
+            MA_CUDA(ma::launch_gather_window_theta(h->d_win_idx, h->d_theta, h->cfg.param_dtype, h->d_gath, cb0, cb1,
+                                                   int(m), int(kbs), int(s.per_block_k), filled, s.block, s.dim, st));
+            ++h->launches;
+        }
         MA_CUDA(cudaEventRecord(done[size_t(c)], st));
         MA_CUDA(cudaStreamWaitEvent(s_d2h, done[size_t(c)], 0));
-        MA_CUDA(cudaMemcpyAsync(static_cast<char*>(h_params) + e0 * psz,
-                                static_cast<const char*>(h->d_theta) + e0 * psz,
-                                size_t(e1 - e0) * psz, cudaMemcpyDeviceToHost, s_d2h));
+        if (sparse_ret) {
+            const size_t q0 = size_t(cb0) * size_t(m * kbs), qn = size_t(cb1 - cb0) * size_t(m * kbs);
+            MA_CUDA(cudaMemcpyAsync(h->h_ring_idx + q0, h->d_win_idx + q0, qn * sizeof(int16_t),
+                                    cudaMemcpyDeviceToHost, s_d2h));
+            MA_CUDA(cudaMemcpyAsync(static_cast<char*>(h->h_gath) + q0 * psz,
+                                    static_cast<const char*>(h->d_gath) + q0 * psz, qn * psz,
+                                    cudaMemcpyDeviceToHost, s_d2h));
+        } else {
+            MA_CUDA(cudaMemcpyAsync(static_cast<char*>(h_params) + e0 * psz,
+                                    static_cast<const char*>(h->d_theta) + e0 * psz,
+                                    size_t(e1 - e0) * psz, cudaMemcpyDeviceToHost, s_d2h));
+        }
+        MA_CUDA(cudaEventRecord(back[size_t(c)], s_d2h));
+    }
+    if (sparse_ret) {
+        // host scatter: h_params[block base + idx] = θ for every live window entry
+        std::atomic<int64_t> next{0};
+        std::atomic<int> err{0};
+        const int nthreads = static_cast<int>(std::max<unsigned>(1, std::min<unsigned>(32, std::thread::hardware_concurrency())));
+        auto worker = [&]() {
+            for (;;) {
+                const int64_t c = next.fetch_add(1);
+                if (c >= nchunks) return;
+                if (cudaEventSynchronize(back[size_t(c)]) != cudaSuccess) {
+                    err = 1;
+                    return;
+                }
+                const int64_t cb0 = c * chunk_blocks, cb1 = std::min(nb, cb0 + chunk_blocks);
+                for (int64_t b = cb0; b < cb1; ++b) {
+                    const int64_t base = b * s.block;
+                    const int64_t len = std::min(s.block, s.dim - base);
+                    const int64_t kb = std::min(s.per_block_k, len);
+                    for (int r = 0; r < filled; ++r) {
+                        const size_t q = size_t((b * m + r) * kbs);
+                        const int16_t* ix = h->h_ring_idx + q;
+                        const unsigned char* vv = static_cast<const unsigned char*>(h->h_gath) + q * psz;
+                        unsigned char* hp = static_cast<unsigned char*>(h_params) + size_t(base) * psz;
+                        if (psz == 2) {
+                            for (int64_t j = 0; j < kb; ++j)
+                                reinterpret_cast<uint16_t*>(hp)[ix[j]] = reinterpret_cast<const uint16_t*>(vv)[j];
+                        } else if (psz == 4) {
+                            for (int64_t j = 0; j < kb; ++j)
+                                reinterpret_cast<uint32_t*>(hp)[ix[j]] = reinterpret_cast<const uint32_t*>(vv)[j];
+                        } else {
+                            for (int64_t j = 0; j < kb; ++j)
+                                reinterpret_cast<uint64_t*>(hp)[ix[j]] = reinterpret_cast<const uint64_t*>(vv)[j];
+                        }
+                    }
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < nthreads; ++t) pool.emplace_back(worker);
+        for (auto& t : pool) t.join();
+        if (err) return fail(MA_ERR_CUDA, "ma_step_host: sparse θ return failed");
     }
     MA_CUDA(cudaStreamSynchronize(s_d2h));
     MA_CUDA(cudaStreamSynchronize(st));
     for (int64_t c = 0; c < nchunks; ++c) {
         cudaEventDestroy(up[size_t(c)]);
         cudaEventDestroy(done[size_t(c)]);
+        cudaEventDestroy(back[size_t(c)]);
     }
     h->last_stream = st;
+    h->host_synced = h_params;
     return ma_sync(h);
 }
 
@@ -974,7 +1066,7 @@ ma_status ma_save_checkpoint(ma_handle* h, const void* params, int32_t params_on
     if (!cf.f) return fail(MA_ERR_INVALID_ARG, std::string("checkpoint: cannot open ") + path + " for writing");
     std::FILE* f = cf.f;
     const int64_t m = h->cfg.hp.window;
-    const unsigned char head8[6] = {'M', 'A', 'D', 'M', 1, h->d_dense ? 1 : 0};  // magic, version, lossless
+    const unsigned char head8[6] = {'M', 'A', 'D', 'M', 1, static_cast<unsigned char>(h->d_dense ? 1 : 0)};  // magic, version, lossless
     bool ok = put_bytes(f, head8, 6) && put_i64(f, s.dim) && put_i64(f, h->step);
     // θ (optim.hpp params()) widened to f64
     const int pdt = h->cfg.param_dtype;
@@ -1090,6 +1182,7 @@ ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_devic
                                       val.data());
         if (st != MA_OK) return st;
         if (params && !params_on_device) h->theta_valid = false;
+        h->host_synced = nullptr;
         return MA_OK;
     }
     unsigned char bits = 0;
@@ -1111,6 +1204,7 @@ ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_devic
                                   val.data());
     if (st != MA_OK) return st;
     if (params && !params_on_device) h->theta_valid = false;  // ma_step_host re-uploads θ
+    h->host_synced = nullptr;
     return MA_OK;
 }
 

@@ -123,6 +123,9 @@ cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int
                                cudaStream_t s);
 cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double* out5,
                                  cudaStream_t s);
+cudaError_t launch_gather_window_theta(const int16_t* win_idx, const void* theta, int pdt, void* out, int64_t b0,
+                                      int64_t b1, int m, int kbs, int kb, int filled, int64_t block, int64_t dim,
+                                      cudaStream_t s);
 cudaError_t launch_fill_synthetic(void* out, int dtype, int64_t n, uint64_t seed, uint64_t step,
                                   int64_t offset, int levels, cudaStream_t s);
 

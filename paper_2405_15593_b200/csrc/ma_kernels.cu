@@ -415,6 +415,30 @@ __global__ void report_reduce_kernel(const double* partials, int64_t nblocks, do
     }
 }
 
+// θ at every live window entry of blocks [b0, b1), same [block][m][kb_stride]
+// layout as the ring (ma_step_host's sparse D2H: θ changes only there).
+__global__ void gather_window_theta_kernel(const int16_t* win_idx, const void* theta, int pdt, void* out,
+                                           int64_t b0, int64_t b1, int m, int kbs, int kb, int filled,
+                                           int64_t block, int64_t dim) {
+    const int64_t per = int64_t(filled) * kbs;
+    const int64_t n = (b1 - b0) * per;
+    const int psz = pdt == F64 ? 8 : (pdt == F32 ? 4 : 2);
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = b0 + t / per;
+        const int64_t rj = t % per;
+        const int j = static_cast<int>(rj % kbs);
+        const int64_t len = (b + 1) * block <= dim ? block : dim - b * block;
+        if (j >= (kb < len ? kb : len)) continue;
+        const int64_t q = (b * m) * kbs + rj;  // ring position (rows r < filled are contiguous)
+        const int64_t e = b * block + win_idx[q];
+        const unsigned char* src = static_cast<const unsigned char*>(theta) + e * psz;
+        unsigned char* dst = static_cast<unsigned char*>(out) + q * psz;
+        if (psz == 2) *reinterpret_cast<uint16_t*>(dst) = *reinterpret_cast<const uint16_t*>(src);
+        else if (psz == 4) *reinterpret_cast<uint32_t*>(dst) = *reinterpret_cast<const uint32_t*>(src);
+        else *reinterpret_cast<uint64_t*>(dst) = *reinterpret_cast<const uint64_t*>(src);
+    }
+}
+
 __global__ void fill_synthetic_kernel(void* out, int dt, int64_t n, uint64_t seed, uint64_t step,
                                       int64_t offset, int levels) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
@@ -474,6 +498,17 @@ cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int
 cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double* out5,
                                  cudaStream_t s) {
     report_reduce_kernel<<<1, 1024, 0, s>>>(partials, nblocks, out5);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_window_theta(const int16_t* win_idx, const void* theta, int pdt, void* out, int64_t b0,
+                                      int64_t b1, int m, int kbs, int kb, int filled, int64_t block, int64_t dim,
+                                      cudaStream_t s) {
+    const int64_t n = (b1 - b0) * int64_t(filled) * kbs;
+    if (n <= 0) return cudaSuccess;
+    const int64_t want = (n + 255) / 256;
+    const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
+    gather_window_theta_kernel<<<grid, 256, 0, s>>>(win_idx, theta, pdt, out, b0, b1, m, kbs, kb, filled, block, dim);
     return cudaGetLastError();
 }
 
