@@ -151,6 +151,21 @@ MA_API ma_status ma_step(ma_handle* h, void* d_params, const void* d_grads, doub
 MA_API ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double lr,
                        ma_step_report* report);
 
+/* Data-parallel step with the gradient reduce-scatter fused in (SURVEY.md
+ * §8(f) rank 2; the step's input a = g + e is optim.cpp:166-168 with g the
+ * reduced gradient). d_srcs[r] (r < nsrc <= 8) point at rank r's gradient for
+ * THIS handle's element range — peer device pointers (CUDA IPC / symmetric
+ * memory over NVLink) or local buffers — and must stay unmodified until the
+ * step completes on `stream`. The step uses
+ *     g = rn_grad_dtype(((src_0 + src_1) + ... + src_{nsrc-1}) * scale)
+ * with fp32 sums and product for bf16/f32 gradients (fp64 for f64), written
+ * into d_grads (may alias one source), and is then bit-identical to ma_step on
+ * that g. The lean kernel reads the sources block by block inside the step
+ * (B_q = 64, k_b <= 64, bf16/bf16/bf16 or f32/f32/f32, no report, finite mode
+ * off/flag); other configurations run a reduce kernel, then ma_step. */
+MA_API ma_status ma_step_reduce(ma_handle* h, void* d_params, void* d_grads, const void* const* d_srcs,
+                                int32_t nsrc, float scale, double lr, void* stream, ma_step_report* report);
+
 /* Wait for outstanding work; returns MA_ERR_NONFINITE if the fused check hit. */
 MA_API ma_status ma_sync(ma_handle* h);
 

@@ -27,7 +27,7 @@ EXPORTED = [
     "ma_read_window_row", "ma_write_state", "ma_set_params", "ma_get_layout",
     "ma_kernel_launches", "ma_last_error", "ma_version", "ma_fill_synthetic", "ma_debug_counters",
     "ma_save_checkpoint", "ma_load_checkpoint", "ma_step_front", "ma_scatter_rows", "ma_step_stats",
-    "ma_read_error_vector",
+    "ma_read_error_vector", "ma_step_reduce",
 ]
 
 
@@ -91,6 +91,7 @@ def lib():
     L.ma_destroy.argtypes = [vp]
     L.ma_step.argtypes = [vp, vp, vp, C.c_double, vp, P(Report)]
     L.ma_step_host.argtypes = [vp, vp, vp, C.c_double, P(Report)]
+    L.ma_step_reduce.argtypes = [vp, vp, vp, P(vp), C.c_int32, C.c_float, C.c_double, vp, P(Report)]
     L.ma_sync.argtypes = [vp]
     L.ma_get_counters.argtypes = [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(C.c_int64)]
     L.ma_read_error_buffer.argtypes = [vp, vp, vp, vp]

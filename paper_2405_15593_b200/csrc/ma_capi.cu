@@ -647,6 +647,49 @@ ma_status ma_step(ma_handle* h, void* d_params, const void* d_grads, double lr, 
     return run_step(h, d_params, d_grads, lr, static_cast<cudaStream_t>(stream), report);
 }
 
+ma_status ma_step_reduce(ma_handle* h, void* d_params, void* d_grads, const void* const* d_srcs, int32_t nsrc,
+                         float scale, double lr, void* stream, ma_step_report* report) {
+    if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
+    if (!d_srcs || nsrc < 1 || nsrc > ma::kMaxRanks)
+        return fail(MA_ERR_INVALID_ARG, "step_reduce: nsrc must be in [1, 8]");
+    for (int r = 0; r < nsrc; ++r)
+        if (!d_srcs[r]) return fail(MA_ERR_INVALID_ARG, "step_reduce: null gradient source");
+    if (!(lr > 0.0)) return fail(MA_ERR_INVALID_ARG, "step: lr must be > 0");
+    if (!d_params || !d_grads) return fail(MA_ERR_INVALID_ARG, "step: null buffer");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const Shape& s = h->shape;
+    ma::StepArgs a;
+    base_args(h, &a);
+    a.rs_n = nsrc;
+    a.rs_scale = scale;
+    for (int r = 0; r < nsrc; ++r) a.rs_src[r] = d_srcs[r];
+    const char* env = std::getenv("MA_RS_UNFUSED");
+    const bool fused = h->fast && h->warp && !s.global && h->cfg.finite_mode != MA_FINITE_STRICT && !report &&
+                       !(env && env[0] == '1') && ma::lean_rs_ok(a);
+    if (!fused) {  // reduce into d_grads, then the ordinary step
+        MA_CUDA(ma::launch_reduce_grads(d_srcs, nsrc, scale, h->cfg.grad_dtype, d_grads, 0, s.dim, st));
+        ++h->launches;
+        return run_step(h, d_params, d_grads, lr, st, report);
+    }
+    // The lean kernel reduces its full blocks itself; the partial tail block
+    // (generic kernel, launched after it) is reduced up front.
+    if (s.dim % s.block) {
+        MA_CUDA(ma::launch_reduce_grads(d_srcs, nsrc, scale, h->cfg.grad_dtype, d_grads, (s.dim / s.block) * s.block,
+                                        s.dim, st));
+        ++h->launches;
+    }
+    a.grads = d_grads;
+    a.params = d_params;
+    a.lr = lr;
+    a.lr32 = static_cast<float>(lr);
+    push_and_weights(h, &a);
+    MA_CUDA(launch(h, a, s.b1 - s.b0, st));
+    ++h->launches;
+    h->last_stream = st;
+    return MA_OK;
+}
+
 ma_status ma_set_params(ma_handle* h, const void* h_params) {
     if (!h || !h_params) return fail(MA_ERR_INVALID_ARG, "null argument");
     DeviceGuard g(h->device);

@@ -23,6 +23,12 @@ __device__ __forceinline__ uint16_t bf16_bits(double x) {
     asm("{ .reg .b16 t; cvt.rn.bf16.f64 t, %1; mov.b16 %0, t; }" : "=h"(r) : "d"(x));
     return r;
 }
+// Two fp32 values to packed bf16 (RNE; lo in the low half), one instruction.
+__device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
 __device__ __forceinline__ double bf16_round(double x) {
     return static_cast<double>(__uint_as_float(static_cast<uint32_t>(bf16_bits(x)) << 16));
 }

@@ -8,6 +8,7 @@
 namespace ma {
 
 constexpr int kMaxWindow = 256;  // m supported on device (params carry m weights)
+constexpr int kMaxRanks = 8;     // gradient sources of a fused reduce-scatter step
 constexpr int kMaxBlock = 8192;  // B_d supported on device (fp64 block held on chip)
 constexpr int kCandCap = 128;    // exact-rank stage capacity of the Top-K select
 constexpr int kReportFields = 5; // Σg², Σa², Σr², Σe_new², nnz per block
@@ -54,6 +55,12 @@ struct StepArgs {
     double* dense;
     int32_t bits;  // EF code width; the generic kernel handles 1..8, the others 4
     int32_t pad1;
+    // fused gradient reduce-scatter (ma_step_reduce, lean kernel RS variant):
+    // g = rn_gdt(((src_0 + src_1) + ...) * rs_scale) in fp32, written to grads
+    // block by block before the step reads it; rs_n = 0 off
+    const void* rs_src[kMaxRanks];
+    int32_t rs_n;
+    float rs_scale;
 };
 
 // Global Top-K mode (ma_global.cu, blockwise = false with d > kMaxBlock).
@@ -126,6 +133,12 @@ cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double
 cudaError_t launch_gather_window_theta(const int16_t* win_idx, const void* theta, int pdt, void* out, int64_t b0,
                                       int64_t b1, int m, int kbs, int kb, int filled, int64_t block, int64_t dim,
                                       cudaStream_t s);
+// g[e0, e1) = rn_gdt(((src_0 + src_1) + ...) * scale) (fp32 sums for bf16/f32
+// gradients, fp64 for f64): the unfused reduce-scatter of ma_step_reduce.
+cudaError_t launch_reduce_grads(const void* const* srcs, int nsrc, float scale, int gdt, void* dst, int64_t e0,
+                                int64_t e1, cudaStream_t s);
+// lean kernel with the fused reduce (B_q = 64, k_b <= 64, bf16/bf16/bf16 or f32/f32/f32)
+bool lean_rs_ok(const StepArgs& a);
 cudaError_t launch_fill_synthetic(void* out, int dtype, int64_t n, uint64_t seed, uint64_t step,
                                   int64_t offset, int levels, cudaStream_t s);
 

@@ -512,6 +512,46 @@ cudaError_t launch_gather_window_theta(const int16_t* win_idx, const void* theta
     return cudaGetLastError();
 }
 
+struct RsSrc {
+    const void* p[kMaxRanks];
+};
+
+// Unfused reduce-scatter of ma_step_reduce: fixed rank order, fp32 sums for
+// bf16/f32 gradients (fp64 for f64), one multiply by the scale, one rounding.
+__global__ void reduce_grads_kernel(RsSrc src, int n, float scale, int gdt, void* dst, int64_t e0, int64_t e1) {
+    for (int64_t e = e0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < e1;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        if (gdt == F64) {
+            double acc = static_cast<const double*>(src.p[0])[e];
+            for (int r = 1; r < n; ++r) acc = __dadd_rn(acc, static_cast<const double*>(src.p[r])[e]);
+            static_cast<double*>(dst)[e] = __dmul_rn(acc, static_cast<double>(scale));
+        } else if (gdt == F32) {
+            float acc = static_cast<const float*>(src.p[0])[e];
+            for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, static_cast<const float*>(src.p[r])[e]);
+            static_cast<float*>(dst)[e] = __fmul_rn(acc, scale);
+        } else {
+            auto ld = [&](int r) {
+                return __uint_as_float(uint32_t(static_cast<const uint16_t*>(src.p[r])[e]) << 16);
+            };
+            float acc = ld(0);
+            for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, ld(r));
+            static_cast<uint16_t*>(dst)[e] = static_cast<uint16_t>(bf16x2_bits(__fmul_rn(acc, scale), 0.0f));
+        }
+    }
+}
+
+cudaError_t launch_reduce_grads(const void* const* srcs, int nsrc, float scale, int gdt, void* dst, int64_t e0,
+                                int64_t e1, cudaStream_t s) {
+    if (e1 <= e0) return cudaSuccess;
+    if (nsrc < 1 || nsrc > kMaxRanks) return cudaErrorInvalidValue;
+    RsSrc src{};
+    for (int r = 0; r < nsrc; ++r) src.p[r] = srcs[r];
+    const int64_t want = (e1 - e0 + 255) / 256;
+    const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
+    reduce_grads_kernel<<<grid, 256, 0, s>>>(src, nsrc, scale, gdt, dst, e0, e1);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fill_synthetic(void* out, int dtype, int64_t n, uint64_t seed, uint64_t step,
                                   int64_t offset, int levels, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;

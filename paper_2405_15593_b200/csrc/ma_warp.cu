@@ -82,10 +82,13 @@ struct WLayout {
     }
 };
 
-template <int LPB_, int GDT_, int PDT_, int VDT_, bool REP_, int CAPL_ = 4>
+template <int LPB_, int GDT_, int PDT_, int VDT_, bool REP_, int CAPL_ = 4, bool RS_ = false>
 struct KW {
     static constexpr int LPB = LPB_, GDT = GDT_, PDT = PDT_, VDT = VDT_;
     static constexpr int CAPL = CAPL_;  // lean kernel: exact-stage candidate slots per lane
+    // lean kernel: the gradient is reduced from p.rs_src[] into p.grads by the
+    // kernel itself (fused reduce-scatter), so p.grads is read with coherent loads
+    static constexpr bool RS = RS_;
     static constexpr int BUCKET = 8 * LPB_;
     static constexpr bool REPORT = REP_;
 };
@@ -96,13 +99,16 @@ struct Raw8 {
     static constexpr int N = DT == BF16 ? 1 : (DT == F32 ? 2 : 4);
     uint4 v[N];
 };
-template <int DT>
+template <int DT, bool NC = true>
 __device__ __forceinline__ Raw8<DT> load_raw8(const void* g, int64_t e0) {
     Raw8<DT> r;
     const uint4* q = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(g) +
                                                     e0 * (DT == BF16 ? 2 : (DT == F32 ? 4 : 8)));
 #pragma unroll
-    for (int k = 0; k < Raw8<DT>::N; ++k) r.v[k] = __ldg(q + k);
+    for (int k = 0; k < Raw8<DT>::N; ++k) {
+        if constexpr (NC) r.v[k] = __ldg(q + k);
+        else r.v[k] = q[k];
+    }
     return r;
 }
 template <int DT>
@@ -218,7 +224,7 @@ __device__ __noinline__ int slow_select(const StepArgs* pp, unsigned char* ws, i
     const int kb = p.per_block_k;
     auto block_a = [&](int j, double (&a)[8]) {
         const int e0 = j * 256 + lane * 8;
-        widen8<KT::GDT>(load_raw8<KT::GDT>(p.grads, base + e0), a);
+        widen8<KT::GDT>(load_raw8<KT::GDT, !KT::RS>(p.grads, base + e0), a);
         add_decoded8(a, *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0) >> 1)),
                      s_ll[e0 / KT::BUCKET]);
     };
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
     uint32_t cm0 = 0, cm1 = 0, cm2 = 0, cm3 = 0;  // candidate bits: byte j = iteration j
     double rep[kReportFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
     {
-        Raw8<KT::GDT> nr = load_raw8<KT::GDT>(p.grads, base + lane * 8);
+        Raw8<KT::GDT> nr = load_raw8<KT::GDT, !KT::RS>(p.grads, base + lane * 8);
         uint32_t ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + lane * 8) >> 1));
 #pragma unroll 1
         for (int j = 0; j < kIter; ++j) {
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
             const Raw8<KT::GDT> r = nr;
             const uint32_t cw = ncw;
             if (j + 1 < kIter) {
-                nr = load_raw8<KT::GDT>(p.grads, base + e0 + 256);
+                nr = load_raw8<KT::GDT, !KT::RS>(p.grads, base + e0 + 256);
                 ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0 + 256) >> 1));
             }
             double a[8];
@@ -747,7 +753,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
     for (int j = 0; j < kIter; ++j) {
         const int e0 = j * 256 + lane * 8;
         double a[8];
-        widen8<KT::GDT>(load_raw8<KT::GDT>(p.grads, base + e0), a);
+        widen8<KT::GDT>(load_raw8<KT::GDT, !KT::RS>(p.grads, base + e0), a);
         add_decoded8(a, *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0) >> 1)),
                      s_ll[e0 / BUCKET]);
         const uint32_t sel8 = (s_sel[e0 >> 5] >> (e0 & 31)) & 0xFFu;
@@ -802,7 +808,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
         if (want_report) {
             const double level = rng == 0.0 ? 0.0 : __ddiv_rn(rng, 15.0);
             double x[8];
-            widen8<KT::GDT>(load_raw8<KT::GDT>(p.grads, base + e0), x);
+            widen8<KT::GDT>(load_raw8<KT::GDT, !KT::RS>(p.grads, base + e0), x);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const double en =
@@ -1178,8 +1184,49 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     unsigned char* gwv = static_cast<unsigned char*>(p.win_val) + went * vsz;
 
     if constexpr (PH & 1) {
+    if constexpr (KT::RS) {
+        // ---- fused reduce-scatter (ma_step_reduce): this block's gradient is
+        //      ((src_0 + src_1) + ...) * scale in fp32, rank order, rounded to the
+        //      gradient dtype and written to p.grads, which the passes below read
+        //      back (same lane, same addresses in pass 1; L1/L2 hits). Sources
+        //      are peer (NVLink) or local pointers; loads of G ranks in flight.
+        constexpr int G = KT::GDT == BF16 ? kMaxRanks : kMaxRanks / 2;
+        const int n = p.rs_n;
+#pragma unroll 1
+        for (int j = 0; j < kIter; ++j) {
+            const int64_t e = base + j * 256 + lane * 8;
+            float acc[8];
+#pragma unroll 1
+            for (int r0 = 0; r0 < n; r0 += G) {
+                Raw8<KT::GDT> v[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q)
+                    if (r0 + q < n) v[q] = load_raw8<KT::GDT, false>(p.rs_src[r0 + q], e);
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    if (r0 + q < n) {
+                        float x[8];
+                        g32x8<KT::GDT>(v[q], x);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) acc[i] = (r0 + q == 0) ? x[i] : __fadd_rn(acc[i], x[i]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = __fmul_rn(acc[i], p.rs_scale);
+            unsigned char* dst = static_cast<unsigned char*>(const_cast<void*>(p.grads)) + e * gsz;
+            if constexpr (KT::GDT == BF16) {
+                *reinterpret_cast<uint4*>(dst) = make_uint4(bf16x2_bits(acc[0], acc[1]), bf16x2_bits(acc[2], acc[3]),
+                                                            bf16x2_bits(acc[4], acc[5]), bf16x2_bits(acc[6], acc[7]));
+            } else {
+                reinterpret_cast<float4*>(dst)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                reinterpret_cast<float4*>(dst)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            }
+        }
+        __syncwarp();
+    }
     if (lane == 0) {
-        prefetch_l2_keep(static_cast<const unsigned char*>(p.grads) + base * gsz, kBlk * gsz);
+        if constexpr (!KT::RS) prefetch_l2_keep(static_cast<const unsigned char*>(p.grads) + base * gsz, kBlk * gsz);
         prefetch_l2_keep(p.codes + base / 2, kBlk / 2);
         prefetch_l2(p.meta + base / BUCKET, NBK * 16);
     }
@@ -1212,7 +1259,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
     // ---- pass 1: fp32 screen of a = g + decode(EF) against the carried threshold ----
     uint32_t cm0 = 0, cm1 = 0, cm2 = 0, cm3 = 0;
     {
-        Raw8<KT::GDT> nr = load_raw8<KT::GDT>(p.grads, base + lane * 8);
+        Raw8<KT::GDT> nr = load_raw8<KT::GDT, !KT::RS>(p.grads, base + lane * 8);
         uint32_t ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + lane * 8) >> 1));
 #pragma unroll 1
         for (int j = 0; j < kIter; ++j) {
@@ -1220,7 +1267,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             const Raw8<KT::GDT> r = nr;
             const uint32_t cw = ncw;
             if (j + 1 < kIter) {
-                nr = load_raw8<KT::GDT>(p.grads, base + e0 + 256);
+                nr = load_raw8<KT::GDT, !KT::RS>(p.grads, base + e0 + 256);
                 ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0 + 256) >> 1));
             }
             const float4 f = s_llf[e0 / BUCKET];
@@ -1511,7 +1558,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __gr
             prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
         }
         double a[8];
-        widen8<KT::GDT>(load_raw8<KT::GDT>(p.grads, base + e0), a);
+        widen8<KT::GDT>(load_raw8<KT::GDT, !KT::RS>(p.grads, base + e0), a);
         add_decoded8(a, *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0) >> 1)), s_ll[e0 / BUCKET]);
         const uint32_t sel8 = (s_sel[e0 >> 5] >> (e0 & 31)) & 0xFFu;
 #pragma unroll
@@ -1820,12 +1867,29 @@ cudaError_t launch_step_lean_phase(const StepArgs& a, int ph, cudaStream_t s) {
     }
 }
 
+// Fused reduce-scatter variant (ma_step_reduce): B_q = 64, k_b <= 64, the two
+// uniform dtype combos; everything else reduces with launch_reduce_grads first.
+bool lean_rs_ok(const StepArgs& a) {
+    if (!lean_ok(a) || a.bucket != 64 || a.per_block_k > kCap / 2) return false;
+    if (a.rs_n < 1 || a.rs_n > kMaxRanks) return false;
+    const int key = dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype);
+    return key == dtype_key_w(BF16, BF16, BF16) || key == dtype_key_w(F32, F32, F32);
+}
+
+cudaError_t launch_lean_rs(const StepArgs& a, cudaStream_t s) {
+    if (!lean_rs_ok(a)) return cudaErrorInvalidConfiguration;
+    if (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype) == dtype_key_w(BF16, BF16, BF16))
+        return launch_kl<KW<8, BF16, BF16, BF16, false, 4, true>>(a, s);
+    return launch_kl<KW<8, F32, F32, F32, false, 4, true>>(a, s);
+}
+
 bool warp_can_run(const StepArgs& a) { return lean_ok(a) || a.per_block_k <= kCap / 2; }
 
 cudaError_t launch_step_warp(const StepArgs& a, cudaStream_t s) {
     if (a.block_count <= 0) return cudaSuccess;
     if (!warp_can_run(a)) return cudaErrorInvalidConfiguration;
     if ((a.block_count + kWarps - 1) / kWarps > 0x7FFFFFFFll) return cudaErrorInvalidConfiguration;
+    if (a.rs_n > 0) return launch_lean_rs(a, s);
     if (lean_ok(a)) return a.bucket == 64 ? launch_ldt<8>(a, s) : launch_ldt<4>(a, s);
     return a.partials ? launch_wrep<true>(a, s) : launch_wrep<false>(a, s);
 }

@@ -305,6 +305,31 @@ class MicroAdam(_Handle):
                           C.byref(rep) if report else None))
         return StepReport.from_c(rep) if report else None
 
+    def step_reduce(self, params, grads, sources, scale: float = 1.0, lr: Optional[float] = None,
+                    stream=None, report: bool = False) -> Optional[StepReport]:
+        """Step with the gradient reduce-scatter fused in (ma_step_reduce).
+
+        `sources` are the ranks' gradients for this engine's element range:
+        device tensors of the gradient dtype or raw device pointers (peer
+        pointers from symmetric memory / CUDA IPC). The step uses
+        g = rn(((s_0 + s_1) + ...) * scale) (fp32 sums for bf16/f32), written
+        into `grads` (which may be one of the sources)."""
+        if not 1 <= len(sources) <= 8:
+            raise ValueError("step_reduce: 1 to 8 gradient sources")
+        ptrs = (C.c_void_p * len(sources))(*[
+            s if isinstance(s, int) else self._ptr(s, self.grad_dtype, "grads") for s in sources])
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        elif hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        rep = _capi.Report()
+        _ok(lib().ma_step_reduce(self._h, self._ptr(params, self.param_dtype, "params"),
+                                 self._ptr(grads, self.grad_dtype, "grads"), ptrs, len(sources),
+                                 float(scale), self.hp.lr if lr is None else lr, C.c_void_p(stream),
+                                 C.byref(rep) if report else None))
+        return StepReport.from_c(rep) if report else None
+
     def step_host(self, h_params, h_grads, lr: Optional[float] = None,
                   report: bool = False) -> Optional[StepReport]:
         """Reference-facing host path (ma_step_host): host θ in/out, host g in.
