@@ -86,7 +86,6 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
         if (dt < MA_F64 || dt > MA_BF16) return fail(MA_ERR_INVALID_ARG, "unknown dtype");
     if (cfg->finite_mode < MA_FINITE_FLAG || cfg->finite_mode > MA_FINITE_OFF)
         return fail(MA_ERR_INVALID_ARG, "unknown finite_mode");
-    if (hp.bits > 8) return fail(MA_ERR_UNSUPPORTED, "device path implements bits <= 8");
     if (hp.window > ma::kMaxWindow) return fail(MA_ERR_UNSUPPORTED, "window > 256 not supported on device");
 
     Shape s;
@@ -560,7 +559,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
                                                  cfg->param_dtype, cfg->value_dtype);
     h->tail_variant = ma::pick_variant(static_cast<int>(s.block));
     size_t smem = ma::step_smem_bytes(h->tail_variant.nt, h->tail_variant.ept, int(s.block),
-                                      int(s.bucket), int(cfg->hp.window), int(s.kb_stride));
+                                      int(s.bucket), int(cfg->hp.window), int(s.kb_stride), int(cfg->hp.bits));
     if (fv.nt && !(force_generic && force_generic[0] == '1')) {
         const size_t fs = ma::fast_smem_bytes(fv, int(s.block), int(s.bucket), int(cfg->hp.window),
                                               int(s.kb_stride), cfg->grad_dtype, cfg->param_dtype,
@@ -920,7 +919,7 @@ ma_status ma_read_error_vector(ma_handle* h, double* out) {
         const double level = m.x == m.y ? 0.0 : (m.y - m.x) / max_code;
         const int64_t pos = i * bits;  // LSB-first bit stream (quantize.cpp:116-128)
         uint32_t w = codes[size_t(pos >> 3)];
-        if ((pos & 7) + bits > 8) w |= uint32_t(codes[size_t((pos >> 3) + 1)]) << 8;
+        for (int k = 1; 8 * k < int(pos & 7) + bits; ++k) w |= uint32_t(codes[size_t((pos >> 3) + k)]) << (8 * k);
         const double c = double((w >> (pos & 7)) & ((1u << bits) - 1u));
         out[i] = c * level + m.x;
     }

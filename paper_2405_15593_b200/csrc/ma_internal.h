@@ -102,7 +102,7 @@ struct Variant {
 };
 
 // Dynamic shared memory bytes needed by the step kernel for this shape.
-size_t step_smem_bytes(int nt, int ept, int block, int bucket, int m, int kb_stride);
+size_t step_smem_bytes(int nt, int ept, int block, int bucket, int m, int kb_stride, int bits = 4);
 // Smallest variant that holds `block` elements on chip; nt == 0 if none.
 Variant pick_variant(int block);
 

@@ -39,7 +39,8 @@ struct SmemLayout {
         off += bytes;
         return r;
     }
-    __host__ __device__ SmemLayout(int nt, int ept, int block, int bucket, int m, int kbs) {
+    // code_w: bytes per staged code (1 for bits <= 8, 4 up to 24)
+    __host__ __device__ SmemLayout(int nt, int ept, int block, int bucket, int m, int kbs, int code_w = 1) {
         const size_t nbk = size_t((block + bucket - 1) / bucket);
         const size_t ent = size_t(m) * size_t(kbs);
         size_t off = 0;
@@ -57,7 +58,7 @@ struct SmemLayout {
         scan = take(off, (size_t(ept / 2) * size_t(nt / 32) + 1) * 4);
         misc = take(off, 32 * 4);
         eidx = take(off, ent * 2);
-        code = take(off, size_t(block));
+        code = take(off, size_t(block) * size_t(code_w));
         selm = take(off, size_t(block));
         total = (off + 15) & ~size_t(15);
     }
@@ -72,7 +73,7 @@ __device__ __forceinline__ uint32_t read_code(const uint8_t* codes, int64_t i, i
     const int64_t byte0 = pos >> 3;
     const int sh = static_cast<int>(pos & 7);
     uint32_t w = codes[byte0];
-    if (sh + bits > 8) w |= static_cast<uint32_t>(codes[byte0 + 1]) << 8;
+    for (int k = 1; 8 * k < sh + bits; ++k) w |= static_cast<uint32_t>(codes[byte0 + k]) << (8 * k);
     return (w >> sh) & ((1u << bits) - 1u);
 }
 
@@ -145,7 +146,7 @@ template <int NT, int EPT>
 __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constant__ StepArgs p) {
     constexpr int NP = EPT / 2;
     extern __shared__ __align__(16) unsigned char smem[];
-    const SmemLayout L(NT, EPT, p.block, p.bucket, p.m, p.kb_stride);
+    const SmemLayout L(NT, EPT, p.block, p.bucket, p.m, p.kb_stride, p.bits > 8 ? 4 : 1);
     double* s_lo = reinterpret_cast<double*>(smem + L.lo);
     double* s_lvl = reinterpret_cast<double*>(smem + L.lvl);
     double* s_a = reinterpret_cast<double*>(smem + L.a);
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
     int* s_misc = reinterpret_cast<int*>(smem + L.misc);
     int16_t* s_eidx = reinterpret_cast<int16_t*>(smem + L.eidx);
     uint8_t* s_code = reinterpret_cast<uint8_t*>(smem + L.code);
+    uint32_t* s_code32 = reinterpret_cast<uint32_t*>(smem + L.code);  // bits > 8
     uint8_t* s_selm = reinterpret_cast<uint8_t*>(smem + L.selm);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -300,6 +302,9 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
         // quotient's unless t lands within 7e-15 of an integer; such t take
         // the IEEE division.
         const bool fast = level >= 0x1p-1000;
+        // |d·rn(1/level) − d/level| ≤ q·1.5·2^-52 with q ≤ max_code: a margin of
+        // max_code·2^-44 (≥ 1e-12) around the integers is conservative.
+        const double guard = fmax(1e-12, max_code * 0x1p-44);
         const double rinv = fast ? __drcp_rn(level) : 0.0;
         for (int i = lane; i < n; i += 32) {
             const double x = s_a[s + i];
@@ -309,11 +314,12 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
                 double t = __dadd_rn(__dmul_rn(d, rinv), 0.5);
                 double f = floor(t);
                 const double fr = __dsub_rn(t, f);
-                if (!fast || fr < 1e-12 || fr > 1.0 - 1e-12) f = floor(__dadd_rn(__ddiv_rn(d, level), 0.5));
+                if (!fast || fr < guard || fr > 1.0 - guard) f = floor(__dadd_rn(__ddiv_rn(d, level), 0.5));
                 f = f < 0.0 ? 0.0 : (f > max_code ? max_code : f);
                 c = static_cast<uint32_t>(f);
             }
-            s_code[s + i] = static_cast<uint8_t>(c);
+            if (bits > 8) s_code32[s + i] = c;
+            else s_code[s + i] = static_cast<uint8_t>(c);
             if (want_report) {
                 const double en = __dadd_rn(__dmul_rn(static_cast<double>(c), level), lo);
                 rep[3] += en * en;
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
             const int b0 = jb * 8;
             for (int i = b0 / bits; i < len && i * bits < b0 + 8; ++i) {
                 const int sh = i * bits - b0;  // bit position of code i relative to this byte
-                const uint32_t c = s_code[i];
+                const uint32_t c = bits > 8 ? s_code32[i] : s_code[i];
                 byte |= sh >= 0 ? (c << sh) : (c >> -sh);
             }
             p.codes[(base * bits) / 8 + jb] = static_cast<uint8_t>(byte & 0xFFu);
@@ -451,7 +457,7 @@ __global__ void fill_synthetic_kernel(void* out, int dt, int64_t n, uint64_t see
 
 template <int NT, int EPT>
 cudaError_t launch_variant(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
-    const size_t smem = SmemLayout(NT, EPT, a.block, a.bucket, a.m, a.kb_stride).total;
+    const size_t smem = SmemLayout(NT, EPT, a.block, a.bucket, a.m, a.kb_stride, a.bits > 8 ? 4 : 1).total;
     auto k = microadam_step_kernel<NT, EPT>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem));
@@ -462,8 +468,8 @@ cudaError_t launch_variant(const StepArgs& a, int64_t nblocks, cudaStream_t s) {
 
 }  // namespace
 
-size_t step_smem_bytes(int nt, int ept, int block, int bucket, int m, int kb_stride) {
-    return SmemLayout(nt, ept, block, bucket, m, kb_stride).total;
+size_t step_smem_bytes(int nt, int ept, int block, int bucket, int m, int kb_stride, int bits) {
+    return SmemLayout(nt, ept, block, bucket, m, kb_stride, bits > 8 ? 4 : 1).total;
 }
 
 Variant pick_variant(int block) {

@@ -135,6 +135,14 @@ StepReport MicroAdam::step(void* d_params, const void* d_grads, double lr, void*
     return StepReport{r.grad_norm, r.error_norm, r.empirical_q, r.update_nnz, r.loss};
 }
 
+StepReport MicroAdam::step_reduce(void* d_params, void* d_grads, const std::vector<const void*>& sources,
+                                  float scale, double lr, void* stream, bool want_report) {
+    ma_step_report r{};
+    check(ma_step_reduce(h_, d_params, d_grads, sources.data(), static_cast<int32_t>(sources.size()), scale, lr,
+                         stream, want_report ? &r : nullptr));
+    return StepReport{r.grad_norm, r.error_norm, r.empirical_q, r.update_nnz, r.loss};
+}
+
 void MicroAdam::synchronize() { check(ma_sync(h_)); }
 
 ma_layout_info MicroAdam::layout() const {

@@ -116,6 +116,10 @@ public:
     // θ -= lr · update, in place; asynchronous on `stream` unless want_report.
     StepReport step(void* d_params, const void* d_grads, double lr, void* stream = nullptr,
                     bool want_report = false);
+    // Data-parallel step with the gradient reduce-scatter fused in
+    // (ma_step_reduce): sources = every rank's gradient for this handle's range.
+    StepReport step_reduce(void* d_params, void* d_grads, const std::vector<const void*>& sources,
+                           float scale, double lr, void* stream = nullptr, bool want_report = false);
     void synchronize();  // throws std::invalid_argument on a flagged non-finite gradient
 
     ma_layout_info layout() const;

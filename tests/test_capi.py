@@ -107,7 +107,7 @@ def test_k_exceeding_dim_rejected(ma):  # optim.cpp:23-26
     assert _validate(ma, dim=5, k=7) == ma._capi.MA_ERR_INVALID_ARG
 
 
-@pytest.mark.parametrize("kw", [dict(bits=12), dict(block=16384), dict(bucket=100),
+@pytest.mark.parametrize("kw", [dict(block=16384), dict(bucket=100),
                                 dict(block=4095), dict(window=300),
                                 dict(lossless_error=1, blockwise=0)])
 def test_unsupported_device_shapes_are_explicit(ma, kw):
@@ -178,5 +178,7 @@ def test_lossless_blockwise_is_supported(ma):
 def test_code_widths(ma):
     assert _validate(ma, dim=100_000, bits=3, block=1000, bucket=8) == ma._capi.MA_OK
     assert _validate(ma, dim=100_000, bits=3, block=1001, bucket=7) == ma._capi.MA_ERR_UNSUPPORTED
-    assert _validate(ma, dim=100_000, bits=12) == ma._capi.MA_ERR_UNSUPPORTED
+    assert _validate(ma, dim=100_000, bits=12) == ma._capi.MA_OK      # up to the reference's 24
+    assert _validate(ma, dim=100_000, bits=24, block=1000, bucket=8) == ma._capi.MA_OK
+    assert _validate(ma, dim=100_000, bits=12, block=1001, bucket=7) == ma._capi.MA_ERR_UNSUPPORTED
     assert _validate(ma, dim=100_000, bits=2, blockwise=0) == ma._capi.MA_ERR_UNSUPPORTED

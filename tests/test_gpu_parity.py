@@ -410,10 +410,12 @@ def test_reference_side_adapter_drives_reference_run_loop():
 
 
 @pytest.mark.parametrize("bits,block,bucket", [(1, 4096, 64), (2, 4096, 64), (3, 1000, 8), (5, 4096, 128),
-                                               (8, 512, 16)])
+                                               (8, 512, 16), (12, 4096, 64), (16, 2048, 32), (24, 1000, 8),
+                                               (23, 8192, 64)])
 def test_other_code_widths_vs_unmodified_reference(bits, block, bucket):
     # QuantizedErrorBuffer with bits != 4 (quantize.cpp:102-128 LSB-first bit
-    # stream, max_code = 2^bits - 1): generic kernel, fp64, bit-exact
+    # stream, max_code = 2^bits - 1, bits up to the reference's 24): generic
+    # kernel, fp64, bit-exact
     hp = dict(lr=1e-2, window=4, bits=bits, block=block, bucket=bucket)
     run_parity(20_011, hp, gdt="f64", pdt="f64", vdt="f64", steps=8,
                check_reference=oracle.reference_available())

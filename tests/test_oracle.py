@@ -321,3 +321,21 @@ def test_oracle_matches_reference_random_configs(seed):
         assert np.array_equal(so.codes, sr.codes)
         assert np.array_equal(so.lo.view(np.uint64), sr.lo.view(np.uint64))
         assert np.array_equal(so.last_idx, sr.last_idx)
+
+
+@pytest.mark.skipif(not oracle.reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("bits", [1, 3, 8, 12, 16, 23, 24])
+def test_oracle_matches_reference_code_widths(bits):
+    # HyperParams::bits in [1, 24] (optim.cpp:12): bit stream + max_code = 2^bits - 1
+    rng = np.random.default_rng(bits)
+    d = 9_001
+    hp = dict(block=1000, bucket=8, window=3, lr=1e-2, bits=bits)
+    theta0 = rng.standard_normal(d)
+    o, r = oracle.Oracle(theta0, hp), oracle.Reference(theta0, hp)
+    for s in range(1, 6):
+        g = oracle.synth(7, s, 0, d, "f32")
+        assert o.step(g) == r.step(g)
+        so, sr = o.state(), r.state()
+        assert np.array_equal(so.params.view(np.uint64), sr.params.view(np.uint64))
+        assert np.array_equal(so.codes, sr.codes)
+        assert np.array_equal(so.lo.view(np.uint64), sr.lo.view(np.uint64))
