@@ -1150,8 +1150,11 @@ __device__ __forceinline__ void prof_mark(const StepArgs& p, int k) {
 
 // PH: 3 = the fused step; 1 = front only (EF decode, Top-K, window row + stage
 // copy, EF re-quantization); 2 = ADAM_STATS + update only (sparse propagation).
+#ifndef MA_LEAN_MINB
+#define MA_LEAN_MINB 8  // resident CTAs per SM the lean kernel is compiled for (64 registers)
+#endif
 template <class KT, int PH = 3>
-__global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_lean(const __grid_constant__ StepArgs p) {
+__global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean(const __grid_constant__ StepArgs p) {
     constexpr int BUCKET = KT::BUCKET, LPB = KT::LPB;
     constexpr int gsz = KT::GDT == F32 ? 4 : 2;
     constexpr int psz = KT::PDT == F64 ? 8 : (KT::PDT == F32 ? 4 : 2);
