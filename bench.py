@@ -414,11 +414,12 @@ def run_ours(args):
         h2d_ms = ev0.elapsed_time(ev1)
         del dg
         lay = eng.layout
-        if os.environ.get("MA_HOST_DENSE") == "1":
-            d2h, ret = n * DT_BYTES[pdt], "updated θ D2H (dense)"
-        else:  # window ring indices (int16) + θ gathered at them, scattered on host threads
+        if os.environ.get("MA_HOST_SPARSE") == "1":
+            # window ring indices (int16) + θ gathered at them, scattered on host threads
             d2h = lay.num_blocks * args.window * lay.kb_stride * (2 + DT_BYTES[pdt])
             ret = "θ at the window coordinates D2H (ring idx + gathered θ), host-thread scatter"
+        else:
+            d2h, ret = n * DT_BYTES[pdt], "updated θ D2H (dense)"
         e2e = {"value": dim_total / te, "unit": UNIT, "h2d_bytes_per_step": n * DT_BYTES[gdt],
                "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "ms_per_step": te * 1e3, "h2d_only_ms": h2d_ms,

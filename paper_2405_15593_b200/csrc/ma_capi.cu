@@ -726,10 +726,12 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
     // Chunked pipeline: H2D grads of chunk c+1 overlaps the step of chunk c
     // and the return of θ for chunk c-1 (two copy engines + SMs busy at once).
     // θ changes only at window coordinates (optim.cpp:183-187: u = 0 off the
-    // window), so unless MA_HOST_DENSE=1 the return is sparse: the window ring
+    // window), so with MA_HOST_SPARSE=1 the return is sparse: the window ring
     // indices and the θ values gathered at them (4 bytes per window entry
     // against 2 per parameter for bf16 θ), scattered into h_params by host
-    // threads as each chunk lands.
+    // threads as each chunk lands. Off by default: the scatter still touches
+    // nearly every cache line of host θ and on a 16-core host costs more than
+    // the dense D2H it replaces (7B: 314 vs 291 ms per call).
     ma::StepArgs a;
     base_args(h, &a);
     a.grads = h->d_gstage;
@@ -739,9 +741,9 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
     push_and_weights(h, &a);
     const int64_t nb = s.b1 - s.b0;
     const int64_t m = h->cfg.hp.window, kbs = s.kb_stride;
-    const char* dense_env = std::getenv("MA_HOST_DENSE");
+    const char* sparse_env = std::getenv("MA_HOST_SPARSE");
     const bool sparse_ret =
-        !s.global && h->host_synced == h_params && !(dense_env && dense_env[0] == '1');
+        !s.global && h->host_synced == h_params && sparse_env && sparse_env[0] == '1';
     const size_t ring_n = size_t(nb) * size_t(m) * size_t(kbs);
     if (sparse_ret && !h->d_gath) {
         MA_CUDA(cudaMalloc(&h->d_gath, ring_n * psz));

@@ -1,14 +1,13 @@
 """ma_step_host (the reference-facing host-buffer step) against ma_step on the
 device, bit for bit.
 
-The chunked host path streams g up and returns θ sparsely: the window ring
-indices plus the θ values gathered at them, scattered into the caller's
-buffer on host threads (θ changes only at window coordinates,
-optim.cpp:183-187). Checked: several 64 MB chunks with a tail block, ring
-wrap-around (steps > m), bf16 / f32 / f64 θ, the dense return
-(MA_HOST_DENSE=1) and a switch to a fresh host buffer mid-run (dense
-fallback: the sparse return is only valid into the buffer that already holds
-the device θ).
+The chunked host path streams g up and θ back; with MA_HOST_SPARSE=1 it
+returns only the window ring indices plus the θ values gathered at them,
+scattered into the caller's buffer on host threads (θ changes only at window
+coordinates, optim.cpp:183-187). Checked: several 64 MB chunks with a tail
+block, ring wrap-around (steps > m), bf16 / f32 / f64 θ, the default dense
+return, and a switch to a fresh host buffer mid-run (dense fallback: the
+sparse return is only valid into the buffer that already holds the device θ).
 """
 import os
 
@@ -34,6 +33,7 @@ def _pair(d, hp, dt):
 
 
 def _run(d, hp, dt, steps, dense=False, swap_at=None):
+    """Sparse return (MA_HOST_SPARSE=1) unless dense."""
     import torch
     gen = torch.Generator(device="cuda").manual_seed(11)
     theta = torch.randn(d, generator=gen, device="cuda").to(_tdt(dt))
@@ -41,8 +41,8 @@ def _run(d, hp, dt, steps, dense=False, swap_at=None):
     p_dev = theta.clone()
     h_p = theta.cpu().pin_memory()
     h_g = torch.empty(d, dtype=_tdt(dt)).pin_memory()
-    if dense:
-        os.environ["MA_HOST_DENSE"] = "1"
+    if not dense:
+        os.environ["MA_HOST_SPARSE"] = "1"
     try:
         for s in range(steps):
             g = (torch.randn(d, generator=gen, device="cuda") * (1 + s)).to(_tdt(dt))
@@ -55,7 +55,7 @@ def _run(d, hp, dt, steps, dense=False, swap_at=None):
             iv = {"bf16": torch.int16, "f32": torch.int32, "f64": torch.int64}[dt]
             assert torch.equal(h_p.view(iv), p_dev.cpu().view(iv)), f"θ differs after step {s + 1}"
     finally:
-        os.environ.pop("MA_HOST_DENSE", None)
+        os.environ.pop("MA_HOST_SPARSE", None)
     assert np.array_equal(dev.error_buffer().codes, host.error_buffer().codes)
     assert np.array_equal(dev.window().indices, host.window().indices)
 
@@ -72,7 +72,7 @@ def test_step_host_f64_and_wide_window():
     _run(300 * BLK + 77, dict(lr=1e-2, window=10, density=0.02), "f64", steps=12)
 
 
-def test_step_host_dense_return_env():
+def test_step_host_dense_return_default():
     _run(9000 * BLK, dict(lr=1e-3, window=4), "bf16", steps=6, dense=True)
 
 
