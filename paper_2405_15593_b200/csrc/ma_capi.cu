@@ -193,6 +193,7 @@ struct ma_handle {
     uint32_t* g_hist = nullptr;
     int2* g_cnt = nullptr;
     int2* g_selinfo = nullptr;
+    unsigned long long* g_selstate = nullptr;
     double* g_z = nullptr;
     double* d_dense = nullptr;  // lossless error feedback (fp64 residual, dim elements)
     // host counters (window.hpp:10-33)
@@ -254,6 +255,7 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_hist);
     cudaFree(h->g_cnt);
     cudaFree(h->g_selinfo);
+    cudaFree(h->g_selstate);
     cudaFree(h->g_z);
     cudaFree(h->d_dense);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
@@ -386,6 +388,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.hist = h->g_hist;
     g.cnt = h->g_cnt;
     g.sel_info = h->g_selinfo;
+    g.sel_state = h->g_selstate;
     g.z1 = h->g_z;
     g.z2 = h->g_z + s.dim;
     g.partials = report ? h->d_partials : nullptr;
@@ -407,51 +410,24 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.scale1 = a.scale1;
     g.scale2 = a.scale2;
     MA_CUDA(ma::g_launch_levels(g, st));
-    // exact k-th largest key: 11-bit digits from bit 62 down, then 8 bits
-    static const int kShift[6] = {52, 41, 30, 19, 8, 0};
-    uint64_t prefix = 0, pmask = 0;
-    int64_t need = s.per_block_k;
-    std::vector<uint32_t> hist(2048);
-    for (int pass = 0; pass < 6; ++pass) {
-        const int shift = kShift[pass], nbins = pass == 5 ? 256 : 2048;
-        MA_CUDA(ma::g_launch_hist(g, shift, nbins, prefix, pmask, st));
-        MA_CUDA(cudaMemcpyAsync(hist.data(), h->g_hist, size_t(nbins) * 4, cudaMemcpyDeviceToHost, st));
-        MA_CUDA(cudaStreamSynchronize(st));
-        int64_t above = 0;
-        int d = nbins - 1;
-        for (; d > 0; --d) {
-            if (above + int64_t(hist[size_t(d)]) >= need) break;
-            above += hist[size_t(d)];
-        }
-        need -= above;
-        prefix |= uint64_t(d) << shift;
-        pmask |= uint64_t(nbins - 1) << shift;
-        h->launches += 1;
-    }
-    g.kstar = prefix;  // the k-th largest key; `need` of its ties are selected
-    const int64_t nch = ma::global_chunks(s.dim);
+    // G1-G2 entirely on the device: the six radix digits are picked by a
+    // one-warp kernel after each histogram, row offsets / ties per chunk by a
+    // one-CTA scan — the step never waits for the host.
+    MA_CUDA(ma::g_launch_select(g, st));
     MA_CUDA(ma::g_launch_count(g, st));
-    std::vector<int2> cnt(static_cast<size_t>(nch)), info(static_cast<size_t>(nch));
-    MA_CUDA(cudaMemcpyAsync(cnt.data(), h->g_cnt, cnt.size() * sizeof(int2), cudaMemcpyDeviceToHost, st));
-    MA_CUDA(cudaStreamSynchronize(st));
-    int64_t off = 0, ties = need;
-    for (int64_t c = 0; c < nch; ++c) {  // ties go to the lowest indices (compress.cpp:43-48)
-        const int64_t take = std::min<int64_t>(ties, cnt[size_t(c)].y);
-        info[size_t(c)] = make_int2(int(off), int(take));
-        off += cnt[size_t(c)].x + take;
-        ties -= take;
-    }
-    if (off != s.per_block_k) return fail(MA_ERR_CUDA, "global select: row count mismatch");
-    MA_CUDA(cudaMemcpyAsync(h->g_selinfo, info.data(), info.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    h->launches += 14;
     MA_CUDA(ma::g_launch_emit(g, st));
     MA_CUDA(ma::g_launch_requant(g, st));
+    // Dense accumulators: at ~10% window coverage the sequential memset + dense
+    // update (0.8 ms at 110M) beat walking the window entries with a claim bit
+    // and clearing them again (1.7 ms: scattered 8-byte accesses, L2 atomics).
     MA_CUDA(cudaMemsetAsync(h->g_z, 0, size_t(s.dim) * 2 * sizeof(double), st));
     for (int64_t r = 0; r < h->filled; ++r) MA_CUDA(ma::g_launch_stats_row(g, int(r), a.w1[r], a.w2[r], st));
     MA_CUDA(ma::g_launch_update(g, st));
     h->launches += 5 + h->filled;
     h->last_stream = st;
     if (report) {
-        MA_CUDA(ma::launch_report_reduce(h->d_partials, nch, h->d_report, st));
+        MA_CUDA(ma::launch_report_reduce(h->d_partials, ma::global_chunks(s.dim), h->d_report, st));
         ++h->launches;
         double r[ma::kReportFields];
         MA_CUDA(cudaMemcpyAsync(r, h->d_report, sizeof(r), cudaMemcpyDeviceToHost, st));
@@ -610,6 +586,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         alloc(reinterpret_cast<void**>(&h->g_hist), 2048 * sizeof(uint32_t));
         alloc(reinterpret_cast<void**>(&h->g_cnt), size_t(nch) * sizeof(int2));
         alloc(reinterpret_cast<void**>(&h->g_selinfo), size_t(nch) * sizeof(int2));
+        alloc(reinterpret_cast<void**>(&h->g_selstate), 4 * sizeof(unsigned long long));
         alloc(reinterpret_cast<void**>(&h->g_z), size_t(s.dim) * 2 * sizeof(double));
     }
     alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));

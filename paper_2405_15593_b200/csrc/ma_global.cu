@@ -5,12 +5,15 @@
 // reference's fp64 arithmetic (a = g + (c·level + lo), optim.cpp:166-168,
 // quantize.cpp:164-178):
 //   G0  per-bucket level = (hi - lo) / 15 of the current EF (quantize.cpp:7-13)
-//   G1  radix histograms of the 63-bit |a| keys, six digit passes driven from
-//       the host (11-bit digits, then 8): the exact k-th key K* and how many
-//       ties at K* the selection takes (compress.cpp:39-53: |a| desc, idx asc)
-//   G2  per 4096-chunk counts of keys > K* and == K*
+//   G1  radix histograms of the 63-bit |a| keys, six digit passes (11-bit
+//       digits, then 8), each digit picked on the device by one warp: the
+//       exact k-th key K* and how many ties at K* the selection takes
+//       (compress.cpp:39-53: |a| desc, idx asc)
+//   G2  per 4096-chunk counts of keys > K* and == K*, then one CTA scans them
+//       into row offsets and ties per chunk (lowest indices first)
 //   G3  emit: the selected entries in ascending index order at their global
-//       row positions (host prefix sums of G2), the selection bitmap
+//       row positions, the selection bitmap
+// No host synchronisation inside the step.
 //   G4  residual (compress.cpp:95-102) + bucket min/max + 4-bit codes by the
 //       IEEE quotient (quantize.cpp:15-24, 42-55, 102-114), StepReport sums
 //   G5  ADAM_STATS as window.cpp:28-46 does it: dense z1/z2 accumulated row by
@@ -18,6 +21,7 @@
 //       within a row), then
 //   G6  the update θ -= lr · mhat / (eps + sqrt(vhat)) (optim.cpp:183-187) for
 //       every coordinate with a nonzero accumulator (u = 0 elsewhere).
+// Passes over d read the gradient and codes 8 elements per thread (g_a8).
 // Window rows: int32 global indices [m][row stride] + values.
 #include <math_constants.h>
 
@@ -42,6 +46,53 @@ __device__ __forceinline__ double g_a(const GlobalArgs& p, int64_t i) {
     return __dadd_rn(ld_val(p.grads, p.g_dtype, i), e);
 }
 
+// a at the 8 consecutive elements [i0, i0 + 8) (i0 % 8 == 0), same arithmetic
+// as g_a; entries at or past dim are 0 and `nv` says how many are valid. One
+// 16-byte gradient load (bf16), one 4-byte code word and one bucket grid when
+// the bucket holds the whole group.
+__device__ __forceinline__ int g_a8(const GlobalArgs& p, int64_t i0, double (&a)[8]) {
+    const int nv = p.dim - i0 >= 8 ? 8 : static_cast<int>(p.dim - i0);
+    const bool vec = nv == 8 && p.bucket_shift >= 3 &&
+                     (reinterpret_cast<uintptr_t>(p.grads) & 15u) == 0;
+    if (!vec) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a[e] = e < nv ? g_a(p, i0 + e) : 0.0;
+        return nv;
+    }
+    const int64_t q = i0 >> p.bucket_shift;
+    const double lo = p.meta[q].x, lv = p.level[q];
+    const uint32_t cw = *reinterpret_cast<const uint32_t*>(p.codes + (i0 >> 1));
+    double g[8];
+    if (p.g_dtype == BF16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(p.grads) + i0);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            g[2 * k] = static_cast<double>(__uint_as_float(w[k] << 16));
+            g[2 * k + 1] = static_cast<double>(__uint_as_float(w[k] & 0xFFFF0000u));
+        }
+    } else if (p.g_dtype == F32) {
+        const float4* f = reinterpret_cast<const float4*>(static_cast<const float*>(p.grads) + i0);
+        const float4 x = f[0], y = f[1];
+        g[0] = x.x; g[1] = x.y; g[2] = x.z; g[3] = x.w;
+        g[4] = y.x; g[5] = y.y; g[6] = y.z; g[7] = y.w;
+    } else {
+        const double2* d2 = reinterpret_cast<const double2*>(static_cast<const double*>(p.grads) + i0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 t = d2[k];
+            g[2 * k] = t.x;
+            g[2 * k + 1] = t.y;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const double c = static_cast<double>((cw >> (4 * e)) & 15u);
+        a[e] = __dadd_rn(g[e], __dadd_rn(__dmul_rn(c, lv), lo));
+    }
+    return 8;
+}
+
 __global__ void g_levels(GlobalArgs p) {
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < p.nbuckets;
          q += int64_t(gridDim.x) * blockDim.x) {
@@ -52,21 +103,35 @@ __global__ void g_levels(GlobalArgs p) {
 
 // One radix digit: histogram of (key >> shift) & (nbins - 1) over keys whose
 // bits above the digit equal `prefix` (under `pmask`).
-__global__ void g_hist(GlobalArgs p, int shift, int nbins, uint64_t prefix, uint64_t pmask) {
+__global__ void g_hist(GlobalArgs p, int shift, int nbins) {
     __shared__ uint32_t h[2048];
+    const uint64_t prefix = p.sel_state[0], pmask = p.sel_state[1];
     for (int i = threadIdx.x; i < nbins; i += blockDim.x) h[i] = 0;
     __syncthreads();
     bool bad = false;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < p.dim;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const uint64_t k = key_of(g_a(p, i));
-        bad |= (k >> 52) >= 0x7FFu;  // inf / NaN (check_finite in topk_global)
-        const bool in = (k & pmask) == prefix;
-        const int bin = in ? static_cast<int>((k >> shift) & uint64_t(nbins - 1)) : -1;
-        // one atomic per distinct bin per warp (keys crowd a few exponent bins)
+    const int64_t ngroups = (p.dim + 7) / 8;
+    for (int64_t gi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; gi < ngroups;
+         gi += int64_t(gridDim.x) * blockDim.x) {
+        double a[8];
+        const int nv = g_a8(p, gi * 8, a);
         const unsigned act = __activemask();
-        const unsigned peers = __match_any_sync(act, bin);
-        if (in && (__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&h[bin], __popc(peers));
+        uint32_t inm = 0;
+        int bins[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint64_t k = key_of(a[e]);
+            bad |= e < nv && (k >> 52) >= 0x7FFu;  // inf / NaN (check_finite in topk_global)
+            const bool in = e < nv && (k & pmask) == prefix;
+            bins[e] = in ? static_cast<int>((k >> shift) & uint64_t(nbins - 1)) : -1;
+            inm |= static_cast<uint32_t>(in) << e;
+        }
+        if (!__any_sync(act, inm != 0)) continue;  // later digits: few keys share the prefix
+        // one atomic per distinct bin per warp (keys crowd a few exponent bins)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const unsigned peers = __match_any_sync(act, bins[e]);
+            if (bins[e] >= 0 && (__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&h[bins[e]], __popc(peers));
+        }
     }
     if (bad && p.check_finite) atomicOr(p.flag, 1u);
     __syncthreads();
@@ -105,12 +170,18 @@ __global__ void g_count(GlobalArgs p) {
     __shared__ int s_tmp[33];
     const int64_t c0 = int64_t(blockIdx.x) * kChunk;
     int gt = 0, eq = 0;
-    for (int j = 0; j < kPer; ++j) {
-        const int64_t i = c0 + j * kThreads + threadIdx.x;
-        if (i >= p.dim) break;
-        const uint64_t k = key_of(g_a(p, i));
-        gt += k > p.kstar;
-        eq += k == p.kstar;
+    const uint64_t kstar = p.sel_state[0];
+    const int64_t e0 = c0 + int64_t(threadIdx.x) * kPer;
+    for (int h = 0; h < kPer / 8; ++h) {
+        if (e0 + 8 * h >= p.dim) break;
+        double a[8];
+        const int nv = g_a8(p, e0 + 8 * h, a);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint64_t k = key_of(a[e]);
+            gt += e < nv && k > kstar;
+            eq += e < nv && k == kstar;
+        }
     }
     int tg, te;
     cta_excl_scan(gt, s_tmp, tg);
@@ -126,15 +197,20 @@ __global__ void g_emit(GlobalArgs p) {
     const int64_t e0 = c0 + int64_t(threadIdx.x) * kPer;
     const int2 cs = p.sel_info[blockIdx.x];  // (row offset, ties to take in this chunk)
     uint32_t gtm = 0, eqm = 0;
+    const uint64_t kstar = p.sel_state[0];
     double av[kPer];
-    for (int j = 0; j < kPer; ++j) {
-        av[j] = 0.0;
-        const int64_t i = e0 + j;
-        if (i >= p.dim) continue;
-        av[j] = g_a(p, i);
-        const uint64_t k = key_of(av[j]);
-        gtm |= static_cast<uint32_t>(k > p.kstar) << j;
-        eqm |= static_cast<uint32_t>(k == p.kstar) << j;
+#pragma unroll
+    for (int h = 0; h < kPer / 8; ++h) {
+        double a8[8];
+        const int nv = e0 + 8 * h < p.dim ? g_a8(p, e0 + 8 * h, a8) : 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int j = 8 * h + e;
+            av[j] = e < nv ? a8[e] : 0.0;
+            const uint64_t k = key_of(av[j]);
+            gtm |= static_cast<uint32_t>(e < nv && k > kstar) << j;
+            eqm |= static_cast<uint32_t>(e < nv && k == kstar) << j;
+        }
     }
     int te;
     int tie_before = cta_excl_scan(__popc(eqm), s_tmp, te);
@@ -163,25 +239,33 @@ __global__ void g_requant(GlobalArgs p) {
     const int64_t c0 = int64_t(blockIdx.x) * kChunk;
     const int n = static_cast<int>(p.dim - c0 < kChunk ? p.dim - c0 : kChunk);
     double rep[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int j = threadIdx.x; j < n; j += kThreads) {
-        const int64_t i = c0 + j;
-        const double a = g_a(p, i);
-        const bool sel = (p.selbits[i / kPer] >> (i % kPer)) & 1u;
-        const double r = sel ? 0.0 : a;
-        s_a[j] = r;
-        if (p.partials) {
-            const double g = ld_val(p.grads, p.g_dtype, i);
-            rep[0] += g * g;
-            rep[1] += a * a;
-            rep[2] += r * r;
+    for (int j0 = 8 * threadIdx.x; j0 < n; j0 += 8 * kThreads) {
+        double a8[8];
+        const int64_t i0 = c0 + j0;
+        const int nv = g_a8(p, i0, a8);
+        const uint32_t sw = (p.selbits[i0 / kPer] >> (i0 % kPer)) & 0xFFu;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if (e >= nv) break;
+            const double a = a8[e];
+            const double r = ((sw >> e) & 1u) ? 0.0 : a;
+            s_a[j0 + e] = r;
+            if (p.partials) {
+                const double g = ld_val(p.grads, p.g_dtype, i0 + e);
+                rep[0] += g * g;
+                rep[1] += a * a;
+                rep[2] += r * r;
+            }
         }
     }
     __syncthreads();
     // buckets inside this chunk (kChunk % bucket == 0): 8 threads per bucket
     // reduce (lo, hi) (quant_params, quantize.cpp:15-24), one writes the grid
     const int B = static_cast<int>(p.bucket);
+    const int nqmax = kChunk >> p.bucket_shift;  // buckets per chunk (bucket | 4096)
     double* s_lo = reinterpret_cast<double*>(s_a + kChunk);
-    double* s_lv = s_lo + kChunk / 1;  // room for up to kChunk buckets
+    double* s_lv = s_lo + nqmax;
+    double* s_ri = s_lv + nqmax;  // rn(1 / level) (0 when the division decides)
     const int nq = (n + B - 1) / B;
     for (int q0 = threadIdx.x / 8; q0 < ((nq + 31) / 32) * 32; q0 += kThreads / 8) {
         const int q = q0, sub = threadIdx.x & 7;
@@ -211,7 +295,9 @@ __global__ void g_requant(GlobalArgs p) {
         if (q < nq && sub == 0) {
             p.meta[(c0 >> p.bucket_shift) + q] = make_double2(lo, hi);
             s_lo[q] = lo;
-            s_lv[q] = lo == hi ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+            const double lv = lo == hi ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+            s_lv[q] = lv;
+            s_ri[q] = lv >= 0x1p-1000 ? __drcp_rn(lv) : 0.0;
         }
     }
     __syncthreads();
@@ -228,10 +314,10 @@ __global__ void g_requant(GlobalArgs p) {
             uint32_t c = 0;
             if (level != 0.0) {
                 const double d = __dsub_rn(s_a[j], s_lo[q]);
-                const bool fast = level >= 0x1p-1000;
+                const double ri = s_ri[q];
                 double f = 0.0;
-                if (fast) {
-                    const double t = __dadd_rn(__dmul_rn(d, __drcp_rn(level)), 0.5);
+                if (ri != 0.0) {
+                    const double t = __dadd_rn(__dmul_rn(d, ri), 0.5);
                     f = floor(t);
                     const double fr = __dsub_rn(t, f);
                     if (fr < 1e-12 || fr > 1.0 - 1e-12) f = floor(__dadd_rn(__ddiv_rn(d, level), 0.5));
@@ -307,6 +393,82 @@ __global__ void g_update(GlobalArgs p) {
     }
 }
 
+// Radix select state: no key prefix yet, k entries still to place.
+__global__ void g_sel_init(GlobalArgs p) {
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) p.hist[i] = 0;
+    if (threadIdx.x == 0) {
+        p.sel_state[0] = 0;
+        p.sel_state[1] = 0;
+        p.sel_state[2] = static_cast<unsigned long long>(p.k);
+    }
+}
+
+// After one digit's histogram: the digit of the k-th largest key is the
+// highest bin d with (keys in bins > d) < need <= (keys in bins >= d) (bin 0
+// takes the rest); need drops by the keys above it. One warp walks the bins
+// from the top 32 at a time; the histogram is cleared for the next digit.
+__global__ void g_pick(GlobalArgs p, int shift, int nbins) {
+    const int lane = threadIdx.x;
+    const unsigned long long need = p.sel_state[2];
+    unsigned long long above = 0;
+    int d = 0;
+    for (int top = nbins - 1; top > 0; top -= 32) {
+        const int bin = top - lane;
+        const unsigned long long c = bin > 0 ? p.hist[bin] : 0ull;
+        unsigned long long incl = c;  // inclusive sum over lanes 0..lane (bins top..bin)
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+            if (lane >= off) incl += t;
+        }
+        const unsigned hit = __ballot_sync(0xFFFFFFFFu, bin > 0 && above + incl >= need);
+        if (hit) {
+            const int l = __ffs(hit) - 1;
+            d = top - l;
+            above += __shfl_sync(0xFFFFFFFFu, incl - c, l);
+            break;
+        }
+        above += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        p.sel_state[0] |= static_cast<unsigned long long>(d) << shift;
+        p.sel_state[1] |= static_cast<unsigned long long>(nbins - 1) << shift;
+        p.sel_state[2] = need - above;
+    }
+    for (int i = lane; i < nbins; i += 32) p.hist[i] = 0;
+}
+
+// Row offsets and ties per chunk from the (> K*, == K*) counts: ties go to the
+// lowest indices (compress.cpp:43-48), entries in ascending index order. One
+// CTA scans the chunks 1024 at a time.
+__global__ void g_alloc(GlobalArgs p, int64_t nch) {
+    __shared__ int s_tmp[33];
+    __shared__ long long s_carry[2];
+    if (threadIdx.x == 0) {
+        s_carry[0] = 0;  // row offset
+        s_carry[1] = 0;  // ties at K* in earlier chunks
+    }
+    __syncthreads();
+    const long long ties = static_cast<long long>(p.sel_state[2]);
+    for (int64_t c0 = 0; c0 < nch; c0 += kThreads) {
+        const int64_t c = c0 + threadIdx.x;
+        const int2 cnt = c < nch ? p.cnt[c] : make_int2(0, 0);
+        int tot_eq;
+        const long long eq_before = s_carry[1] + cta_excl_scan(cnt.y, s_tmp, tot_eq);
+        long long take = ties - eq_before;
+        take = take < 0 ? 0 : (take > cnt.y ? cnt.y : take);
+        int tot_n;
+        const long long off = s_carry[0] + cta_excl_scan(cnt.x + static_cast<int>(take), s_tmp, tot_n);
+        if (c < nch) p.sel_info[c] = make_int2(static_cast<int>(off), static_cast<int>(take));
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_carry[0] += tot_n;
+            s_carry[1] += tot_eq;
+        }
+        __syncthreads();
+    }
+}
+
 unsigned grid_for(int64_t n, int per) {
     const int64_t want = (n + per - 1) / per;
     return static_cast<unsigned>(want < 148 * 16 ? (want > 0 ? want : 1) : 148 * 16);
@@ -317,8 +479,8 @@ unsigned grid_for(int64_t n, int per) {
 int64_t global_chunks(int64_t dim) { return (dim + kChunk - 1) / kChunk; }
 
 size_t global_requant_smem(int64_t bucket) {
-    (void)bucket;
-    return size_t(kChunk) * 8 * 3;  // residuals + per-bucket lo + level (up to kChunk buckets)
+    // residuals + per-bucket lo, level, 1/level
+    return size_t(kChunk) * 8 + 3 * size_t(kChunk / (bucket < kChunk ? bucket : kChunk)) * 8;
 }
 
 cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s) {
@@ -326,16 +488,24 @@ cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t g_launch_hist(const GlobalArgs& a, int shift, int nbins, uint64_t prefix, uint64_t pmask,
-                          cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(a.hist, 0, 2048 * sizeof(uint32_t), s);
-    if (e != cudaSuccess) return e;
-    g_hist<<<grid_for(a.dim, 256 * 16), 256, 0, s>>>(a, shift, nbins, prefix, pmask);
+// G1 (compress.cpp:39-53 over the whole vector): the exact k-th largest |a|
+// key K* and how many of its ties to take, 11-bit digits from bit 62 down,
+// then 8 bits, each digit picked on the device (no host round trip).
+cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
+    static const int kShift[6] = {52, 41, 30, 19, 8, 0};
+    g_sel_init<<<1, 256, 0, s>>>(a);
+    for (int pass = 0; pass < 6; ++pass) {
+        const int nbins = pass == 5 ? 256 : 2048;
+        g_hist<<<grid_for(a.dim, 256 * 16), 256, 0, s>>>(a, kShift[pass], nbins);
+        g_pick<<<1, 32, 0, s>>>(a, kShift[pass], nbins);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s) {
-    g_count<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, 0, s>>>(a);
+    const int64_t nch = global_chunks(a.dim);
+    g_count<<<static_cast<unsigned>(nch), kThreads, 0, s>>>(a);
+    g_alloc<<<1, kThreads, 0, s>>>(a, nch);
     return cudaGetLastError();
 }
 

@@ -75,22 +75,21 @@ struct GlobalArgs {
     uint16_t* selbits;   // selection bits, 16 elements per word
     uint32_t* hist;      // [2048] radix histogram
     int2* cnt;           // [chunks] (keys > K*, keys == K*)
-    const int2* sel_info;  // [chunks] (row offset, ties taken)
+    int2* sel_info;        // [chunks] (row offset, ties taken)
+    unsigned long long* sel_state;  // radix select on device: [0] key prefix (K* at the end), [1] mask, [2] ties left
     double* z1;
     double* z2;
     double* partials;    // nullable: [chunks][kReportFields]
     unsigned int* flag;
     int64_t dim, nbuckets, bucket, k, row_stride;
-    uint64_t kstar;
     int32_t slot, g_dtype, p_dtype, v_dtype, check_finite, bucket_shift;
     double eps, lr, scale1, scale2;
 };
 int64_t global_chunks(int64_t dim);
 size_t global_requant_smem(int64_t bucket);
 cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s);
-cudaError_t g_launch_hist(const GlobalArgs& a, int shift, int nbins, uint64_t prefix, uint64_t pmask,
-                          cudaStream_t s);
-cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s);
+cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s);  // G1: six digit passes, no host sync
+cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s);  // G2 + row offsets / ties per chunk
 cudaError_t g_launch_emit(const GlobalArgs& a, cudaStream_t s);
 cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s);
 cudaError_t g_launch_stats_row(const GlobalArgs& a, int r, double w1, double w2, cudaStream_t s);
