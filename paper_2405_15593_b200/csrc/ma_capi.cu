@@ -194,7 +194,7 @@ struct ma_handle {
     int2* g_cnt = nullptr;
     int2* g_selinfo = nullptr;
     unsigned long long* g_selstate = nullptr;
-    double* g_z = nullptr;
+    int32_t* g_bounds = nullptr;
     double* d_dense = nullptr;  // lossless error feedback (fp64 residual, dim elements)
     // host counters (window.hpp:10-33)
     int64_t step = 0, head = 0, filled = 0;
@@ -256,7 +256,7 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_cnt);
     cudaFree(h->g_selinfo);
     cudaFree(h->g_selstate);
-    cudaFree(h->g_z);
+    cudaFree(h->g_bounds);
     cudaFree(h->d_dense);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
     delete h->pending;
@@ -389,8 +389,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.cnt = h->g_cnt;
     g.sel_info = h->g_selinfo;
     g.sel_state = h->g_selstate;
-    g.z1 = h->g_z;
-    g.z2 = h->g_z + s.dim;
+    g.bounds = h->g_bounds;
     g.partials = report ? h->d_partials : nullptr;
     g.flag = h->d_flag;
     g.dim = s.dim;
@@ -418,13 +417,13 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     h->launches += 14;
     MA_CUDA(ma::g_launch_emit(g, st));
     MA_CUDA(ma::g_launch_requant(g, st));
-    // Dense accumulators: at ~10% window coverage the sequential memset + dense
-    // update (0.8 ms at 110M) beat walking the window entries with a claim bit
-    // and clearing them again (1.7 ms: scattered 8-byte accesses, L2 atomics).
-    MA_CUDA(cudaMemsetAsync(h->g_z, 0, size_t(s.dim) * 2 * sizeof(double), st));
-    for (int64_t r = 0; r < h->filled; ++r) MA_CUDA(ma::g_launch_stats_row(g, int(r), a.w1[r], a.w2[r], st));
-    MA_CUDA(ma::g_launch_update(g, st));
-    h->launches += 5 + h->filled;
+    ma::GWeights w;
+    for (int64_t r = 0; r < h->filled; ++r) {
+        w.w1[r] = a.w1[r];
+        w.w2[r] = a.w2[r];
+    }
+    MA_CUDA(ma::g_launch_stats_update(g, w, int(h->filled), st));
+    h->launches += 5;
     h->last_stream = st;
     if (report) {
         MA_CUDA(ma::launch_report_reduce(h->d_partials, ma::global_chunks(s.dim), h->d_report, st));
@@ -587,7 +586,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         alloc(reinterpret_cast<void**>(&h->g_cnt), size_t(nch) * sizeof(int2));
         alloc(reinterpret_cast<void**>(&h->g_selinfo), size_t(nch) * sizeof(int2));
         alloc(reinterpret_cast<void**>(&h->g_selstate), 4 * sizeof(unsigned long long));
-        alloc(reinterpret_cast<void**>(&h->g_z), size_t(s.dim) * 2 * sizeof(double));
+        alloc(reinterpret_cast<void**>(&h->g_bounds), size_t(cfg->hp.window) * size_t(nch + 1) * sizeof(int32_t));
     }
     alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));
     alloc(reinterpret_cast<void**>(&h->d_flag), sizeof(unsigned));

@@ -16,9 +16,9 @@
 // No host synchronisation inside the step.
 //   G4  residual (compress.cpp:95-102) + bucket min/max + 4-bit codes by the
 //       IEEE quotient (quantize.cpp:15-24, 42-55, 102-114), StepReport sums
-//   G5  ADAM_STATS as window.cpp:28-46 does it: dense z1/z2 accumulated row by
-//       row in physical slot order (one launch per row; indices are unique
-//       within a row), then
+//   G5  ADAM_STATS as window.cpp:28-46 does it, per 4096-chunk in shared
+//       memory: each row's entries of the chunk (bounds found once per step)
+//       accumulated row by row in physical slot order, then
 //   G6  the update θ -= lr · mhat / (eps + sqrt(vhat)) (optim.cpp:183-187) for
 //       every coordinate with a nonzero accumulator (u = 0 elsewhere).
 // Passes over d read the gradient and codes 8 elements per thread (g_a8).
@@ -36,6 +36,9 @@ using namespace dev;
 constexpr int kChunk = 4096;     // elements per CTA in G2/G3/G4
 constexpr int kThreads = 256;
 constexpr int kPer = kChunk / kThreads;  // 16 elements per thread (strided by 256)
+
+__device__ __forceinline__ int64_t global_chunks_d(int64_t dim) { return (dim + kChunk - 1) / kChunk; }
+constexpr int kStage = 768;   // window entries per chunk staged in shared memory by g_stats_update
 
 __device__ __forceinline__ double g_a(const GlobalArgs& p, int64_t i) {
     const int64_t q = i >> p.bucket_shift;  // bucket | 4096: a power of two
@@ -350,45 +353,130 @@ __global__ void g_requant(GlobalArgs p) {
     }
 }
 
-// z[idx] += w · v (or w · v²) for one window row (window.cpp:37-41).
-__global__ void g_stats_row(GlobalArgs p, int r, double w1, double w2) {
-    const int32_t* ri = p.win_idx + int64_t(r) * p.row_stride;
-    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < p.k;
-         j += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t idx = ri[j];
-        const double v = ld_val(p.win_val, p.v_dtype, int64_t(r) * p.row_stride + j);
-        p.z1[idx] = __dadd_rn(p.z1[idx], __dmul_rn(w1, v));
-        p.z2[idx] = __dadd_rn(p.z2[idx], __dmul_rn(w2, __dmul_rn(v, v)));
+// Window entries of each chunk: rows are ascending (the emit order, and
+// SparseSelection::validate for loaded checkpoints), so bounds[r][c] = first
+// entry j of row r with idx >= c·kChunk, for c in [0, nch]; each entry writes
+// the bounds of the chunks between its predecessor's and its own.
+__global__ void g_bounds(GlobalArgs p, int filled) {
+    const int64_t nch = global_chunks_d(p.dim);
+    const int64_t n = int64_t(filled) * p.k;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = t / p.k, j = t - r * p.k;
+        const int32_t* ri = p.win_idx + r * p.row_stride;
+        int32_t* bd = p.bounds + r * (nch + 1);
+        const int64_t c = int64_t(ri[j]) / kChunk;
+        const int64_t cp = j > 0 ? int64_t(ri[j - 1]) / kChunk : -1;
+        for (int64_t cc = cp + 1; cc <= c; ++cc) bd[cc] = static_cast<int32_t>(j);
+        if (j == p.k - 1)
+            for (int64_t cc = c + 1; cc <= nch; ++cc) bd[cc] = static_cast<int32_t>(p.k);
     }
 }
 
-// θ -= lr · (z1 s1) / (eps + sqrt(z2 s2)) where the accumulators are nonzero
-// (elsewhere u = 0 / (eps + 0) = 0 and θ is unchanged); nnz per chunk.
-__global__ void g_update(GlobalArgs p) {
+// ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) for one 4096-
+// element chunk, accumulators in shared memory: rows in physical slot order,
+// z += w·v and z += w·v² in the reference's fp64 operation order (indices are
+// unique within a row, so a row's entries add without conflicts), then θ -=
+// lr · (z1 s1) / (eps + sqrt(z2 s2)) where (z1, z2) ≠ 0 (u = 0 elsewhere);
+// update_nnz per chunk for the report. No dense accumulators in HBM.
+__global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w, int filled) {
+    extern __shared__ double s_z[];  // [kChunk] z1, [kChunk] z2, [kStage] values
     __shared__ double s_red[kThreads / 32];
-    const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+    __shared__ int s_j0[kMaxWindow], s_off[kMaxWindow + 1];
+    __shared__ int16_t s_ei[kStage];
+    double* s_z1 = s_z;
+    double* s_z2 = s_z + kChunk;
+    double* s_ev = s_z + 2 * kChunk;
+    const int64_t nch = global_chunks_d(p.dim);
+    const int64_t c = blockIdx.x, c0 = c * kChunk;
+    // every row's entry range of this chunk at once (one memory latency)
+    for (int r = threadIdx.x; r < filled; r += kThreads) {
+        const int32_t* bd = p.bounds + int64_t(r) * (nch + 1);
+        s_j0[r] = bd[c];
+        s_off[r + 1] = bd[c + 1] - bd[c];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_off[0] = 0;
+        for (int r = 0; r < filled; ++r) s_off[r + 1] += s_off[r];
+    }
+    __syncthreads();
+    const int total = s_off[filled];
     double nnz = 0.0;
-    for (int j = threadIdx.x; j < kChunk; j += kThreads) {
+    auto update = [&](int j, double z1, double z2) {  // optim.cpp:183-187
         const int64_t i = c0 + j;
-        if (i >= p.dim) break;
-        const double z1 = p.z1[i], z2 = p.z2[i];
-        if (z1 == 0.0 && z2 == 0.0) continue;
         const double mhat = __dmul_rn(z1, p.scale1);
         const double vhat = __dmul_rn(z2, p.scale2);
         const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
         if (u != 0.0) nnz += 1.0;
         const double th = ld_val(p.params, p.p_dtype, i);
         st_val(p.params, p.p_dtype, i, __dsub_rn(th, __dmul_rn(p.lr, u)));
+    };
+    if (total <= kStage) {
+        // stage the chunk's window entries (rows concatenated in slot order);
+        // only the coordinates they touch are cleared, summed and updated
+        for (int e = threadIdx.x; e < total; e += kThreads) {
+            int r = 0;
+            while (s_off[r + 1] <= e) ++r;
+            const int64_t q = int64_t(r) * p.row_stride + s_j0[r] + (e - s_off[r]);
+            const int i = static_cast<int>(p.win_idx[q] - c0);
+            s_ei[e] = static_cast<int16_t>(i);
+            s_ev[e] = ld_val(p.win_val, p.v_dtype, q);
+            s_z1[i] = 0.0;
+            s_z2[i] = 0.0;
+        }
+        __syncthreads();
+        for (int r = 0; r < filled; ++r) {
+            for (int e = s_off[r] + threadIdx.x; e < s_off[r + 1]; e += kThreads) {
+                const int i = s_ei[e];
+                const double v = s_ev[e];
+                s_z1[i] = __dadd_rn(s_z1[i], __dmul_rn(w.w1[r], v));
+                s_z2[i] = __dadd_rn(s_z2[i], __dmul_rn(w.w2[r], __dmul_rn(v, v)));
+            }
+            __syncthreads();
+        }
+        // the first entry to claim a coordinate updates it: the sign bit of z2,
+        // which the sums never set (z2 = Σ w2·v² ≥ +0)
+        for (int e = threadIdx.x; e < total; e += kThreads) {
+            const int i = s_ei[e];
+            const unsigned long long old =
+                atomicOr(reinterpret_cast<unsigned long long*>(s_z2 + i), 0x8000000000000000ull);
+            if (old >> 63) continue;
+            const double z1 = s_z1[i], z2 = __longlong_as_double(static_cast<long long>(old));
+            if (z1 == 0.0 && z2 == 0.0) continue;
+            update(i, z1, z2);
+        }
+    } else {
+        for (int j = threadIdx.x; j < kChunk; j += kThreads) {
+            s_z1[j] = 0.0;
+            s_z2[j] = 0.0;
+        }
+        __syncthreads();
+        for (int r = 0; r < filled; ++r) {
+            const int64_t rb = int64_t(r) * p.row_stride + s_j0[r];
+            for (int e = threadIdx.x; e < s_off[r + 1] - s_off[r]; e += kThreads) {
+                const int i = static_cast<int>(p.win_idx[rb + e] - c0);
+                const double v = ld_val(p.win_val, p.v_dtype, rb + e);
+                s_z1[i] = __dadd_rn(s_z1[i], __dmul_rn(w.w1[r], v));
+                s_z2[i] = __dadd_rn(s_z2[i], __dmul_rn(w.w2[r], __dmul_rn(v, v)));
+            }
+            __syncthreads();
+        }
+        for (int j = threadIdx.x; j < kChunk; j += kThreads) {
+            if (c0 + j >= p.dim) break;
+            const double z1 = s_z1[j], z2 = s_z2[j];
+            if (z1 == 0.0 && z2 == 0.0) continue;
+            update(j, z1, z2);
+        }
     }
     if (p.partials) {
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
         for (int off = 16; off > 0; off >>= 1) nnz += __shfl_xor_sync(0xFFFFFFFFu, nnz, off);
-        if (lane == 0) s_red[w] = nnz;
+        if (lane == 0) s_red[wi] = nnz;
         __syncthreads();
         if (threadIdx.x == 0) {
-            double s = 0.0;
-            for (int w2 = 0; w2 < kThreads / 32; ++w2) s += s_red[w2];
-            p.partials[int64_t(blockIdx.x) * kReportFields + 4] = s;
+            double sum = 0.0;
+            for (int w2 = 0; w2 < kThreads / 32; ++w2) sum += s_red[w2];
+            p.partials[c * kReportFields + 4] = sum;
         }
     }
 }
@@ -522,13 +610,12 @@ cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t g_launch_stats_row(const GlobalArgs& a, int r, double w1, double w2, cudaStream_t s) {
-    g_stats_row<<<grid_for(a.k, 256 * 4), 256, 0, s>>>(a, r, w1, w2);
-    return cudaGetLastError();
-}
-
-cudaError_t g_launch_update(const GlobalArgs& a, cudaStream_t s) {
-    g_update<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, 0, s>>>(a);
+cudaError_t g_launch_stats_update(const GlobalArgs& a, const GWeights& w, int filled, cudaStream_t s) {
+    g_bounds<<<grid_for(int64_t(filled) * a.k, 256 * 4), 256, 0, s>>>(a, filled);
+    const size_t smem = size_t(kChunk) * 2 * sizeof(double) + size_t(kStage) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(g_stats_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    g_stats_update<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, smem, s>>>(a, w, filled);
     return cudaGetLastError();
 }
 

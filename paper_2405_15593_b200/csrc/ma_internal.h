@@ -77,8 +77,7 @@ struct GlobalArgs {
     int2* cnt;           // [chunks] (keys > K*, keys == K*)
     int2* sel_info;        // [chunks] (row offset, ties taken)
     unsigned long long* sel_state;  // radix select on device: [0] key prefix (K* at the end), [1] mask, [2] ties left
-    double* z1;
-    double* z2;
+    int32_t* bounds;     // [m][chunks + 1] first entry of each 4096-chunk per row
     double* partials;    // nullable: [chunks][kReportFields]
     unsigned int* flag;
     int64_t dim, nbuckets, bucket, k, row_stride;
@@ -92,8 +91,11 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s);  // G1: six di
 cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s);  // G2 + row offsets / ties per chunk
 cudaError_t g_launch_emit(const GlobalArgs& a, cudaStream_t s);
 cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s);
-cudaError_t g_launch_stats_row(const GlobalArgs& a, int r, double w1, double w2, cudaStream_t s);
-cudaError_t g_launch_update(const GlobalArgs& a, cudaStream_t s);
+struct GWeights {
+    double w1[kMaxWindow];
+    double w2[kMaxWindow];
+};
+cudaError_t g_launch_stats_update(const GlobalArgs& a, const GWeights& w, int filled, cudaStream_t s);
 
 struct Variant {
     int nt;   // threads per CTA
