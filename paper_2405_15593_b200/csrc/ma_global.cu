@@ -235,6 +235,106 @@ __global__ void g_emit(GlobalArgs p) {
     if (e0 < p.dim) p.selbits[e0 / kPer] = static_cast<uint16_t>(selm);
 }
 
+// Re-quantization for 8 <= B_q <= 256 with the elements in registers: thread
+// t of a chunk holds the 8-groups t and t + 256, a bucket spans B_q / 8
+// consecutive threads (shuffle min/max), codes packed 8 to a word. Same
+// arithmetic and IEEE-quotient guard as g_requant.
+template <int LPB>
+__global__ void g_requant8(GlobalArgs p) {
+    __shared__ double s_red[kThreads / 32][4];
+    const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+    double rep[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int h = 0; h < kChunk / (8 * kThreads); ++h) {
+        const int64_t i0 = c0 + 8 * (int64_t(threadIdx.x) + int64_t(h) * kThreads);
+        double a[8];
+        const int nv = i0 < p.dim ? g_a8(p, i0, a) : 0;
+        const uint32_t sw = nv ? (p.selbits[i0 / kPer] >> (i0 % kPer)) & 0xFFu : 0u;
+        double lo = CUDART_INF, hi = -CUDART_INF;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const double r = ((sw >> e) & 1u) ? 0.0 : a[e];
+            if (p.partials && e < nv) {
+                const double g = ld_val(p.grads, p.g_dtype, i0 + e);
+                rep[0] += g * g;
+                rep[1] += a[e] * a[e];
+                rep[2] += r * r;
+            }
+            a[e] = r;
+            if (e < nv) {
+                lo = r < lo ? r : lo;
+                hi = r > hi ? r : hi;
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < LPB; off <<= 1) {
+            const double ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
+            const double oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+            lo = ol < lo ? ol : lo;
+            hi = oh > hi ? oh : hi;
+        }
+        if (nv == 0) continue;
+        // code = clamp(floor((r - lo) / level + 0.5)) (quantize.cpp:42-55): one
+        // DFMA forms 2^24 + t + 0.5 + 2^-15 with t = (r - lo) * 15 / (hi - lo)
+        // to fp32 accuracy; its low word holds the code in bits 28..31. A
+        // fraction within 2^-14 of an integer sends the group to the IEEE
+        // quotient (same bound as the blockwise lean kernel, ma_warp.cu pass 2).
+        const double rng = __dsub_rn(hi, lo);
+        uint32_t word = 0;
+        if (rng != 0.0) {
+            const float r32 = __double2float_rn(rng);
+            bool bad = true;
+            if (r32 >= 0x1p-100f && r32 <= 0x1p100f) {
+                const double k64 = static_cast<double>(__fdividef(15.0f, r32));
+                const double add = 0x1p24 + 0.5 + 0x1p-15;
+                bad = false;
+#pragma unroll
+                for (int e = 7; e >= 0; --e) {
+                    const uint32_t y = static_cast<uint32_t>(__double_as_longlong(__fma_rn(__dsub_rn(a[e], lo), k64, add)));
+                    word = __funnelshift_l(y, word, 4);
+                    bad |= e < nv && (y << 4) < (2u << 17);
+                }
+            }
+            if (bad) {
+                const double level = __ddiv_rn(rng, 15.0);
+                word = 0;
+                for (int e = 7; e >= 0; --e) {
+                    double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(a[e], lo), level), 0.5));
+                    f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+                    word = (word << 4) | static_cast<uint32_t>(f);
+                }
+            }
+        }
+        if (nv < 8) word &= (1u << (4 * nv)) - 1u;  // padding nibbles stay 0
+        if (p.partials) {
+            const double level = rng == 0.0 ? 0.0 : __ddiv_rn(rng, 15.0);
+            for (int e = 0; e < nv; ++e) {
+                const double en = __dadd_rn(__dmul_rn(static_cast<double>((word >> (4 * e)) & 15u), level), lo);
+                rep[3] += en * en;
+            }
+        }
+        if (nv == 8) {
+            *reinterpret_cast<uint32_t*>(p.codes + (i0 >> 1)) = word;
+        } else {
+            for (int b = 0; 2 * b < nv; ++b) p.codes[(i0 >> 1) + b] = static_cast<uint8_t>(word >> (8 * b));
+        }
+        if ((threadIdx.x & (LPB - 1)) == 0) p.meta[i0 >> p.bucket_shift] = make_double2(lo, hi);
+    }
+    if (p.partials) {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int f = 0; f < 4; ++f) {
+            for (int off = 16; off > 0; off >>= 1) rep[f] += __shfl_xor_sync(0xFFFFFFFFu, rep[f], off);
+            if (lane == 0) s_red[w][f] = rep[f];
+        }
+        __syncthreads();
+        if (threadIdx.x < 4) {
+            double sum = 0.0;
+            for (int w2 = 0; w2 < kThreads / 32; ++w2) sum += s_red[w2][threadIdx.x];
+            p.partials[int64_t(blockIdx.x) * kReportFields + threadIdx.x] = sum;
+        }
+    }
+}
+
 // Residual, bucket (lo, hi), 4-bit codes by the IEEE quotient; report sums.
 __global__ void g_requant(GlobalArgs p) {
     extern __shared__ double s_a[];  // kChunk residuals
@@ -603,6 +703,16 @@ cudaError_t g_launch_emit(const GlobalArgs& a, cudaStream_t s) {
 }
 
 cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s) {
+    const unsigned nch = static_cast<unsigned>(global_chunks(a.dim));
+    switch (a.bucket) {  // the register path for 8 <= B_q <= 256
+        case 8: g_requant8<1><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
+        case 16: g_requant8<2><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
+        case 32: g_requant8<4><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
+        case 64: g_requant8<8><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
+        case 128: g_requant8<16><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
+        case 256: g_requant8<32><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
+        default: break;
+    }
     const size_t smem = global_requant_smem(a.bucket);
     cudaError_t e = cudaFuncSetAttribute(g_requant, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
