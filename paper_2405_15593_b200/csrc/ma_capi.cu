@@ -194,6 +194,8 @@ struct ma_handle {
     int2* g_cnt = nullptr;
     int2* g_selinfo = nullptr;
     unsigned long long* g_selstate = nullptr;
+    uint64_t* g_cand = nullptr;
+    unsigned cand_cap = 0;
     int32_t* g_bounds = nullptr;
     double* d_dense = nullptr;  // lossless error feedback (fp64 residual, dim elements)
     // host counters (window.hpp:10-33)
@@ -256,12 +258,15 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_cnt);
     cudaFree(h->g_selinfo);
     cudaFree(h->g_selstate);
+    cudaFree(h->g_cand);
     cudaFree(h->g_bounds);
     cudaFree(h->d_dense);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
     delete h->pending;
     delete h;
 }
+
+constexpr unsigned kGlobalCandCap = 1u << 20;  // global radix select: keys kept after three digits
 
 // Advance the host counters exactly like GradientWindow::push (window.cpp:14-26)
 // and build the kernel weights like adam_stats (window.cpp:28-46).
@@ -389,6 +394,9 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.cnt = h->g_cnt;
     g.sel_info = h->g_selinfo;
     g.sel_state = h->g_selstate;
+    g.cand = h->g_cand;
+    g.cand_n = reinterpret_cast<unsigned int*>(h->g_selstate + 3);
+    g.cand_cap = h->cand_cap;
     g.bounds = h->g_bounds;
     g.partials = report ? h->d_partials : nullptr;
     g.flag = h->d_flag;
@@ -586,6 +594,10 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         alloc(reinterpret_cast<void**>(&h->g_cnt), size_t(nch) * sizeof(int2));
         alloc(reinterpret_cast<void**>(&h->g_selinfo), size_t(nch) * sizeof(int2));
         alloc(reinterpret_cast<void**>(&h->g_selstate), 4 * sizeof(unsigned long long));
+        // MA_GLOBAL_CAND_CAP (tests): a small capacity forces the overflow path
+        const char* cc = std::getenv("MA_GLOBAL_CAND_CAP");
+        h->cand_cap = cc ? static_cast<unsigned>(std::strtoul(cc, nullptr, 10)) : kGlobalCandCap;
+        alloc(reinterpret_cast<void**>(&h->g_cand), size_t(h->cand_cap) * sizeof(uint64_t));
         alloc(reinterpret_cast<void**>(&h->g_bounds), size_t(cfg->hp.window) * size_t(nch + 1) * sizeof(int32_t));
     }
     alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));

@@ -106,9 +106,13 @@ __global__ void g_levels(GlobalArgs p) {
 
 // One radix digit: histogram of (key >> shift) & (nbins - 1) over keys whose
 // bits above the digit equal `prefix` (under `pmask`).
-__global__ void g_hist(GlobalArgs p, int shift, int nbins) {
+// collect: also append the keys that share the prefix (the candidates of the
+// remaining digits) to p.cand; from_cand: passes after the collecting one read
+// p.cand instead of re-decoding the vector, unless it overflowed.
+__global__ void g_hist(GlobalArgs p, int shift, int nbins, int collect, int from_cand) {
     __shared__ uint32_t h[2048];
     const uint64_t prefix = p.sel_state[0], pmask = p.sel_state[1];
+    if (from_cand && *p.cand_n <= p.cand_cap) return;  // g_hist_cand covers this digit
     for (int i = threadIdx.x; i < nbins; i += blockDim.x) h[i] = 0;
     __syncthreads();
     bool bad = false;
@@ -134,6 +138,26 @@ __global__ void g_hist(GlobalArgs p, int shift, int nbins) {
         for (int e = 0; e < 8; ++e) {
             const unsigned peers = __match_any_sync(act, bins[e]);
             if (bins[e] >= 0 && (__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&h[bins[e]], __popc(peers));
+        }
+        if (collect) {
+            const int n = __popc(inm);
+            int incl = n;  // warp-aggregated slot reservation
+            const int lane = threadIdx.x & 31;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(act, incl, off);
+                if (lane >= off && ((act >> (lane - off)) & 1u)) incl += t;
+            }
+            const int last = 31 - __clz(act);
+            const int tot = __shfl_sync(act, incl, last);
+            unsigned base = 0;
+            if (lane == last) base = atomicAdd(p.cand_n, static_cast<unsigned>(tot));
+            base = __shfl_sync(act, base, last) + static_cast<unsigned>(incl - n);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if ((inm >> e) & 1u) {
+                    if (base < p.cand_cap) p.cand[base] = key_of(a[e]);
+                    ++base;
+                }
         }
     }
     if (bad && p.check_finite) atomicOr(p.flag, 1u);
@@ -581,6 +605,23 @@ __global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w,
     }
 }
 
+// One digit's histogram over the collected candidate keys.
+__global__ void g_hist_cand(GlobalArgs p, int shift, int nbins) {
+    __shared__ uint32_t h[2048];
+    const unsigned n = *p.cand_n;
+    if (n > p.cand_cap) return;  // overflowed: the full pass runs instead
+    const uint64_t prefix = p.sel_state[0], pmask = p.sel_state[1];
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t k = p.cand[i];
+        if ((k & pmask) == prefix) atomicAdd(&h[(k >> shift) & uint64_t(nbins - 1)], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x)
+        if (h[i]) atomicAdd(&p.hist[i], h[i]);
+}
+
 // Radix select state: no key prefix yet, k entries still to place.
 __global__ void g_sel_init(GlobalArgs p) {
     for (int i = threadIdx.x; i < 2048; i += blockDim.x) p.hist[i] = 0;
@@ -588,6 +629,7 @@ __global__ void g_sel_init(GlobalArgs p) {
         p.sel_state[0] = 0;
         p.sel_state[1] = 0;
         p.sel_state[2] = static_cast<unsigned long long>(p.k);
+        *p.cand_n = 0;
     }
 }
 
@@ -682,9 +724,12 @@ cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s) {
 cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
     static const int kShift[6] = {52, 41, 30, 19, 8, 0};
     g_sel_init<<<1, 256, 0, s>>>(a);
+    // digit 3 collects the keys sharing the 22-bit prefix; digits 4-6 read
+    // them (a few thousand keys) instead of re-decoding d elements
     for (int pass = 0; pass < 6; ++pass) {
         const int nbins = pass == 5 ? 256 : 2048;
-        g_hist<<<grid_for(a.dim, 256 * 16), 256, 0, s>>>(a, kShift[pass], nbins);
+        g_hist<<<grid_for(a.dim, 256 * 16), 256, 0, s>>>(a, kShift[pass], nbins, pass == 2, pass > 2);
+        if (pass > 2) g_hist_cand<<<64, 256, 0, s>>>(a, kShift[pass], nbins);
         g_pick<<<1, 32, 0, s>>>(a, kShift[pass], nbins);
     }
     return cudaGetLastError();

@@ -77,6 +77,9 @@ struct GlobalArgs {
     int2* cnt;           // [chunks] (keys > K*, keys == K*)
     int2* sel_info;        // [chunks] (row offset, ties taken)
     unsigned long long* sel_state;  // radix select on device: [0] key prefix (K* at the end), [1] mask, [2] ties left
+    uint64_t* cand;       // keys sharing the prefix after three digits (cand_cap entries)
+    unsigned int* cand_n;
+    unsigned int cand_cap;
     int32_t* bounds;     // [m][chunks + 1] first entry of each 4096-chunk per row
     double* partials;    // nullable: [chunks][kReportFields]
     unsigned int* flag;

@@ -19,9 +19,15 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="
 needs_ref = pytest.mark.skipif(not oracle.reference_available(), reason="needs /root/reference")
 
 
-def _global_engine(d, hp, dt, vdt):
+def _global_engine(d, hp, dt, vdt, cand_cap=None):
+    import os
     from paper_2405_15593_b200 import MicroAdam
-    return MicroAdam(d, hp, param_dtype=dt, grad_dtype=dt, value_dtype=vdt, blockwise=False)
+    if cand_cap is not None:
+        os.environ["MA_GLOBAL_CAND_CAP"] = str(cand_cap)
+    try:
+        return MicroAdam(d, hp, param_dtype=dt, grad_dtype=dt, value_dtype=vdt, blockwise=False)
+    finally:
+        os.environ.pop("MA_GLOBAL_CAND_CAP", None)
 
 
 @needs_ref
@@ -50,14 +56,16 @@ def test_global_fp64_matches_unmodified_reference(d, hp, levels):
         assert np.array_equal(_bits(_host(p)), _bits(st.params)), f"θ @ {s}"
 
 
-@pytest.mark.parametrize("dt", ["bf16", "f32"])
-def test_global_low_precision_matches_composed_oracle(dt):
+@pytest.mark.parametrize("dt,cap", [("bf16", None), ("f32", None), ("bf16", 0), ("f32", 3)])
+def test_global_low_precision_matches_composed_oracle(dt, cap):
+    # cap: capacity of the candidate-key buffer of the radix select's last
+    # three digits; 0 / 3 force the overflow path (full passes)
     d = 30_011
     hp = dict(lr=1e-2, window=4, density=0.02)
     torch = _torch()
     th0 = _host(_dev(oracle.synth(1, 0, 0, d, dt), dt))
     orc = oracle.Oracle(th0, dict(hp, block=d), param_dtype=dt, value_dtype="bf16")
-    eng = _global_engine(d, hp, dt, "bf16")
+    eng = _global_engine(d, hp, dt, "bf16", cand_cap=cap)
     p = _dev(th0, dt)
     for s in range(1, 8):
         g = _host(_dev(oracle.synth(42, s, 0, d, dt), dt))
@@ -106,7 +114,7 @@ def test_global_mode_tie_heavy_f32():
     torch = _torch()
     th0 = _host(_dev(oracle.synth(1, 0, 0, d, "f32"), "f32"))
     orc = oracle.Oracle(th0, dict(hp, block=d), param_dtype="f32", value_dtype="f32")
-    eng = _global_engine(d, hp, "f32", "f32")
+    eng = _global_engine(d, hp, "f32", "f32", cand_cap=5)  # ties overflow the candidate buffer
     p = _dev(th0, "f32")
     for s in range(1, 6):
         g = _host(_dev(oracle.synth(5, s, 0, d, "f32", levels=True), "f32"))
