@@ -166,6 +166,7 @@ __global__ void g_hist(GlobalArgs p, int shift, int nbins, int collect, int from
         if (h[i]) atomicAdd(&p.hist[i], h[i]);
 }
 
+template <int NT = kThreads>
 __device__ __forceinline__ int cta_excl_scan(int v, int* s_tmp, int& total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int incl = v;
@@ -176,14 +177,14 @@ __device__ __forceinline__ int cta_excl_scan(int v, int* s_tmp, int& total) {
     if (lane == 31) s_tmp[w] = incl;
     __syncthreads();
     if (w == 0) {
-        int x = lane < kThreads / 32 ? s_tmp[lane] : 0;
+        int x = lane < NT / 32 ? s_tmp[lane] : 0;
         int xi = x;
         for (int off = 1; off < 32; off <<= 1) {
             const int t = __shfl_up_sync(0xFFFFFFFFu, xi, off);
             if (lane >= off) xi += t;
         }
-        if (lane < kThreads / 32) s_tmp[lane] = xi - x;
-        if (lane == kThreads / 32 - 1) s_tmp[32] = xi;
+        if (lane < NT / 32) s_tmp[lane] = xi - x;
+        if (lane == NT / 32 - 1) s_tmp[32] = xi;
     }
     __syncthreads();
     total = s_tmp[32];
@@ -671,6 +672,7 @@ __global__ void g_pick(GlobalArgs p, int shift, int nbins) {
 // Row offsets and ties per chunk from the (> K*, == K*) counts: ties go to the
 // lowest indices (compress.cpp:43-48), entries in ascending index order. One
 // CTA scans the chunks 1024 at a time.
+constexpr int kAllocThreads = 1024;
 __global__ void g_alloc(GlobalArgs p, int64_t nch) {
     __shared__ int s_tmp[33];
     __shared__ long long s_carry[2];
@@ -680,15 +682,15 @@ __global__ void g_alloc(GlobalArgs p, int64_t nch) {
     }
     __syncthreads();
     const long long ties = static_cast<long long>(p.sel_state[2]);
-    for (int64_t c0 = 0; c0 < nch; c0 += kThreads) {
+    for (int64_t c0 = 0; c0 < nch; c0 += kAllocThreads) {
         const int64_t c = c0 + threadIdx.x;
         const int2 cnt = c < nch ? p.cnt[c] : make_int2(0, 0);
         int tot_eq;
-        const long long eq_before = s_carry[1] + cta_excl_scan(cnt.y, s_tmp, tot_eq);
+        const long long eq_before = s_carry[1] + cta_excl_scan<kAllocThreads>(cnt.y, s_tmp, tot_eq);
         long long take = ties - eq_before;
         take = take < 0 ? 0 : (take > cnt.y ? cnt.y : take);
         int tot_n;
-        const long long off = s_carry[0] + cta_excl_scan(cnt.x + static_cast<int>(take), s_tmp, tot_n);
+        const long long off = s_carry[0] + cta_excl_scan<kAllocThreads>(cnt.x + static_cast<int>(take), s_tmp, tot_n);
         if (c < nch) p.sel_info[c] = make_int2(static_cast<int>(off), static_cast<int>(take));
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -738,7 +740,7 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
 cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s) {
     const int64_t nch = global_chunks(a.dim);
     g_count<<<static_cast<unsigned>(nch), kThreads, 0, s>>>(a);
-    g_alloc<<<1, kThreads, 0, s>>>(a, nch);
+    g_alloc<<<1, kAllocThreads, 0, s>>>(a, nch);
     return cudaGetLastError();
 }
 
