@@ -30,6 +30,6 @@ for arg in sys.argv[1:] or ["1.1e8"]:
         eng.step(p, gs[i % 4], 1e-3)
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t) / n * 1e3
-    print(f"global d={d:,} {ms:.3f} ms/step {d / ms / 1e6:.3e} params/s", flush=True)
+    print(f"global d={d:,} {ms:.3f} ms/step {d / ms * 1e3:.3e} params/s", flush=True)
     del eng, p, gs
     torch.cuda.empty_cache()
