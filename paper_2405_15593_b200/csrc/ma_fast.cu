@@ -18,7 +18,7 @@
 //    L2-hot re-read of g and the codes) instead of holding 32 doubles/thread.
 //  * Block Top-K: P1 keeps a 16-bit key (bits 62..48 of |a|) per element in
 //    registers. A threshold t with k_b <= #{key16 >= t} <= cap is taken from
-//    the previous step (≈ the kTarget-th largest key, carried per block) or
+//    the previous step (one 16-bit bucket below its k_b-th key, carried per block) or
 //    found by bisection on block-wide counts (SIMD __vcmpgeu2 + popc, one
 //    barrier per probe). The candidates above t are ranked exactly by
 //    (|a| desc, index asc) — high word first, full key and index only on ties
@@ -49,7 +49,6 @@ using namespace dev;
 
 constexpr int kNT = 128;          // threads per CTA
 constexpr int kEPT = 32;          // elements per thread at B_d = 4096 (fallback view)
-constexpr int kTarget = 56;       // candidate rank that seeds the next step's threshold
 constexpr uint32_t kGuard = 64;   // fixed-point guard band (units of 2^-20)
 constexpr int kMaxRowsFast = 127; // owner byte holds the row (7 bits) + a duplicate bit
 
