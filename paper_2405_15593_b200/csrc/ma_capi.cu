@@ -195,6 +195,7 @@ struct ma_handle {
     int2* g_selinfo = nullptr;
     unsigned long long* g_selstate = nullptr;
     uint64_t* g_cand = nullptr;
+    int32_t* g_ovf = nullptr;
     unsigned cand_cap = 0;
     int32_t* g_bounds = nullptr;
     double* d_dense = nullptr;  // lossless error feedback (fp64 residual, dim elements)
@@ -259,6 +260,7 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_selinfo);
     cudaFree(h->g_selstate);
     cudaFree(h->g_cand);
+    cudaFree(h->g_ovf);
     cudaFree(h->g_bounds);
     cudaFree(h->d_dense);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
@@ -397,6 +399,8 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.cand = h->g_cand;
     g.cand_n = reinterpret_cast<unsigned int*>(h->g_selstate + 3);
     g.cand_cap = h->cand_cap;
+    g.ovf_list = h->g_ovf;
+    g.ovf_n = reinterpret_cast<unsigned int*>(h->g_selstate + 4);
     g.bounds = h->g_bounds;
     g.partials = report ? h->d_partials : nullptr;
     g.flag = h->d_flag;
@@ -593,7 +597,8 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         alloc(reinterpret_cast<void**>(&h->g_hist), 2048 * sizeof(uint32_t));
         alloc(reinterpret_cast<void**>(&h->g_cnt), size_t(nch) * sizeof(int2));
         alloc(reinterpret_cast<void**>(&h->g_selinfo), size_t(nch) * sizeof(int2));
-        alloc(reinterpret_cast<void**>(&h->g_selstate), 4 * sizeof(unsigned long long));
+        alloc(reinterpret_cast<void**>(&h->g_selstate), 8 * sizeof(unsigned long long));
+        alloc(reinterpret_cast<void**>(&h->g_ovf), size_t(nch) * sizeof(int32_t));
         // MA_GLOBAL_CAND_CAP (tests): a small capacity forces the overflow path
         const char* cc = std::getenv("MA_GLOBAL_CAND_CAP");
         h->cand_cap = cc ? static_cast<unsigned>(std::strtoul(cc, nullptr, 10)) : kGlobalCandCap;

@@ -38,7 +38,7 @@ constexpr int kThreads = 256;
 constexpr int kPer = kChunk / kThreads;  // 16 elements per thread (strided by 256)
 
 __device__ __forceinline__ int64_t global_chunks_d(int64_t dim) { return (dim + kChunk - 1) / kChunk; }
-constexpr int kStage = 768;   // window entries per chunk staged in shared memory by g_stats_update
+constexpr int kStage = 2048;  // window entries per chunk staged in shared memory by g_stats_update
 
 __device__ __forceinline__ double g_a(const GlobalArgs& p, int64_t i) {
     const int64_t q = i >> p.bucket_shift;  // bucket | 4096: a power of two
@@ -497,24 +497,11 @@ __global__ void g_bounds(GlobalArgs p, int filled) {
     }
 }
 
-// ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) for one 4096-
-// element chunk, accumulators in shared memory: rows in physical slot order,
-// z += w·v and z += w·v² in the reference's fp64 operation order (indices are
-// unique within a row, so a row's entries add without conflicts), then θ -=
-// lr · (z1 s1) / (eps + sqrt(z2 s2)) where (z1, z2) ≠ 0 (u = 0 elsewhere);
-// update_nnz per chunk for the report. No dense accumulators in HBM.
-__global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w, int filled) {
-    extern __shared__ double s_z[];  // [kChunk] z1, [kChunk] z2, [kStage] values
-    __shared__ double s_red[kThreads / 32];
-    __shared__ int s_j0[kMaxWindow], s_off[kMaxWindow + 1];
-    __shared__ int16_t s_ei[kStage];
-    double* s_z1 = s_z;
-    double* s_z2 = s_z + kChunk;
-    double* s_ev = s_z + 2 * kChunk;
+// Every row's entry range of chunk c (one memory latency): s_j0[r] = first
+// entry, s_off = exclusive prefix of the per-row counts. Returns the total.
+__device__ __forceinline__ int chunk_rows(const GlobalArgs& p, int64_t c, int filled, int* s_j0, int* s_off) {
     const int64_t nch = global_chunks_d(p.dim);
-    const int64_t c = blockIdx.x, c0 = c * kChunk;
-    // every row's entry range of this chunk at once (one memory latency)
-    for (int r = threadIdx.x; r < filled; r += kThreads) {
+    for (int r = threadIdx.x; r < filled; r += blockDim.x) {
         const int32_t* bd = p.bounds + int64_t(r) * (nch + 1);
         s_j0[r] = bd[c];
         s_off[r + 1] = bd[c + 1] - bd[c];
@@ -525,52 +512,133 @@ __global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w,
         for (int r = 0; r < filled; ++r) s_off[r + 1] += s_off[r];
     }
     __syncthreads();
-    const int total = s_off[filled];
+    return s_off[filled];
+}
+
+// θ -= lr · (z1 s1) / (eps + sqrt(z2 s2)) at element i (optim.cpp:183-187).
+__device__ __forceinline__ void g_apply(const GlobalArgs& p, int64_t i, double z1, double z2, double& nnz) {
+    const double mhat = __dmul_rn(z1, p.scale1);
+    const double vhat = __dmul_rn(z2, p.scale2);
+    const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+    if (u != 0.0) nnz += 1.0;
+    const double th = ld_val(p.params, p.p_dtype, i);
+    st_val(p.params, p.p_dtype, i, __dsub_rn(th, __dmul_rn(p.lr, u)));
+}
+
+__device__ __forceinline__ void g_nnz_partial(const GlobalArgs& p, int64_t c, double nnz, double* s_red) {
+    if (!p.partials) return;
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    for (int off = 16; off > 0; off >>= 1) nnz += __shfl_xor_sync(0xFFFFFFFFu, nnz, off);
+    if (lane == 0) s_red[wi] = nnz;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int w2 = 0; w2 < kThreads / 32; ++w2) sum += s_red[w2];
+        p.partials[c * kReportFields + 4] = sum;
+    }
+    __syncthreads();
+}
+
+// ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) for one 4096-
+// element chunk without dense accumulators: the chunk's window entries (a few
+// hundred: rows ascending, bounds found once per step) are staged in shared
+// memory; each entry looks its coordinate up in every row's segment (binary
+// search), and the entry in the earliest row sums the coordinate's terms in
+// physical slot order — z += w·v, z += w·v², the reference's fp64 operation
+// order — and applies the update. Chunks with more than kStage entries go to
+// an overflow list for g_stats_update_dense.
+__global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w, int filled) {
+    extern __shared__ uint4 s_th4[];  // the chunk's θ, staged with 16-byte loads
+    __shared__ double s_red[kThreads / 32];
+    __shared__ int s_j0[kMaxWindow], s_off[kMaxWindow + 1];
+    __shared__ int16_t s_ei[kStage];
+    __shared__ double s_ev[kStage];
+    const int64_t c = blockIdx.x, c0 = c * kChunk;
+    const int psz = p.p_dtype == F64 ? 8 : (p.p_dtype == F32 ? 4 : 2);
+    const int n = static_cast<int>(p.dim - c0 < kChunk ? p.dim - c0 : kChunk);
+    // θ of the chunk, coalesced: ~10% of it is updated, but at that density
+    // nearly every 32-byte sector is touched, so a scattered update moves the
+    // same bytes with a dependent load per element
+    const bool vec = n == kChunk && (reinterpret_cast<uintptr_t>(p.params) & 15u) == 0;
+    const int nv16 = kChunk * psz / 16;
+    if (vec) {
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(p.params) + c0 * psz);
+        for (int t = threadIdx.x; t < nv16; t += kThreads) s_th4[t] = src[t];
+    }
+    const int total = chunk_rows(p, c, filled, s_j0, s_off);
+    if (total > kStage) {
+        if (threadIdx.x == 0) p.ovf_list[atomicAdd(p.ovf_n, 1u)] = static_cast<int>(c);
+        return;
+    }
+    for (int e = threadIdx.x; e < total; e += kThreads) {
+        int r = 0;
+        while (s_off[r + 1] <= e) ++r;
+        const int64_t q = int64_t(r) * p.row_stride + s_j0[r] + (e - s_off[r]);
+        s_ei[e] = static_cast<int16_t>(p.win_idx[q] - c0);
+        s_ev[e] = ld_val(p.win_val, p.v_dtype, q);
+    }
+    __syncthreads();
     double nnz = 0.0;
-    auto update = [&](int j, double z1, double z2) {  // optim.cpp:183-187
-        const int64_t i = c0 + j;
-        const double mhat = __dmul_rn(z1, p.scale1);
-        const double vhat = __dmul_rn(z2, p.scale2);
-        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
-        if (u != 0.0) nnz += 1.0;
-        const double th = ld_val(p.params, p.p_dtype, i);
-        st_val(p.params, p.p_dtype, i, __dsub_rn(th, __dmul_rn(p.lr, u)));
-    };
-    if (total <= kStage) {
-        // stage the chunk's window entries (rows concatenated in slot order);
-        // only the coordinates they touch are cleared, summed and updated
-        for (int e = threadIdx.x; e < total; e += kThreads) {
-            int r = 0;
-            while (s_off[r + 1] <= e) ++r;
-            const int64_t q = int64_t(r) * p.row_stride + s_j0[r] + (e - s_off[r]);
-            const int i = static_cast<int>(p.win_idx[q] - c0);
-            s_ei[e] = static_cast<int16_t>(i);
-            s_ev[e] = ld_val(p.win_val, p.v_dtype, q);
-            s_z1[i] = 0.0;
-            s_z2[i] = 0.0;
-        }
-        __syncthreads();
-        for (int r = 0; r < filled; ++r) {
-            for (int e = s_off[r] + threadIdx.x; e < s_off[r + 1]; e += kThreads) {
-                const int i = s_ei[e];
-                const double v = s_ev[e];
-                s_z1[i] = __dadd_rn(s_z1[i], __dmul_rn(w.w1[r], v));
-                s_z2[i] = __dadd_rn(s_z2[i], __dmul_rn(w.w2[r], __dmul_rn(v, v)));
+    for (int e = threadIdx.x; e < total; e += kThreads) {
+        int r = 0;
+        while (s_off[r + 1] <= e) ++r;
+        const int i = s_ei[e];
+        bool first = true;
+        double z1 = 0.0, z2 = 0.0;
+        for (int q = 0; q < filled; ++q) {
+            int pos = -1;
+            if (q == r) {
+                pos = e;
+            } else {  // rows are ascending: binary search the segment
+                int lo = s_off[q], hi = s_off[q + 1];
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_ei[mid] < i) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo < s_off[q + 1] && s_ei[lo] == i) pos = lo;
             }
-            __syncthreads();
+            if (pos < 0) continue;
+            if (q < r) {  // an earlier row holds the coordinate: it updates
+                first = false;
+                break;
+            }
+            const double v = s_ev[pos];
+            z1 = __dadd_rn(z1, __dmul_rn(w.w1[q], v));
+            z2 = __dadd_rn(z2, __dmul_rn(w.w2[q], __dmul_rn(v, v)));
         }
-        // the first entry to claim a coordinate updates it: the sign bit of z2,
-        // which the sums never set (z2 = Σ w2·v² ≥ +0)
-        for (int e = threadIdx.x; e < total; e += kThreads) {
-            const int i = s_ei[e];
-            const unsigned long long old =
-                atomicOr(reinterpret_cast<unsigned long long*>(s_z2 + i), 0x8000000000000000ull);
-            if (old >> 63) continue;
-            const double z1 = s_z1[i], z2 = __longlong_as_double(static_cast<long long>(old));
-            if (z1 == 0.0 && z2 == 0.0) continue;
-            update(i, z1, z2);
+        if (!first || (z1 == 0.0 && z2 == 0.0)) continue;
+        if (vec) {
+            const double mhat = __dmul_rn(z1, p.scale1);
+            const double vhat = __dmul_rn(z2, p.scale2);
+            const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+            if (u != 0.0) nnz += 1.0;
+            void* th = s_th4;
+            st_val(th, p.p_dtype, i, __dsub_rn(ld_val(th, p.p_dtype, i), __dmul_rn(p.lr, u)));
+        } else {
+            g_apply(p, c0 + i, z1, z2, nnz);
         }
-    } else {
+    }
+    if (vec) {
+        __syncthreads();
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<unsigned char*>(p.params) + c0 * psz);
+        for (int t = threadIdx.x; t < nv16; t += kThreads) dst[t] = s_th4[t];
+    }
+    g_nnz_partial(p, c, nnz, s_red);
+}
+
+// Chunks with more window entries than kStage: dense accumulators in shared
+// memory, rows in slot order (persistent CTAs over the overflow list).
+__global__ void g_stats_update_dense(GlobalArgs p, const __grid_constant__ GWeights w, int filled) {
+    extern __shared__ double s_z[];  // [kChunk] z1, [kChunk] z2
+    __shared__ double s_red[kThreads / 32];
+    __shared__ int s_j0[kMaxWindow], s_off[kMaxWindow + 1];
+    double* s_z1 = s_z;
+    double* s_z2 = s_z + kChunk;
+    const unsigned novf = *p.ovf_n;
+    for (unsigned o = blockIdx.x; o < novf; o += gridDim.x) {
+        const int64_t c = p.ovf_list[o], c0 = c * kChunk;
+        chunk_rows(p, c, filled, s_j0, s_off);
         for (int j = threadIdx.x; j < kChunk; j += kThreads) {
             s_z1[j] = 0.0;
             s_z2[j] = 0.0;
@@ -586,23 +654,14 @@ __global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w,
             }
             __syncthreads();
         }
+        double nnz = 0.0;
         for (int j = threadIdx.x; j < kChunk; j += kThreads) {
             if (c0 + j >= p.dim) break;
             const double z1 = s_z1[j], z2 = s_z2[j];
             if (z1 == 0.0 && z2 == 0.0) continue;
-            update(j, z1, z2);
+            g_apply(p, c0 + j, z1, z2, nnz);
         }
-    }
-    if (p.partials) {
-        const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-        for (int off = 16; off > 0; off >>= 1) nnz += __shfl_xor_sync(0xFFFFFFFFu, nnz, off);
-        if (lane == 0) s_red[wi] = nnz;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double sum = 0.0;
-            for (int w2 = 0; w2 < kThreads / 32; ++w2) sum += s_red[w2];
-            p.partials[c * kReportFields + 4] = sum;
-        }
+        g_nnz_partial(p, c, nnz, s_red);
     }
 }
 
@@ -769,10 +828,16 @@ cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s) {
 
 cudaError_t g_launch_stats_update(const GlobalArgs& a, const GWeights& w, int filled, cudaStream_t s) {
     g_bounds<<<grid_for(int64_t(filled) * a.k, 256 * 4), 256, 0, s>>>(a, filled);
-    const size_t smem = size_t(kChunk) * 2 * sizeof(double) + size_t(kStage) * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(g_stats_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = cudaMemsetAsync(a.ovf_n, 0, sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
-    g_stats_update<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, smem, s>>>(a, w, filled);
+    const size_t th_smem = size_t(kChunk) * (a.p_dtype == F64 ? 8 : (a.p_dtype == F32 ? 4 : 2));
+    e = cudaFuncSetAttribute(g_stats_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(th_smem));
+    if (e != cudaSuccess) return e;
+    g_stats_update<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, th_smem, s>>>(a, w, filled);
+    const size_t smem = size_t(kChunk) * 2 * sizeof(double);
+    e = cudaFuncSetAttribute(g_stats_update_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    g_stats_update_dense<<<148 * 2, kThreads, smem, s>>>(a, w, filled);
     return cudaGetLastError();
 }
 

@@ -81,6 +81,8 @@ struct GlobalArgs {
     unsigned int* cand_n;
     unsigned int cand_cap;
     int32_t* bounds;     // [m][chunks + 1] first entry of each 4096-chunk per row
+    int32_t* ovf_list;   // [chunks] chunks with more window entries than the staged path holds
+    unsigned int* ovf_n;
     double* partials;    // nullable: [chunks][kReportFields]
     unsigned int* flag;
     int64_t dim, nbuckets, bucket, k, row_stride;

@@ -124,3 +124,23 @@ def test_global_mode_tie_heavy_f32():
     so = orc.state()
     assert np.array_equal(_bits(_host(p)), _bits(so.params))
     assert np.array_equal(eng.error_buffer().codes, so.codes)
+
+
+@pytest.mark.parametrize("dt,density", [("bf16", 0.03), ("f32", 0.08), ("bf16", 0.08)])
+def test_global_dense_window_chunks(dt, density):
+    # m = 8: ~980 (3%) or ~2600 (8%) window entries per 4096-chunk; the latter
+    # exceed the staged ADAM_STATS path (2048) and take the dense one
+    hp = dict(lr=1e-2, window=8, density=density)
+    d = 32_001  # the oracle's block limit (block = d in global mode)
+    th0 = _host(_dev(oracle.synth(1, 0, 0, d, dt), dt))
+    orc = oracle.Oracle(th0, dict(hp, block=d), param_dtype=dt, value_dtype="bf16")
+    eng = _global_engine(d, hp, dt, "bf16")
+    p = _dev(th0, dt)
+    torch = _torch()
+    for s in range(1, 11):
+        g = _host(_dev(oracle.synth(42, s, 0, d, dt), dt))
+        orc.step(g, hp["lr"])
+        eng.step(p, _dev(g, dt), hp["lr"])
+        torch.cuda.synchronize()
+        assert np.array_equal(_bits(_host(p)), _bits(orc.state().params)), f"θ @ {s}"
+    assert np.array_equal(eng.error_buffer().codes, orc.state().codes)
