@@ -38,7 +38,7 @@ constexpr int kThreads = 256;
 constexpr int kPer = kChunk / kThreads;  // 16 elements per thread (strided by 256)
 
 __device__ __forceinline__ int64_t global_chunks_d(int64_t dim) { return (dim + kChunk - 1) / kChunk; }
-constexpr int kStage = 2048;  // window entries per chunk staged in shared memory by g_stats_update
+constexpr int kStage = 1024;  // window entries per chunk staged in shared memory by g_stats_update
 
 __device__ __forceinline__ double g_a(const GlobalArgs& p, int64_t i) {
     const int64_t q = i >> p.bucket_shift;  // bucket | 4096: a power of two
@@ -542,17 +542,20 @@ __device__ __forceinline__ void g_nnz_partial(const GlobalArgs& p, int64_t c, do
 // ADAM_STATS (window.cpp:28-46) + update (optim.cpp:183-187) for one 4096-
 // element chunk without dense accumulators: the chunk's window entries (a few
 // hundred: rows ascending, bounds found once per step) are staged in shared
-// memory; each entry looks its coordinate up in every row's segment (binary
-// search), and the entry in the earliest row sums the coordinate's terms in
+// memory; each coordinate's owner is its entry in the earliest row (atomicMin
+// over entry indices), the rows are summed into per-owner accumulators in
 // physical slot order — z += w·v, z += w·v², the reference's fp64 operation
-// order — and applies the update. Chunks with more than kStage entries go to
-// an overflow list for g_stats_update_dense.
+// order — and owners apply the update to the chunk's θ staged in shared
+// memory. Chunks with more than kStage entries go to an overflow list for
+// g_stats_update_dense.
 __global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w, int filled) {
     extern __shared__ uint4 s_th4[];  // the chunk's θ, staged with 16-byte loads
     __shared__ double s_red[kThreads / 32];
     __shared__ int s_j0[kMaxWindow], s_off[kMaxWindow + 1];
     __shared__ int16_t s_ei[kStage];
     __shared__ double s_ev[kStage];
+    __shared__ double s_z1[kStage], s_z2[kStage];  // per owner entry
+    __shared__ int s_first[kChunk];                // owner entry per coordinate (touched ones)
     const int64_t c = blockIdx.x, c0 = c * kChunk;
     const int psz = p.p_dtype == F64 ? 8 : (p.p_dtype == F32 ? 4 : 2);
     const int n = static_cast<int>(p.dim - c0 < kChunk ? p.dim - c0 : kChunk);
@@ -578,36 +581,33 @@ __global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w,
         s_ev[e] = ld_val(p.win_val, p.v_dtype, q);
     }
     __syncthreads();
+    // owner of a coordinate = its entry in the earliest row (entries are
+    // concatenated in slot order, so the smallest entry index)
+    for (int e = threadIdx.x; e < total; e += kThreads) s_first[s_ei[e]] = 0x7FFF;
+    __syncthreads();
+    for (int e = threadIdx.x; e < total; e += kThreads) atomicMin(&s_first[s_ei[e]], e);
+    __syncthreads();
+    for (int e = threadIdx.x; e < total; e += kThreads)
+        if (s_first[s_ei[e]] == e) {
+            s_z1[e] = 0.0;
+            s_z2[e] = 0.0;
+        }
+    __syncthreads();
+    for (int r = 0; r < filled; ++r) {  // slot order: z += w·v, z += w·v² (window.cpp:37-41)
+        for (int e = s_off[r] + threadIdx.x; e < s_off[r + 1]; e += kThreads) {
+            const int o = s_first[s_ei[e]];
+            const double v = s_ev[e];
+            s_z1[o] = __dadd_rn(s_z1[o], __dmul_rn(w.w1[r], v));
+            s_z2[o] = __dadd_rn(s_z2[o], __dmul_rn(w.w2[r], __dmul_rn(v, v)));
+        }
+        __syncthreads();
+    }
     double nnz = 0.0;
     for (int e = threadIdx.x; e < total; e += kThreads) {
-        int r = 0;
-        while (s_off[r + 1] <= e) ++r;
         const int i = s_ei[e];
-        bool first = true;
-        double z1 = 0.0, z2 = 0.0;
-        for (int q = 0; q < filled; ++q) {
-            int pos = -1;
-            if (q == r) {
-                pos = e;
-            } else {  // rows are ascending: binary search the segment
-                int lo = s_off[q], hi = s_off[q + 1];
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (s_ei[mid] < i) lo = mid + 1;
-                    else hi = mid;
-                }
-                if (lo < s_off[q + 1] && s_ei[lo] == i) pos = lo;
-            }
-            if (pos < 0) continue;
-            if (q < r) {  // an earlier row holds the coordinate: it updates
-                first = false;
-                break;
-            }
-            const double v = s_ev[pos];
-            z1 = __dadd_rn(z1, __dmul_rn(w.w1[q], v));
-            z2 = __dadd_rn(z2, __dmul_rn(w.w2[q], __dmul_rn(v, v)));
-        }
-        if (!first || (z1 == 0.0 && z2 == 0.0)) continue;
+        if (s_first[i] != e) continue;
+        const double z1 = s_z1[e], z2 = s_z2[e];
+        if (z1 == 0.0 && z2 == 0.0) continue;
         if (vec) {
             const double mhat = __dmul_rn(z1, p.scale1);
             const double vhat = __dmul_rn(z2, p.scale2);
