@@ -106,3 +106,30 @@ def test_bad_source_counts_rejected():
         eng.step_reduce(p, g, [g] * 9)
     with pytest.raises(Exception):
         eng.step_reduce(p, g, [g, torch.zeros(d, dtype=torch.float32, device="cuda")])
+
+
+def test_fused_reduce_on_block_shards():
+    # each shard handle reads its element range of every rank's full gradient
+    # (sources offset by the shard start, as the symmetric-memory loop does)
+    import torch
+    from paper_2405_15593_b200 import MicroAdam, sharding
+    d, hp, nsrc = 30 * BLK + 123, dict(lr=1e-3, window=3), 4
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    th0 = torch.randn(d, generator=gen, device="cuda").to(torch.bfloat16)
+    full = MicroAdam(d, hp, param_dtype="bf16", grad_dtype="bf16", value_dtype="bf16")
+    p_full = th0.clone()
+    shards = []
+    for r in range(3):
+        b0, b1, e0, e1 = sharding.partition_blocks(d, BLK, 3, r)
+        eng = MicroAdam(d, hp, param_dtype="bf16", grad_dtype="bf16", value_dtype="bf16", block_range=(b0, b1))
+        shards.append((eng, e0, e1, th0[e0:e1].clone()))
+    for s in range(5):
+        srcs = [torch.randn(d, generator=gen, device="cuda").to(torch.bfloat16) for _ in range(nsrc)]
+        g = _reduce(srcs, 0.25)
+        full.step(p_full, g, hp["lr"])
+        for eng, e0, e1, p in shards:
+            out = torch.empty(e1 - e0, dtype=torch.bfloat16, device="cuda")
+            eng.step_reduce(p, out, [x[e0:e1] for x in srcs], 0.25, hp["lr"])
+        torch.cuda.synchronize()
+        for eng, e0, e1, p in shards:
+            assert torch.equal(p.view(torch.int16), p_full[e0:e1].view(torch.int16)), f"shard θ @ {s}"
