@@ -147,7 +147,11 @@ MA_API ma_status ma_step(ma_handle* h, void* d_params, const void* d_grads, doub
  * h_params are HOST buffers (pinned or pageable, grad/param dtype). The handle
  * keeps a device copy of θ (uploaded from h_params on the first call or after
  * ma_set_params), streams the gradient up and the updated θ back in chunks
- * that overlap the step, and returns when h_params holds the new θ. */
+ * that overlap the step, and returns when h_params holds the new θ. The device
+ * θ is authoritative between calls: modify θ only through ma_set_params. With
+ * MA_HOST_SPARSE=1 in the environment only θ at the window coordinates comes
+ * back (scattered by host threads) when h_params is the buffer of the
+ * previous call; otherwise, and by default, the whole θ is copied back. */
 MA_API ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double lr,
                        ma_step_report* report);
 
