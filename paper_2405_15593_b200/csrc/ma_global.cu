@@ -25,6 +25,8 @@
 // Window rows: int32 global indices [m][row stride] + values.
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "ma_device.cuh"
 #include "ma_internal.h"
 
@@ -109,11 +111,16 @@ __global__ void g_levels(GlobalArgs p) {
 // collect: also append the keys that share the prefix (the candidates of the
 // remaining digits) to p.cand; from_cand: passes after the collecting one read
 // p.cand instead of re-decoding the vector, unless it overflowed.
+template <bool PRIV>
 __global__ void g_hist(GlobalArgs p, int shift, int nbins, int collect, int from_cand) {
-    __shared__ uint32_t h[2048];
+    // PRIV (first digits, keys crowd a few bins): one histogram per warp and
+    // plain shared atomics; otherwise one per CTA with match.any aggregation
+    extern __shared__ uint32_t s_hw[];
+    __shared__ uint32_t s_h1[PRIV ? 1 : 2048];
+    uint32_t* h = PRIV ? s_hw + (threadIdx.x >> 5) * 2048 : s_h1;
     const uint64_t prefix = p.sel_state[0], pmask = p.sel_state[1];
     if (from_cand && *p.cand_n <= p.cand_cap) return;  // g_hist_cand covers this digit
-    for (int i = threadIdx.x; i < nbins; i += blockDim.x) h[i] = 0;
+    for (int i = threadIdx.x; i < (PRIV ? 2048 * (kThreads / 32) : nbins); i += blockDim.x) (PRIV ? s_hw : s_h1)[i] = 0;
     __syncthreads();
     bool bad = false;
     const int64_t ngroups = (p.dim + 7) / 8;
@@ -133,11 +140,17 @@ __global__ void g_hist(GlobalArgs p, int shift, int nbins, int collect, int from
             inm |= static_cast<uint32_t>(in) << e;
         }
         if (!__any_sync(act, inm != 0)) continue;  // later digits: few keys share the prefix
-        // one atomic per distinct bin per warp (keys crowd a few exponent bins)
+        if constexpr (PRIV) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const unsigned peers = __match_any_sync(act, bins[e]);
-            if (bins[e] >= 0 && (__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&h[bins[e]], __popc(peers));
+            for (int e = 0; e < 8; ++e)
+                if (bins[e] >= 0) atomicAdd(&h[bins[e]], 1u);
+        } else {
+            // one atomic per distinct bin per warp (keys crowd a few exponent bins)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const unsigned peers = __match_any_sync(act, bins[e]);
+                if (bins[e] >= 0 && (__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&h[bins[e]], __popc(peers));
+            }
         }
         if (collect) {
             const int n = __popc(inm);
@@ -162,8 +175,15 @@ __global__ void g_hist(GlobalArgs p, int shift, int nbins, int collect, int from
     }
     if (bad && p.check_finite) atomicOr(p.flag, 1u);
     __syncthreads();
-    for (int i = threadIdx.x; i < nbins; i += blockDim.x)
-        if (h[i]) atomicAdd(&p.hist[i], h[i]);
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x) {
+        uint32_t v = 0;
+        if constexpr (PRIV) {
+            for (int w = 0; w < kThreads / 32; ++w) v += s_hw[w * 2048 + i];
+        } else {
+            v = s_h1[i];
+        }
+        if (v) atomicAdd(&p.hist[i], v);
+    }
 }
 
 template <int NT = kThreads>
@@ -784,12 +804,23 @@ cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s) {
 // then 8 bits, each digit picked on the device (no host round trip).
 cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
     static const int kShift[6] = {52, 41, 30, 19, 8, 0};
+    constexpr size_t kPrivSmem = size_t(2048) * 4 * (kThreads / 32);
+    static const bool g_hist_priv = [] {
+        const char* e = std::getenv("MA_GLOBAL_HIST_MATCH");  // A/B: match.any on every digit
+        if (e && e[0] == '1') return false;
+        return cudaFuncSetAttribute(g_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPrivSmem)) ==
+               cudaSuccess;
+    }();
     g_sel_init<<<1, 256, 0, s>>>(a);
     // digit 3 collects the keys sharing the 22-bit prefix; digits 4-6 read
     // them (a few thousand keys) instead of re-decoding d elements
     for (int pass = 0; pass < 6; ++pass) {
         const int nbins = pass == 5 ? 256 : 2048;
-        g_hist<<<grid_for(a.dim, 256 * 16), 256, 0, s>>>(a, kShift[pass], nbins, pass == 2, pass > 2);
+        if (pass < 2 && g_hist_priv) {
+            g_hist<true><<<grid_for(a.dim, 256 * 16), 256, kPrivSmem, s>>>(a, kShift[pass], nbins, 0, 0);
+        } else {
+            g_hist<false><<<grid_for(a.dim, 256 * 16), 256, 0, s>>>(a, kShift[pass], nbins, pass == 2, pass > 2);
+        }
         if (pass > 2) g_hist_cand<<<64, 256, 0, s>>>(a, kShift[pass], nbins);
         g_pick<<<1, 32, 0, s>>>(a, kShift[pass], nbins);
     }
