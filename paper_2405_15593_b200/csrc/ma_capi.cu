@@ -215,6 +215,7 @@ struct ma_handle {
     // the sparse θ return is only valid into that buffer
     const void* host_synced = nullptr;
     cudaStream_t host_stream = nullptr;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // ma_step_host copy streams
     cudaStream_t last_stream = nullptr;
     int64_t launches = 0;
     // sparse propagation: the step's kernel arguments between ma_step_front and ma_step_stats
@@ -264,6 +265,8 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_bounds);
     cudaFree(h->d_dense);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
+    if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+    if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     delete h->pending;
     delete h;
 }
@@ -745,16 +748,20 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
     }
     const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(64) << 20) / (s.block * int64_t(gsz)));
     const int64_t nchunks = (nb + chunk_blocks - 1) / chunk_blocks;
-    std::vector<cudaEvent_t> up(static_cast<size_t>(nchunks)), done(static_cast<size_t>(nchunks)),
-        back(static_cast<size_t>(nchunks));
-    static thread_local cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-    if (!s_h2d) MA_CUDA(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking));
-    if (!s_d2h) MA_CUDA(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking));
-    for (int64_t c = 0; c < nchunks; ++c) {
-        MA_CUDA(cudaEventCreateWithFlags(&up[size_t(c)], cudaEventDisableTiming));
-        MA_CUDA(cudaEventCreateWithFlags(&done[size_t(c)], cudaEventDisableTiming));
-        MA_CUDA(cudaEventCreateWithFlags(&back[size_t(c)], cudaEventDisableTiming));
-    }
+    struct Events {  // released on every return path
+        std::vector<cudaEvent_t> e;
+        ~Events() {
+            for (cudaEvent_t x : e) cudaEventDestroy(x);
+        }
+    } ev;
+    ev.e.assign(static_cast<size_t>(3 * nchunks), nullptr);
+    cudaEvent_t* up = ev.e.data();
+    cudaEvent_t* done = up + nchunks;
+    cudaEvent_t* back = done + nchunks;
+    if (!h->s_h2d) MA_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    if (!h->s_d2h) MA_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    cudaStream_t s_h2d = h->s_h2d, s_d2h = h->s_d2h;
+    for (size_t i = 0; i < ev.e.size(); ++i) MA_CUDA(cudaEventCreateWithFlags(&ev.e[i], cudaEventDisableTiming));
     const int filled = static_cast<int>(h->filled);
     for (int64_t c = 0; c < nchunks; ++c) {
         const int64_t cb0 = c * chunk_blocks, cb1 = std::min(nb, cb0 + chunk_blocks);
@@ -832,11 +839,6 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
     }
     MA_CUDA(cudaStreamSynchronize(s_d2h));
     MA_CUDA(cudaStreamSynchronize(st));
-    for (int64_t c = 0; c < nchunks; ++c) {
-        cudaEventDestroy(up[size_t(c)]);
-        cudaEventDestroy(done[size_t(c)]);
-        cudaEventDestroy(back[size_t(c)]);
-    }
     h->last_stream = st;
     h->host_synced = h_params;
     return ma_sync(h);
