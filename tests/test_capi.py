@@ -57,6 +57,9 @@ def test_cpp_host_api_links(ma, tmp_path):
         "  if (argc > 5) {  // link check only: never runs without a GPU\n"
         "    microadam_b200::MicroAdamOptimizer opt(microadam_b200::Vec(8, 0.0), hp);\n"
         "    microadam_b200::Optimizer& o = opt; o.step(microadam_b200::Vec(8, 1.0));\n"
+        "    microadam_b200::MicroAdam eng(8, hp);\n"
+        "    std::vector<const void*> srcs(2, nullptr);\n"
+        "    eng.step_reduce(nullptr, nullptr, srcs, 0.5f, 1e-3);\n"
         "  }\n"
         "  return hp.resolve_k(1000) == 10 ? 0 : 1;\n}\n")
     exe = tmp_path / "caller"
