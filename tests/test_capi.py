@@ -106,6 +106,11 @@ def test_invalid_hyperparams_rejected(ma, field, value):  # optim.cpp:7-21
         ma.HyperParams(**{field: value}).validate()
 
 
+def test_empty_vector_rejected(ma):  # optim.cpp:136 "empty parameter vector"
+    assert _validate(ma, dim=0) == ma._capi.MA_ERR_INVALID_ARG
+    assert _validate(ma, dim=1) == ma._capi.MA_OK
+
+
 def test_k_exceeding_dim_rejected(ma):  # optim.cpp:23-26
     assert _validate(ma, dim=5, k=7) == ma._capi.MA_ERR_INVALID_ARG
 

@@ -151,6 +151,8 @@ def test_fp32_window_values():
     (8192 * 3 + 5, 8192, 64, 0.01, 10),  # the 8192 variant + 5-element tail
     (130, 128, 64, 0.5, 1),        # m = 1
     (8, 4, 2, 0.25, 10),           # test_optim.cpp:265-274 shape
+    (1, 4096, 64, 0.01, 3),        # d = 1: block = 1, the element is always selected
+    (3, 2, 1, 0.5, 2),             # bucket 1, ragged last block
 ])
 @pytest.mark.parametrize("kernel", ["fast", "generic"])
 def test_shapes(d, block, bucket, density, m, kernel):
