@@ -357,7 +357,7 @@ def test_persistent_spikes_duplicate_window_coordinates(kernel):
                grad_fn=g, kernel=kernel)
 
 
-@pytest.mark.parametrize("density,m", [(0.015, 10), (0.002, 30), (0.01, 127)])
+@pytest.mark.parametrize("density,m", [(0.015, 10), (0.002, 30), (0.01, 127), (0.004, 256)])
 def test_warp_kernel_shapes(density, m):
     run_parity(4096 * 9, dict(lr=1e-2, density=density, window=m), gdt="bf16", pdt="bf16",
                vdt="bf16", steps=min(m + 3, 20))
