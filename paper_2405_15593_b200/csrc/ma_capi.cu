@@ -195,6 +195,7 @@ struct ma_handle {
     int2* g_selinfo = nullptr;
     unsigned long long* g_selstate = nullptr;
     uint64_t* g_cand = nullptr;
+    int32_t* g_cand_idx = nullptr;
     int32_t* g_ovf = nullptr;
     unsigned cand_cap = 0;
     int32_t* g_bounds = nullptr;
@@ -261,6 +262,7 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_selinfo);
     cudaFree(h->g_selstate);
     cudaFree(h->g_cand);
+    cudaFree(h->g_cand_idx);
     cudaFree(h->g_ovf);
     cudaFree(h->g_bounds);
     cudaFree(h->d_dense);
@@ -400,6 +402,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.sel_info = h->g_selinfo;
     g.sel_state = h->g_selstate;
     g.cand = h->g_cand;
+    g.cand_idx = h->g_cand_idx;
     g.cand_n = reinterpret_cast<unsigned int*>(h->g_selstate + 3);
     g.cand_cap = h->cand_cap;
     g.ovf_list = h->g_ovf;
@@ -606,6 +609,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         const char* cc = std::getenv("MA_GLOBAL_CAND_CAP");
         h->cand_cap = cc ? static_cast<unsigned>(std::strtoul(cc, nullptr, 10)) : kGlobalCandCap;
         alloc(reinterpret_cast<void**>(&h->g_cand), size_t(h->cand_cap) * sizeof(uint64_t));
+        alloc(reinterpret_cast<void**>(&h->g_cand_idx), size_t(h->cand_cap) * sizeof(int32_t));
         alloc(reinterpret_cast<void**>(&h->g_bounds), size_t(cfg->hp.window) * size_t(nch + 1) * sizeof(int32_t));
     }
     alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));

@@ -131,13 +131,21 @@ __global__ void g_hist(GlobalArgs p, int shift, int nbins, int collect, int from
         const unsigned act = __activemask();
         uint32_t inm = 0;
         int bins[8];
+        int above = 0;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const uint64_t k = key_of(a[e]);
             bad |= e < nv && (k >> 52) >= 0x7FFu;  // inf / NaN (check_finite in topk_global)
             const bool in = e < nv && (k & pmask) == prefix;
+            above += e < nv && (k & pmask) > prefix;
             bins[e] = in ? static_cast<int>((k >> shift) & uint64_t(nbins - 1)) : -1;
             inm |= static_cast<uint32_t>(in) << e;
+        }
+        if (collect) {
+            // keys above the collected prefix are above K*: count them per
+            // chunk (a warp's 32 groups lie in one 4096-chunk)
+            const int wsum = __reduce_add_sync(act, above);
+            if (wsum && (threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(&p.cnt[(gi * 8) / kChunk].x, wsum);
         }
         if (!__any_sync(act, inm != 0)) continue;  // later digits: few keys share the prefix
         if constexpr (PRIV) {
@@ -168,7 +176,10 @@ __global__ void g_hist(GlobalArgs p, int shift, int nbins, int collect, int from
 #pragma unroll
             for (int e = 0; e < 8; ++e)
                 if ((inm >> e) & 1u) {
-                    if (base < p.cand_cap) p.cand[base] = key_of(a[e]);
+                    if (base < p.cand_cap) {
+                        p.cand[base] = key_of(a[e]);
+                        p.cand_idx[base] = static_cast<int32_t>(gi * 8 + e);
+                    }
                     ++base;
                 }
         }
@@ -216,6 +227,7 @@ __device__ __forceinline__ int cta_excl_scan(int v, int* s_tmp, int& total) {
 // Counts of keys > K* and == K* per chunk.
 __global__ void g_count(GlobalArgs p) {
     __shared__ int s_tmp[33];
+    if (*p.cand_n <= p.cand_cap) return;  // g_count_cand: the collect pass counted
     const int64_t c0 = int64_t(blockIdx.x) * kChunk;
     int gt = 0, eq = 0;
     const uint64_t kstar = p.sel_state[0];
@@ -702,9 +714,25 @@ __global__ void g_hist_cand(GlobalArgs p, int shift, int nbins) {
         if (h[i]) atomicAdd(&p.hist[i], h[i]);
 }
 
+// Per-chunk (> K*, == K*) counts from the collected keys, on top of the
+// above-prefix counts the collecting pass made (unless the buffer overflowed:
+// then g_count recounts every chunk).
+__global__ void g_count_cand(GlobalArgs p) {
+    const unsigned n = *p.cand_n;
+    if (n > p.cand_cap) return;
+    const uint64_t kstar = p.sel_state[0];
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t k = p.cand[i];
+        const int64_t c = p.cand_idx[i] / kChunk;
+        if (k > kstar) atomicAdd(&p.cnt[c].x, 1);
+        else if (k == kstar) atomicAdd(&p.cnt[c].y, 1);
+    }
+}
+
 // Radix select state: no key prefix yet, k entries still to place.
-__global__ void g_sel_init(GlobalArgs p) {
+__global__ void g_sel_init(GlobalArgs p, int64_t nch) {
     for (int i = threadIdx.x; i < 2048; i += blockDim.x) p.hist[i] = 0;
+    for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) p.cnt[c] = make_int2(0, 0);
     if (threadIdx.x == 0) {
         p.sel_state[0] = 0;
         p.sel_state[1] = 0;
@@ -811,7 +839,7 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
         return cudaFuncSetAttribute(g_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPrivSmem)) ==
                cudaSuccess;
     }();
-    g_sel_init<<<1, 256, 0, s>>>(a);
+    g_sel_init<<<1, 1024, 0, s>>>(a, global_chunks(a.dim));
     // digit 3 collects the keys sharing the 22-bit prefix; digits 4-6 read
     // them (a few thousand keys) instead of re-decoding d elements
     for (int pass = 0; pass < 6; ++pass) {
@@ -830,6 +858,7 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
 cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s) {
     const int64_t nch = global_chunks(a.dim);
     g_count<<<static_cast<unsigned>(nch), kThreads, 0, s>>>(a);
+    g_count_cand<<<256, 256, 0, s>>>(a);
     g_alloc<<<1, kAllocThreads, 0, s>>>(a, nch);
     return cudaGetLastError();
 }

@@ -78,6 +78,7 @@ struct GlobalArgs {
     int2* sel_info;        // [chunks] (row offset, ties taken)
     unsigned long long* sel_state;  // radix select on device: [0] key prefix (K* at the end), [1] mask, [2] ties left
     uint64_t* cand;       // keys sharing the prefix after three digits (cand_cap entries)
+    int32_t* cand_idx;    // their indices
     unsigned int* cand_n;
     unsigned int cand_cap;
     int32_t* bounds;     // [m][chunks + 1] first entry of each 4096-chunk per row
