@@ -225,28 +225,29 @@ __device__ __forceinline__ int cta_excl_scan(int v, int* s_tmp, int& total) {
 }
 
 // Counts of keys > K* and == K* per chunk.
-__global__ void g_count(GlobalArgs p) {
+__global__ void g_count(GlobalArgs p, int64_t nch) {
     __shared__ int s_tmp[33];
     if (*p.cand_n <= p.cand_cap) return;  // g_count_cand: the collect pass counted
-    const int64_t c0 = int64_t(blockIdx.x) * kChunk;
-    int gt = 0, eq = 0;
     const uint64_t kstar = p.sel_state[0];
-    const int64_t e0 = c0 + int64_t(threadIdx.x) * kPer;
-    for (int h = 0; h < kPer / 8; ++h) {
-        if (e0 + 8 * h >= p.dim) break;
-        double a[8];
-        const int nv = g_a8(p, e0 + 8 * h, a);
+    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {  // persistent: cheap when skipped
+        const int64_t e0 = c * kChunk + int64_t(threadIdx.x) * kPer;
+        int gt = 0, eq = 0;
+        for (int h = 0; h < kPer / 8; ++h) {
+            if (e0 + 8 * h >= p.dim) break;
+            double a[8];
+            const int nv = g_a8(p, e0 + 8 * h, a);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const uint64_t k = key_of(a[e]);
-            gt += e < nv && k > kstar;
-            eq += e < nv && k == kstar;
+            for (int e = 0; e < 8; ++e) {
+                const uint64_t k = key_of(a[e]);
+                gt += e < nv && k > kstar;
+                eq += e < nv && k == kstar;
+            }
         }
+        int tg, te;
+        cta_excl_scan(gt, s_tmp, tg);
+        cta_excl_scan(eq, s_tmp, te);
+        if (threadIdx.x == 0) p.cnt[c] = make_int2(tg, te);
     }
-    int tg, te;
-    cta_excl_scan(gt, s_tmp, tg);
-    cta_excl_scan(eq, s_tmp, te);
-    if (threadIdx.x == 0) p.cnt[blockIdx.x] = make_int2(tg, te);
 }
 
 // Selected entries of a chunk at their global row positions, ascending index.
@@ -857,7 +858,7 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
 
 cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s) {
     const int64_t nch = global_chunks(a.dim);
-    g_count<<<static_cast<unsigned>(nch), kThreads, 0, s>>>(a);
+    g_count<<<static_cast<unsigned>(nch < 148 * 8 ? nch : 148 * 8), kThreads, 0, s>>>(a, nch);
     g_count_cand<<<256, 256, 0, s>>>(a);
     g_alloc<<<1, kAllocThreads, 0, s>>>(a, nch);
     return cudaGetLastError();
