@@ -834,6 +834,11 @@ cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s) {
 cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
     static const int kShift[6] = {52, 41, 30, 19, 8, 0};
     constexpr size_t kPrivSmem = size_t(2048) * 4 * (kThreads / 32);
+    static const int g_priv_passes = [] {  // A/B knob: leading digits with per-warp histograms
+        const char* e = std::getenv("MA_GLOBAL_PRIV_PASSES");
+        const int n = e ? std::atoi(e) : 2;
+        return n < 0 ? 0 : (n > 2 ? 2 : n);  // digit 3 collects: never the per-warp variant
+    }();
     static const bool g_hist_priv = [] {
         const char* e = std::getenv("MA_GLOBAL_HIST_MATCH");  // A/B: match.any on every digit
         if (e && e[0] == '1') return false;
@@ -845,7 +850,7 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
     // them (a few thousand keys) instead of re-decoding d elements
     for (int pass = 0; pass < 6; ++pass) {
         const int nbins = pass == 5 ? 256 : 2048;
-        if (pass < 2 && g_hist_priv) {
+        if (pass < g_priv_passes && g_hist_priv) {
             g_hist<true><<<grid_for(a.dim, 256 * 16), 256, kPrivSmem, s>>>(a, kShift[pass], nbins, 0, 0);
         } else {
             g_hist<false><<<grid_for(a.dim, 256 * 16), 256, 0, s>>>(a, kShift[pass], nbins, pass == 2, pass > 2);
