@@ -26,7 +26,7 @@ namespace microadam {
 // ---- the adapter ----
 class CudaMicroAdamOptimizer : public Optimizer {
 public:
-    CudaMicroAdamOptimizer(Vec theta0, const HyperParams& hp, bool blockwise = true)
+    CudaMicroAdamOptimizer(Vec theta0, const HyperParams& hp, bool blockwise = false)
         : theta_(std::move(theta0)), hp_(hp) {
         ma_config cfg;
         ma_config_default(&cfg);

@@ -221,6 +221,11 @@ struct ma_handle {
     int64_t launches = 0;
     // sparse propagation: the step's kernel arguments between ma_step_front and ma_step_stats
     ma::StepArgs* pending = nullptr;
+    // completion of the handle's last enqueued work (ma_sync and the readers
+    // wait on it: stream-scoped, never a device-wide synchronize)
+    cudaEvent_t done_ev = nullptr;
+    // ma_step_host chunk events, created once and reused across calls
+    std::vector<cudaEvent_t> host_ev;
 };
 
 namespace {
@@ -266,6 +271,8 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_ovf);
     cudaFree(h->g_bounds);
     cudaFree(h->d_dense);
+    if (h->done_ev) cudaEventDestroy(h->done_ev);
+    for (cudaEvent_t e : h->host_ev) cudaEventDestroy(e);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
@@ -274,6 +281,43 @@ void free_handle(ma_handle* h) {
 }
 
 constexpr unsigned kGlobalCandCap = 1u << 20;  // global radix select: keys kept after three digits
+
+// Record the completion of everything the handle enqueued on `st`.
+ma_status mark_done(ma_handle* h, cudaStream_t st) {
+    if (!h->done_ev) MA_CUDA(cudaEventCreateWithFlags(&h->done_ev, cudaEventDisableTiming));
+    MA_CUDA(cudaEventRecord(h->done_ev, st));
+    h->last_stream = st;
+    return MA_OK;
+}
+// Wait for the handle's last step (event-scoped: other streams and handles on
+// the device keep running).
+ma_status wait_done(ma_handle* h) {
+    if (h->done_ev) MA_CUDA(cudaEventSynchronize(h->done_ev));
+    return MA_OK;
+}
+
+// The host counters before a step: a step whose launch fails leaves the
+// handle as it was (the reference throws before any mutation, optim.cpp:34-37).
+struct CounterSnap {
+    int64_t step, head, filled, stamp;
+};
+CounterSnap snap_counters(const ma_handle* h) {
+    return CounterSnap{h->step, h->head, h->filled, h->stamps[size_t(h->head)]};
+}
+void restore_counters(ma_handle* h, const CounterSnap& c) {
+    h->step = c.step;
+    h->head = c.head;
+    h->filled = c.filled;
+    h->stamps[size_t(c.head)] = c.stamp;
+}
+#define MA_CUDA_ROLLBACK(h, snap, call)                     \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) {                            \
+            restore_counters((h), (snap));                  \
+            return cuda_fail(_e, #call);                    \
+        }                                                   \
+    } while (0)
 
 // Advance the host counters exactly like GradientWindow::push (window.cpp:14-26)
 // and build the kernel weights like adam_stats (window.cpp:28-46).
@@ -373,10 +417,21 @@ ma_status strict_prescan(ma_handle* h, const void* d_grads, cudaStream_t st) {
     MA_CUDA(cudaMemsetAsync(h->d_flag, 0, sizeof(unsigned), st));
     MA_CUDA(ma::launch_finite_scan(d_grads, h->cfg.grad_dtype, h->shape.dim, h->d_flag, st));
     ++h->launches;
+    if (h->cfg.grad_dtype == MA_F64 && h->step > 0) {
+        // a = g + e can overflow only for f64 gradients (bf16/f32 g plus an EF
+        // bounded by earlier finite a stays finite in fp64)
+        MA_CUDA(ma::launch_finite_scan_a(static_cast<const double*>(d_grads), h->d_codes, h->d_meta, h->d_dense,
+                                         h->shape.dim, h->shape.bucket, int(h->cfg.hp.bits), h->d_flag, st));
+        ++h->launches;
+    }
     unsigned flag = 0;
     MA_CUDA(cudaMemcpyAsync(&flag, h->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, st));
     MA_CUDA(cudaStreamSynchronize(st));
-    if (flag) return fail(MA_ERR_NONFINITE, "step gradient: non-finite entry");
+    if (flag) {
+        const unsigned zero = 0;
+        MA_CUDA(cudaMemcpy(h->d_flag, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+        return fail(MA_ERR_NONFINITE, "step gradient: non-finite entry");
+    }
     return MA_OK;
 }
 
@@ -387,6 +442,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     const Shape& s = h->shape;
     ma::StepArgs a;
     base_args(h, &a);
+    const CounterSnap snap = snap_counters(h);
     push_and_weights(h, &a);
     ma::GlobalArgs g{};
     g.grads = d_grads;
@@ -426,7 +482,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.lr = lr;
     g.scale1 = a.scale1;
     g.scale2 = a.scale2;
-    MA_CUDA(ma::g_launch_levels(g, st));
+    MA_CUDA_ROLLBACK(h, snap, ma::g_launch_levels(g, st));
     // G1-G2 entirely on the device: the six radix digits are picked by a
     // one-warp kernel after each histogram, row offsets / ties per chunk by a
     // one-CTA scan — the step never waits for the host.
@@ -442,7 +498,8 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     }
     MA_CUDA(ma::g_launch_stats_update(g, w, int(h->filled), st));
     h->launches += 5;
-    h->last_stream = st;
+    ma_status ms = mark_done(h, st);
+    if (ms != MA_OK) return ms;
     if (report) {
         MA_CUDA(ma::launch_report_reduce(h->d_partials, ma::global_chunks(s.dim), h->d_report, st));
         ++h->launches;
@@ -475,10 +532,12 @@ ma_status run_step(ma_handle* h, void* d_params, const void* d_grads, double lr,
     a.lr = lr;
     a.lr32 = static_cast<float>(lr);
     a.partials = report ? h->d_partials : nullptr;
+    const CounterSnap snap = snap_counters(h);
     push_and_weights(h, &a);
-    MA_CUDA(launch(h, a, h->shape.b1 - h->shape.b0, st));
+    MA_CUDA_ROLLBACK(h, snap, launch(h, a, h->shape.b1 - h->shape.b0, st));
     ++h->launches;
-    h->last_stream = st;
+    ma_status ms = mark_done(h, st);
+    if (ms != MA_OK) return ms;
     if (report) return finish_report(h, st, report);
     return MA_OK;
 }
@@ -682,11 +741,11 @@ ma_status ma_step_reduce(ma_handle* h, void* d_params, void* d_grads, const void
     a.params = d_params;
     a.lr = lr;
     a.lr32 = static_cast<float>(lr);
+    const CounterSnap snap = snap_counters(h);
     push_and_weights(h, &a);
-    MA_CUDA(launch(h, a, s.b1 - s.b0, st));
+    MA_CUDA_ROLLBACK(h, snap, launch(h, a, s.b1 - s.b0, st));
     ++h->launches;
-    h->last_stream = st;
-    return MA_OK;
+    return mark_done(h, st);
 }
 
 ma_status ma_set_params(ma_handle* h, const void* h_params) {
@@ -713,8 +772,9 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
         if (st != MA_OK) return st;
     }
     cudaStream_t st = h->host_stream;
-    if (h->cfg.finite_mode == MA_FINITE_STRICT || report) {
-        // Whole-vector path: strict pre-scan / report need the full gradient.
+    if (h->cfg.finite_mode == MA_FINITE_STRICT || report || s.global) {
+        // Whole-vector path: strict pre-scan / report need the full gradient;
+        // global Top-K (ma_global.cu) selects over the whole vector at once.
         MA_CUDA(cudaMemcpyAsync(h->d_gstage, h_grads, size_t(s.dim) * gsz, cudaMemcpyHostToDevice, st));
         ma_status r = run_step(h, h->d_theta, h->d_gstage, lr, st, report);
         if (r != MA_OK) return r;
@@ -738,6 +798,7 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
     a.params = h->d_theta;
     a.lr = lr;
     a.lr32 = static_cast<float>(lr);
+    const CounterSnap snap = snap_counters(h);
     push_and_weights(h, &a);
     const int64_t nb = s.b1 - s.b0;
     const int64_t m = h->cfg.hp.window, kbs = s.kb_stride;
@@ -752,20 +813,18 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
     }
     const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(64) << 20) / (s.block * int64_t(gsz)));
     const int64_t nchunks = (nb + chunk_blocks - 1) / chunk_blocks;
-    struct Events {  // released on every return path
-        std::vector<cudaEvent_t> e;
-        ~Events() {
-            for (cudaEvent_t x : e) cudaEventDestroy(x);
-        }
-    } ev;
-    ev.e.assign(static_cast<size_t>(3 * nchunks), nullptr);
-    cudaEvent_t* up = ev.e.data();
+    // chunk events: created on the first call, reused afterwards
+    while (h->host_ev.size() < size_t(3 * nchunks)) {
+        cudaEvent_t e = nullptr;
+        MA_CUDA_ROLLBACK(h, snap, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->host_ev.push_back(e);
+    }
+    cudaEvent_t* up = h->host_ev.data();
     cudaEvent_t* done = up + nchunks;
     cudaEvent_t* back = done + nchunks;
-    if (!h->s_h2d) MA_CUDA(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
-    if (!h->s_d2h) MA_CUDA(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+    if (!h->s_h2d) MA_CUDA_ROLLBACK(h, snap, cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+    if (!h->s_d2h) MA_CUDA_ROLLBACK(h, snap, cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
     cudaStream_t s_h2d = h->s_h2d, s_d2h = h->s_d2h;
-    for (size_t i = 0; i < ev.e.size(); ++i) MA_CUDA(cudaEventCreateWithFlags(&ev.e[i], cudaEventDisableTiming));
     const int filled = static_cast<int>(h->filled);
     for (int64_t c = 0; c < nchunks; ++c) {
         const int64_t cb0 = c * chunk_blocks, cb1 = std::min(nb, cb0 + chunk_blocks);
@@ -776,7 +835,8 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
         MA_CUDA(cudaEventRecord(up[size_t(c)], s_h2d));
         MA_CUDA(cudaStreamWaitEvent(st, up[size_t(c)], 0));
         a.block_offset = cb0;
-        MA_CUDA(launch(h, a, cb1 - cb0, st));
+        if (c == 0) MA_CUDA_ROLLBACK(h, snap, launch(h, a, cb1 - cb0, st));  // nothing mutated yet
+        else MA_CUDA(launch(h, a, cb1 - cb0, st));
         ++h->launches;
         if (sparse_ret) {
             MA_CUDA(ma::launch_gather_window_theta(h->d_win_idx, h->d_theta, h->cfg.param_dtype, h->d_gath, cb0, cb1,
@@ -842,8 +902,7 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
         if (err) return fail(MA_ERR_CUDA, "ma_step_host: sparse θ return failed");
     }
     MA_CUDA(cudaStreamSynchronize(s_d2h));
-    MA_CUDA(cudaStreamSynchronize(st));
-    h->last_stream = st;
+    { ma_status ms = mark_done(h, st); if (ms != MA_OK) return ms; }
     h->host_synced = h_params;
     return ma_sync(h);
 }
@@ -851,11 +910,13 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
 ma_status ma_sync(ma_handle* h) {
     if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
     DeviceGuard g(h->device);
-    MA_CUDA(cudaDeviceSynchronize());
+    ma_status ws = wait_done(h);
+    if (ws != MA_OK) return ws;
     unsigned flag = 0;
     MA_CUDA(cudaMemcpy(&flag, h->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
     if (flag) {
-        MA_CUDA(cudaMemset(h->d_flag, 0, sizeof(unsigned)));
+        const unsigned zero = 0;
+        MA_CUDA(cudaMemcpy(h->d_flag, &zero, sizeof(zero), cudaMemcpyHostToDevice));
         return fail(MA_ERR_NONFINITE, "step gradient: non-finite entry (state of that step is undefined)");
     }
     return MA_OK;
@@ -875,7 +936,7 @@ ma_status ma_read_error_buffer(ma_handle* h, uint8_t* codes, double* lo, double*
     if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
     if (h->d_dense) return fail(MA_ERR_STATE, "error_buffer: engine uses dense error storage");
     DeviceGuard g(h->device);
-    MA_CUDA(cudaDeviceSynchronize());
+    { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
     if (codes) MA_CUDA(cudaMemcpy(codes, h->d_codes, size_t(h->shape.code_bytes), cudaMemcpyDeviceToHost));
     if (lo || hi) {
         std::vector<double2> meta(size_t(h->shape.nbuckets));
@@ -902,7 +963,7 @@ double widen(const void* p, int dt, size_t i) {
 ma_status ma_read_error_vector(ma_handle* h, double* out) {
     if (!h || !out) return fail(MA_ERR_INVALID_ARG, "null argument");
     DeviceGuard g(h->device);
-    MA_CUDA(cudaDeviceSynchronize());
+    { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
     const Shape& s = h->shape;
     if (h->d_dense) {
         MA_CUDA(cudaMemcpy(out, h->d_dense, size_t(s.dim) * sizeof(double), cudaMemcpyDeviceToHost));
@@ -931,7 +992,7 @@ ma_status ma_read_window_row(ma_handle* h, int64_t slot, int64_t* indices, doubl
     if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
     if (slot < 0 || slot >= h->cfg.hp.window) return fail(MA_ERR_INVALID_ARG, "slot out of range");
     DeviceGuard g(h->device);
-    MA_CUDA(cudaDeviceSynchronize());
+    { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
     const Shape& s = h->shape;
     const int64_t nb = s.b1 - s.b0, m = h->cfg.hp.window, kbs = s.kb_stride;
     const size_t vsz = dtype_size(h->cfg.value_dtype);
@@ -969,6 +1030,40 @@ ma_status ma_read_window_row(ma_handle* h, int64_t slot, int64_t* indices, doubl
     return MA_OK;
 }
 
+namespace {
+// Window rows as SparseSelection::validate (compress.cpp:8-17) and the ring
+// layout require: for every written row (stamp != 0), indices inside the
+// handle's range, strictly increasing, and (blockwise) each block's entries
+// inside that block.
+ma_status check_window_rows(const ma_handle* h, int64_t step, int64_t head, const int64_t* stamps,
+                            const int64_t* win_indices) {
+    const Shape& s = h->shape;
+    const int64_t m = h->cfg.hp.window;
+    if (step < 0 || head < 0 || head >= m) return fail(MA_ERR_INVALID_ARG, "bad counters");
+    for (int64_t r = 0; r < m; ++r) {
+        if (stamps[r] == 0) continue;
+        const int64_t* row = win_indices + r * s.row_width;
+        for (int64_t j = 0; j < s.row_width; ++j) {
+            if (row[j] < s.elem0 || row[j] >= s.elem0 + s.dim)
+                return fail(MA_ERR_INVALID_ARG, "window index outside the vector");
+            if (j > 0 && row[j] <= row[j - 1])
+                return fail(MA_ERR_INVALID_ARG, "window row indices are not strictly increasing");
+        }
+        if (s.global) continue;
+        int64_t n = 0;
+        for (int64_t b = 0; b < s.b1 - s.b0; ++b) {
+            const int64_t start = s.elem0 + b * s.block;
+            const int64_t len = std::min(s.block, s.elem0 + s.dim - start);
+            const int64_t kb = std::min(s.per_block_k, len);
+            for (int64_t j = 0; j < kb; ++j, ++n)
+                if (row[n] < start || row[n] >= start + len)
+                    return fail(MA_ERR_INVALID_ARG, "window index outside its block");
+        }
+    }
+    return MA_OK;
+}
+}  // namespace
+
 ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, const double* hi,
                          int64_t step, int64_t head, const int64_t* stamps,
                          const int64_t* win_indices, const double* win_values) {
@@ -976,13 +1071,19 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
         return fail(MA_ERR_INVALID_ARG, "null argument");
     const Shape& s = h->shape;
     const int64_t m = h->cfg.hp.window;
-    if (step < 0 || head < 0 || head >= m) return fail(MA_ERR_INVALID_ARG, "bad counters");
+    { ma_status cs = check_window_rows(h, step, head, stamps, win_indices); if (cs != MA_OK) return cs; }
     DeviceGuard g(h->device);
-    MA_CUDA(cudaDeviceSynchronize());
-    MA_CUDA(cudaMemcpy(h->d_codes, codes, size_t(s.code_bytes), cudaMemcpyHostToDevice));
+    { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
+    // Everything is validated and staged on the host first; the device state
+    // changes only when the whole input is valid (SparseSelection::validate,
+    // compress.cpp:8-17: strictly increasing indices inside the vector).
     std::vector<double2> meta(size_t(s.nbuckets));
     for (size_t i = 0; i < meta.size(); ++i) meta[i] = make_double2(lo[i], hi[i]);
-    MA_CUDA(cudaMemcpy(h->d_meta, meta.data(), meta.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    auto commit_ef = [&]() -> ma_status {
+        MA_CUDA(cudaMemcpy(h->d_codes, codes, size_t(s.code_bytes), cudaMemcpyHostToDevice));
+        MA_CUDA(cudaMemcpy(h->d_meta, meta.data(), meta.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        return MA_OK;
+    };
     const int64_t nb = s.b1 - s.b0, kbs = s.kb_stride;
     const int vdt = h->cfg.value_dtype;
     const size_t vsz = dtype_size(vdt);
@@ -1008,9 +1109,12 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
                 const int64_t idx = win_indices[r * s.row_width + j];
                 if (stamps[r] != 0 && (idx < 0 || idx >= s.dim))
                     return fail(MA_ERR_INVALID_ARG, "window index outside the vector");
+                if (stamps[r] != 0 && j > 0 && idx <= win_indices[r * s.row_width + j - 1])
+                    return fail(MA_ERR_INVALID_ARG, "window row indices are not strictly increasing");
                 gi[size_t(r * kbs + j)] = int32_t(idx < 0 ? 0 : idx);
                 put_val(&gv[size_t(r * kbs + j) * vsz], win_values[r * s.row_width + j]);
             }
+        { ma_status cs = commit_ef(); if (cs != MA_OK) return cs; }
         MA_CUDA(cudaMemcpy(h->d_win_idx, gi.data(), gi.size() * 4, cudaMemcpyHostToDevice));
         MA_CUDA(cudaMemcpy(h->d_win_val, gv.data(), gv.size(), cudaMemcpyHostToDevice));
         h->step = step;
@@ -1031,6 +1135,8 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
                 const int64_t rel = win_indices[n] - s.elem0 - start;
                 if (stamps[r] != 0 && (rel < 0 || rel >= len))
                     return fail(MA_ERR_INVALID_ARG, "window index outside its block");
+                if (stamps[r] != 0 && j > 0 && win_indices[n] <= win_indices[n - 1])
+                    return fail(MA_ERR_INVALID_ARG, "window row indices are not strictly increasing");
                 const size_t q = size_t((b * m + r) * kbs + j);
                 idx[q] = int16_t(rel < 0 ? 0 : rel);
                 const double v = win_values[n];
@@ -1049,6 +1155,7 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
             }
         }
     }
+    { ma_status cs = commit_ef(); if (cs != MA_OK) return cs; }
     MA_CUDA(cudaMemcpy(h->d_win_idx, idx.data(), idx.size() * 2, cudaMemcpyHostToDevice));
     MA_CUDA(cudaMemset(h->d_thresh, 0, size_t(nb) * sizeof(uint32_t)));
     MA_CUDA(cudaMemcpy(h->d_win_val, val.data(), val.size(), cudaMemcpyHostToDevice));
@@ -1103,7 +1210,7 @@ ma_status ma_save_checkpoint(ma_handle* h, const void* params, int32_t params_on
     const Shape& s = h->shape;
     if (s.dim != s.dim_global) return fail(MA_ERR_UNSUPPORTED, "checkpoint: sharded handles are not supported");
     DeviceGuard g(h->device);
-    MA_CUDA(cudaDeviceSynchronize());
+    { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
     CkptFile cf;
     cf.f = std::fopen(path, "wb");
     if (!cf.f) return fail(MA_ERR_INVALID_ARG, std::string("checkpoint: cannot open ") + path + " for writing");
@@ -1166,6 +1273,9 @@ ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_devic
     cf.f = std::fopen(path, "rb");
     if (!cf.f) return fail(MA_ERR_INVALID_ARG, std::string("checkpoint: cannot open ") + path);
     std::FILE* f = cf.f;
+    if (std::fseek(f, 0, SEEK_END) != 0) return fail(MA_ERR_INVALID_ARG, "checkpoint: cannot seek");
+    const long long fsize = std::ftell(f);
+    std::rewind(f);
     unsigned char head8[6];
     if (!get_bytes(f, head8, 6)) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
     if (std::memcmp(head8, "MADM", 4) != 0) return fail(MA_ERR_INVALID_ARG, "checkpoint: bad magic");
@@ -1175,34 +1285,13 @@ ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_devic
     int64_t dim = 0, step = 0, cap = 0, rw = 0, head = 0, filled = 0;
     if (!get_i64(f, &dim) || !get_i64(f, &step)) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
     if (dim != s.dim) return fail(MA_ERR_DIM, "checkpoint: dimension differs from the optimizer's");
-    const int pdt = h->cfg.param_dtype;
-    const size_t psz = dtype_size(pdt);
-    std::vector<double> wide;
-    std::vector<unsigned char> raw;
-    for (int64_t i0 = 0; i0 < dim; i0 += int64_t(kCkptChunk)) {
-        const size_t n = size_t(std::min<int64_t>(int64_t(kCkptChunk), dim - i0));
-        wide.resize(n);
-        if (!get_f64s(f, wide.data(), n)) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
-        if (!params) continue;
-        raw.resize(n * psz);
-        for (size_t i = 0; i < n; ++i) {
-            if (pdt == MA_F64) {
-                std::memcpy(&raw[i * 8], &wide[i], 8);
-            } else if (pdt == MA_F32) {
-                const float x = float(wide[i]);
-                std::memcpy(&raw[i * 4], &x, 4);
-            } else {  // bf16: values written from a bf16 θ are exact; others round to nearest even
-                const float x = float(wide[i]);
-                uint32_t u;
-                std::memcpy(&u, &x, 4);
-                const uint16_t b = uint16_t((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
-                std::memcpy(&raw[i * 2], &b, 2);
-            }
-        }
-        unsigned char* dst = static_cast<unsigned char*>(params) + size_t(i0) * psz;
-        if (params_on_device) MA_CUDA(cudaMemcpy(dst, raw.data(), raw.size(), cudaMemcpyHostToDevice));
-        else std::memcpy(dst, raw.data(), raw.size());
-    }
+    // θ is read last (streamed): first parse and validate everything after it,
+    // so a malformed file leaves θ and the optimizer state untouched.
+    const long long theta_off = std::ftell(f);
+    if (theta_off < 0 || fsize - theta_off < static_cast<long long>(dim) * 8)
+        return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    if (std::fseek(f, static_cast<long>(theta_off + static_cast<long long>(dim) * 8), SEEK_SET) != 0)
+        return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
     if (!get_i64(f, &cap) || !get_i64(f, &rw) || !get_i64(f, &head) || !get_i64(f, &filled))
         return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
     const int64_t m = h->cfg.hp.window;
@@ -1215,36 +1304,74 @@ ma_status ma_load_checkpoint(ma_handle* h, void* params, int32_t params_on_devic
             !get_f64s(f, &val[size_t(r * rw)], size_t(rw)))
             return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
     }
-    if (h->d_dense) {  // lossless: dense error vector, then the window state
-        std::vector<double> ev(static_cast<size_t>(dim));
+    { ma_status cs = check_window_rows(h, step, head, stamps.data(), idx.data()); if (cs != MA_OK) return cs; }
+    std::vector<double> ev;
+    unsigned char bits = 0;
+    int64_t bucket = 0, nbk = 0, nbytes = 0;
+    std::vector<double> lo, hi;
+    std::vector<uint8_t> codes;
+    if (h->d_dense) {  // lossless: dense error vector after the window state
+        ev.resize(static_cast<size_t>(dim));
         if (!get_f64s(f, ev.data(), ev.size())) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    } else {
+        if (!get_bytes(f, &bits, 1) || !get_i64(f, &bucket) || !get_i64(f, &nbk))
+            return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+        if (bits != h->cfg.hp.bits || bucket != s.bucket || nbk != s.nbuckets)
+            return fail(MA_ERR_INVALID_ARG, "checkpoint: bucket count mismatch");
+        lo.resize(static_cast<size_t>(nbk));
+        hi.resize(static_cast<size_t>(nbk));
+        for (int64_t q = 0; q < nbk; ++q)
+            if (!get_f64s(f, &lo[size_t(q)], 1) || !get_f64s(f, &hi[size_t(q)], 1))
+                return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+        if (!get_i64(f, &nbytes) || nbytes != s.code_bytes)
+            return fail(MA_ERR_INVALID_ARG, "checkpoint: code length mismatch");
+        codes.resize(static_cast<size_t>(nbytes));
+        if (!get_bytes(f, codes.data(), codes.size())) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+    }
+    // The whole file is valid: θ, then the optimizer state.
+    if (params) {
+        if (std::fseek(f, static_cast<long>(theta_off), SEEK_SET) != 0)
+            return fail(MA_ERR_INVALID_ARG, "checkpoint: cannot seek");
+        const int pdt = h->cfg.param_dtype;
+        const size_t psz = dtype_size(pdt);
+        std::vector<double> wide;
+        std::vector<unsigned char> raw;
+        for (int64_t i0 = 0; i0 < dim; i0 += int64_t(kCkptChunk)) {
+            const size_t n = size_t(std::min<int64_t>(int64_t(kCkptChunk), dim - i0));
+            wide.resize(n);
+            if (!get_f64s(f, wide.data(), n)) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
+            raw.resize(n * psz);
+            for (size_t i = 0; i < n; ++i) {
+                if (pdt == MA_F64) {
+                    std::memcpy(&raw[i * 8], &wide[i], 8);
+                } else if (pdt == MA_F32) {
+                    const float x = float(wide[i]);
+                    std::memcpy(&raw[i * 4], &x, 4);
+                } else {  // bf16: values written from a bf16 θ are exact; others round to nearest even
+                    const float x = float(wide[i]);
+                    uint32_t u;
+                    std::memcpy(&u, &x, 4);
+                    const uint16_t b = uint16_t((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+                    std::memcpy(&raw[i * 2], &b, 2);
+                }
+            }
+            unsigned char* dst = static_cast<unsigned char*>(params) + size_t(i0) * psz;
+            if (params_on_device) MA_CUDA(cudaMemcpy(dst, raw.data(), raw.size(), cudaMemcpyHostToDevice));
+            else std::memcpy(dst, raw.data(), raw.size());
+        }
+    }
+    ma_status st;
+    if (h->d_dense) {
+        { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
         MA_CUDA(cudaMemcpy(h->d_dense, ev.data(), ev.size() * sizeof(double), cudaMemcpyHostToDevice));
         std::vector<uint8_t> zc(static_cast<size_t>(s.code_bytes), 0);
         std::vector<double> z0(static_cast<size_t>(s.nbuckets), 0.0);
-        ma_status st = ma_write_state(h, zc.data(), z0.data(), z0.data(), step, head, stamps.data(), idx.data(),
-                                      val.data());
-        if (st != MA_OK) return st;
-        if (params && !params_on_device) h->theta_valid = false;
-        h->host_synced = nullptr;
-        return MA_OK;
+        st = ma_write_state(h, zc.data(), z0.data(), z0.data(), step, head, stamps.data(), idx.data(), val.data());
+    } else {
+        // rows >= filled are unwritten (stamp 0): ma_write_state zero-fills them
+        st = ma_write_state(h, codes.data(), lo.data(), hi.data(), step, head, stamps.data(), idx.data(),
+                            val.data());
     }
-    unsigned char bits = 0;
-    int64_t bucket = 0, nbk = 0, nbytes = 0;
-    if (!get_bytes(f, &bits, 1) || !get_i64(f, &bucket) || !get_i64(f, &nbk))
-        return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
-    if (bits != h->cfg.hp.bits || bucket != s.bucket || nbk != s.nbuckets)
-        return fail(MA_ERR_INVALID_ARG, "checkpoint: bucket count mismatch");
-    std::vector<double> lo(static_cast<size_t>(nbk)), hi(static_cast<size_t>(nbk));
-    for (int64_t q = 0; q < nbk; ++q)
-        if (!get_f64s(f, &lo[size_t(q)], 1) || !get_f64s(f, &hi[size_t(q)], 1))
-            return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
-    if (!get_i64(f, &nbytes) || nbytes != s.code_bytes)
-        return fail(MA_ERR_INVALID_ARG, "checkpoint: code length mismatch");
-    std::vector<uint8_t> codes(static_cast<size_t>(nbytes));
-    if (!get_bytes(f, codes.data(), codes.size())) return fail(MA_ERR_INVALID_ARG, "checkpoint: truncated file");
-    // rows >= filled are unwritten (stamp 0): ma_write_state zero-fills them
-    ma_status st = ma_write_state(h, codes.data(), lo.data(), hi.data(), step, head, stamps.data(), idx.data(),
-                                  val.data());
     if (st != MA_OK) return st;
     if (params && !params_on_device) h->theta_valid = false;  // ma_step_host re-uploads θ
     h->host_synced = nullptr;
@@ -1280,18 +1407,22 @@ ma_status ma_step_front(ma_handle* h, const void* d_grads, int64_t block_begin, 
     a.params = nullptr;
     a.lr = h->cfg.hp.lr;
     a.lr32 = static_cast<float>(a.lr);
+    const CounterSnap snap = snap_counters(h);
     push_and_weights(h, &a);
     a.block_offset = block_begin;
     a.block_count = block_end - block_begin;
     a.stage_idx = static_cast<int16_t*>(d_stage_idx);
     a.stage_val = d_stage_val;
     a.stage_b0 = block_begin;
-    MA_CUDA(ma::launch_step_lean_phase(a, 1, st));
+    if (!h->pending) h->pending = new (std::nothrow) ma::StepArgs;
+    if (!h->pending) {
+        restore_counters(h, snap);
+        return fail(MA_ERR_INVALID_ARG, "out of host memory");
+    }
+    MA_CUDA_ROLLBACK(h, snap, ma::launch_step_lean_phase(a, 1, st));
     ++h->launches;
-    if (!h->pending) h->pending = new ma::StepArgs;
     *h->pending = a;
-    h->last_stream = st;
-    return MA_OK;
+    return mark_done(h, st);
 }
 
 ma_status ma_scatter_rows(ma_handle* h, const void* d_rows_idx, const void* d_rows_val, int64_t block_begin,
@@ -1331,8 +1462,7 @@ ma_status ma_step_stats(ma_handle* h, void* d_params, double lr, void* stream) {
     ++h->launches;
     delete h->pending;
     h->pending = nullptr;
-    h->last_stream = st;
-    return MA_OK;
+    return mark_done(h, st);
 }
 
 ma_status ma_get_layout(const ma_handle* h, ma_layout_info* out) {
@@ -1348,7 +1478,7 @@ ma_status ma_debug_counters(ma_handle* h, int64_t* out, int n) {
     DeviceGuard g(h->device);
     unsigned v[32] = {};
     if (h->d_dbg) {
-        MA_CUDA(cudaDeviceSynchronize());
+        { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
         MA_CUDA(cudaMemcpy(v, h->d_dbg, sizeof(v), cudaMemcpyDeviceToHost));
     }
     // [0, 8): event counters; [8, 20): per-phase warp cycles (MA_LEAN_PROF builds)

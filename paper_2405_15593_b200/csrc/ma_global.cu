@@ -839,12 +839,14 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
         const int n = e ? std::atoi(e) : 2;
         return n < 0 ? 0 : (n > 2 ? 2 : n);  // digit 3 collects: never the per-warp variant
     }();
-    static const bool g_hist_priv = [] {
+    static const bool g_hist_match = [] {
         const char* e = std::getenv("MA_GLOBAL_HIST_MATCH");  // A/B: match.any on every digit
-        if (e && e[0] == '1') return false;
-        return cudaFuncSetAttribute(g_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPrivSmem)) ==
-               cudaSuccess;
+        return e && e[0] == '1';
     }();
+    // the smem opt-in is per device / context: set it on every launch (cheap)
+    const bool g_hist_priv =
+        !g_hist_match &&
+        cudaFuncSetAttribute(g_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPrivSmem)) == cudaSuccess;
     g_sel_init<<<1, 1024, 0, s>>>(a, global_chunks(a.dim));
     // digit 3 collects the keys sharing the 22-bit prefix; digits 4-6 read
     // them (a few thousand keys) instead of re-decoding d elements

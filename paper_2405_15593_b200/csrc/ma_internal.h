@@ -135,6 +135,10 @@ bool lean_phase_ok(const StepArgs& a);
 cudaError_t launch_step_lean_phase(const StepArgs& a, int ph, cudaStream_t s);
 cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int* flag,
                                cudaStream_t s);
+// STRICT finiteness of a = g + e for f64 gradients (reference: check_finite in
+// topk_blockwise, compress.cpp:76), before any mutation.
+cudaError_t launch_finite_scan_a(const double* g, const uint8_t* codes, const double2* meta, const double* dense,
+                                 int64_t n, int64_t bucket, int bits, unsigned int* flag, cudaStream_t s);
 cudaError_t launch_report_reduce(const double* partials, int64_t nblocks, double* out5,
                                  cudaStream_t s);
 cudaError_t launch_gather_window_theta(const int16_t* win_idx, const void* theta, int pdt, void* out, int64_t b0,

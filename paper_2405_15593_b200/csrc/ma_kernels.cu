@@ -403,6 +403,34 @@ __global__ void finite_scan_kernel(const void* g, int dt, int64_t n, unsigned in
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
+// check_finite on a = g + e (compress.cpp:76 via topk_blockwise) for f64
+// gradients, the only dtype whose sum with a finite EF can overflow: e is the
+// decoded quantized buffer (quantize.cpp:164-178, LSB-first codes) or the
+// dense residual of a lossless engine.
+__global__ void finite_scan_a_kernel(const double* g, const uint8_t* codes, const double2* meta,
+                                     const double* dense, int64_t n, int64_t bucket, int bits,
+                                     unsigned int* flag) {
+    bool bad = false;
+    const uint32_t cmask = (1u << bits) - 1u;
+    const double max_code = static_cast<double>(cmask);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        double e;
+        if (dense) {
+            e = dense[i];
+        } else {
+            const double2 mt = meta[i / bucket];
+            const double level = mt.x == mt.y ? 0.0 : __ddiv_rn(__dsub_rn(mt.y, mt.x), max_code);
+            const int64_t pos = i * bits;
+            uint32_t w = codes[pos >> 3];
+            for (int k = 1; 8 * k < int(pos & 7) + bits; ++k) w |= uint32_t(codes[(pos >> 3) + k]) << (8 * k);
+            e = __dadd_rn(__dmul_rn(static_cast<double>((w >> (pos & 7)) & cmask), level), mt.x);
+        }
+        bad |= !isfinite(__dadd_rn(g[i], e));
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
 __global__ void report_reduce_kernel(const double* partials, int64_t nblocks, double* out) {
     __shared__ double red[1024 / 32][kReportFields];
     double v[kReportFields] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -498,6 +526,15 @@ cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int
     const int64_t want = (n + 255) / 256;
     const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
     finite_scan_kernel<<<grid, 256, 0, s>>>(g, dtype, n, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finite_scan_a(const double* g, const uint8_t* codes, const double2* meta, const double* dense,
+                                 int64_t n, int64_t bucket, int bits, unsigned int* flag, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t want = (n + 255) / 256;
+    const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
+    finite_scan_a_kernel<<<grid, 256, 0, s>>>(g, codes, meta, dense, n, bucket, bits, flag);
     return cudaGetLastError();
 }
 

@@ -106,7 +106,11 @@ Vec QuantizedErrorBuffer::decode() const {
     for (int64_t i = 0; i < dim; ++i) {
         const int64_t b = i / bucket;
         const double lvl = lo[size_t(b)] == hi[size_t(b)] ? 0.0 : (hi[size_t(b)] - lo[size_t(b)]) / mx;
-        const uint32_t c = (codes[size_t(i / 2)] >> ((i & 1) * 4)) & 15u;
+        // LSB-first bit stream of `bits`-wide codes (quantize.cpp:102-128)
+        const int64_t pos = i * bits;
+        uint32_t w = codes[size_t(pos >> 3)];
+        for (int k = 1; 8 * k < int(pos & 7) + bits; ++k) w |= uint32_t(codes[size_t((pos >> 3) + k)]) << (8 * k);
+        const uint32_t c = (w >> (pos & 7)) & ((1u << bits) - 1u);
         out[size_t(i)] = static_cast<double>(c) * lvl + lo[size_t(b)];
     }
     return out;

@@ -137,12 +137,14 @@ private:
     HyperParams hp_;
 };
 
-// Drop-in for microadam::MicroAdamOptimizer(theta0, hp, blockwise=true):
+// Drop-in for microadam::MicroAdamOptimizer(theta0, hp, blockwise = false,
+// lossless_error = false) (optim.hpp:103-104: the same defaults, so code written
+// against the reference selects global Top-K here too):
 // host vectors in and out, fp64 θ/g/window on the device, strict
 // (reject-before-mutate) finiteness — bit-identical to the reference step.
 class MicroAdamOptimizer : public Optimizer {
 public:
-    MicroAdamOptimizer(Vec theta0, HyperParams hp, bool blockwise = true,
+    MicroAdamOptimizer(Vec theta0, HyperParams hp, bool blockwise = false,
                        bool lossless_error = false, int device = 0);
     ~MicroAdamOptimizer() override;
     StepReport step(const Vec& grad) override;

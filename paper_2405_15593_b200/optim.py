@@ -152,10 +152,11 @@ class QuantizedErrorBuffer:
 
     def decode(self) -> np.ndarray:
         """quantize.cpp:164-178 (separate multiply and add, fp64)."""
-        codes = np.empty(self.codes.size * 2, np.uint8)
-        codes[0::2] = self.codes & 15
-        codes[1::2] = self.codes >> 4
-        codes = codes[: self.dim].astype(np.float64)
+        # LSB-first bit stream of `bits`-wide codes (quantize.cpp:102-128)
+        bitstream = np.unpackbits(self.codes, bitorder="little")
+        pos = np.arange(self.dim, dtype=np.int64)[:, None] * self.bits + np.arange(self.bits)[None, :]
+        weights = (1 << np.arange(self.bits, dtype=np.int64))[None, :]
+        codes = (bitstream[pos].astype(np.int64) * weights).sum(axis=1).astype(np.float64)
         b = np.arange(self.dim) // self.bucket
         lvl = np.where(self.lo == self.hi, 0.0, (self.hi - self.lo) / float((1 << self.bits) - 1))
         return codes * lvl[b] + self.lo[b]
@@ -417,11 +418,11 @@ def _buffer(x):
 
 
 class MicroAdamOptimizer(_Handle):
-    """Drop-in for microadam::MicroAdamOptimizer(theta0, hp, blockwise=true)
-    (optim.hpp:98-128): host fp64 vectors in and out, fp64 on the device,
+    """Drop-in for microadam::MicroAdamOptimizer(theta0, hp, blockwise=false,
+    lossless_error=false) (optim.hpp:98-128, same defaults as optim.hpp:103-104): host fp64 vectors in and out, fp64 on the device,
     reject-before-mutate finiteness — bit-identical to the reference step."""
 
-    def __init__(self, theta0, hp=None, blockwise: bool = True, lossless_error: bool = False,
+    def __init__(self, theta0, hp=None, blockwise: bool = False, lossless_error: bool = False,
                  device: int = 0):
         self.hp = HyperParams.from_any(hp)
         self._theta = np.array(theta0, dtype=np.float64, copy=True)

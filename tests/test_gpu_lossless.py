@@ -25,7 +25,7 @@ def _bits(x):
 def test_lossless_matches_reference_and_conserves(d, hp):
     from paper_2405_15593_b200 import MicroAdamOptimizer
     th0 = oracle.synth(1, 0, 0, d)
-    opt = MicroAdamOptimizer(th0, hp, lossless_error=True)
+    opt = MicroAdamOptimizer(th0, hp, blockwise=True, lossless_error=True)
     ref = oracle.Reference(th0, hp, lossless=True)
     assert opt.lossless()
     e_prev = np.zeros(d)
@@ -54,7 +54,7 @@ def test_lossless_checkpoint_bytes_equal_reference(tmp_path):
     d, hp = 20_000, dict(lr=1e-2, window=3)
     th0 = oracle.synth(1, 0, 0, d)
     ref = oracle.Reference(th0, hp, lossless=True)
-    opt = MicroAdamOptimizer(th0, hp, lossless_error=True)
+    opt = MicroAdamOptimizer(th0, hp, blockwise=True, lossless_error=True)
     for s in range(1, 6):
         g = oracle.synth(42, s, 0, d)
         ref.step(g)
@@ -63,7 +63,7 @@ def test_lossless_checkpoint_bytes_equal_reference(tmp_path):
     ref.save_checkpoint(a)
     opt.save_checkpoint(b)
     assert open(a, "rb").read() == open(b, "rb").read()
-    resumed = MicroAdamOptimizer(np.zeros(d), hp, lossless_error=True)
+    resumed = MicroAdamOptimizer(np.zeros(d), hp, blockwise=True, lossless_error=True)
     resumed.load_checkpoint(b)
     for s in range(6, 9):
         g = oracle.synth(42, s, 0, d)

@@ -232,7 +232,7 @@ def test_host_dropin_matches_reference():
     from paper_2405_15593_b200 import MicroAdamOptimizer
     d, hp = 50_000, dict(lr=1e-2, window=4)
     theta0 = oracle.synth(1, 0, 0, d)
-    opt = MicroAdamOptimizer(theta0, hp)
+    opt = MicroAdamOptimizer(theta0, hp, blockwise=True)
     orc = oracle.Oracle(theta0, hp)
     ref = oracle.Reference(theta0, hp) if oracle.reference_available() else None
     assert opt.name() == "microadam"
