@@ -81,6 +81,19 @@ def parse():
     return ap.parse_args()
 
 
+# The gradient stream of the timed loop: step i (0-based, warm-up included)
+# reads resident buffer i % n_grads — ma_synth stream step (i % n_grads) + 1 —
+# at element offset off(i), so no step repeats an earlier gradient. Shared with
+# tests/test_gpu_scale.py, which replays it against the oracle.
+SHIFT = 64 * 4096
+STEP8 = 1283  # offset step in units of 8 elements (16-byte aligned for bf16)
+
+
+def grad_source(i: int, n_grads: int):
+    """(ma_synth step, element offset) of the gradient bench step i reads."""
+    return (i % n_grads) + 1, ((i // n_grads) * STEP8 * 8) % SHIFT
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -306,8 +319,6 @@ def run_ours(args):
     # and step i reads buffer i % B at offset (i // B) * STEP8 * 8 elements.
     # Re-feeding an identical gradient every B steps (B < m) would make the
     # window and the EF see exact repeats, which real training never produces.
-    SHIFT = 64 * 4096
-    STEP8 = 1283  # offset step in units of 8 elements (16-byte aligned for bf16)
     free, _ = torch.cuda.mem_get_info()
     gbytes = (n + SHIFT) * DT_BYTES[gdt]
     reserve = 2 * n * DT_BYTES[gdt] + (8 << 30)  # e2e staging (θ + g copies) + headroom
@@ -318,8 +329,8 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     def grad_view(i):
-        off = ((i // n_grads) * STEP8 * 8) % SHIFT
-        return grads[i % n_grads][off: off + n]
+        j, off = grad_source(i, n_grads)
+        return grads[j - 1][off: off + n]
 
     nb_all = d // hp.block
 

@@ -48,4 +48,28 @@ MA_HD double ma_synth_levels(uint64_t seed, uint64_t step, uint64_t index) {
     return (double)(int64_t)(h & 15u) - 7.5;
 }
 
+/* Heavy-tailed, scale-varying variant (test and bench stress input): the
+ * Gaussian-like value times 2^(e_block + e_tail), where e_block in [-16, 16]
+ * is drawn per 4096-element block and changes every 4 steps (gradient scale
+ * differing by 2^32 across blocks and drifting over time), and e_tail in
+ * [0, 12] is nonzero for 1 element in 64 (outliers up to 2^12 times the
+ * block's scale). Every value is an exact fp32 (|x| < 2^15, multiples of
+ * 2^-31), so host and device round it to bf16 identically. */
+MA_HD double ma_synth_heavy(uint64_t seed, uint64_t step, uint64_t index) {
+    uint64_t hb = ma_synth_hash(seed ^ 0xB10CB10CB10CB10Cull, step >> 2, index >> 12);
+    int eb = (int)(hb % 33u) - 16;
+    uint64_t ht = ma_synth_hash(seed ^ 0x7A117A117A117A11ull, step, index);
+    int et = (ht & 63u) == 0 ? (int)((ht >> 6) % 13u) : 0;
+    int e = eb + et;
+    double scale = 1.0;
+    for (int k = 0; k < (e < 0 ? -e : e); ++k) scale = e < 0 ? scale * 0.5 : scale * 2.0;
+    return ma_synth_normal(seed, step, index) * scale;
+}
+
+/* mode 0: ma_synth_normal, 1: ma_synth_levels, 2: ma_synth_heavy */
+MA_HD double ma_synth_value(int mode, uint64_t seed, uint64_t step, uint64_t index) {
+    return mode == 1 ? ma_synth_levels(seed, step, index)
+                     : (mode == 2 ? ma_synth_heavy(seed, step, index) : ma_synth_normal(seed, step, index));
+}
+
 #endif /* MA_SYNTH_H */

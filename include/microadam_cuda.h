@@ -187,6 +187,19 @@ MA_API ma_status ma_read_error_buffer(ma_handle* h, uint8_t* codes, double* lo, 
  * like error_buffer() throwing std::logic_error, optim.cpp:155-158). */
 MA_API ma_status ma_read_error_vector(ma_handle* h, double* out);
 
+/* error_buffer() restricted to blocks [block_begin, block_end) of the handle:
+ * their packed codes (elements [block_begin*block, min(block_end*block, dim)),
+ * byte-aligned since block*bits is a multiple of 8) and their buckets' (lo, hi).
+ * For parity checks of sampled block ranges of very large handles. */
+MA_API ma_status ma_read_error_buffer_blocks(ma_handle* h, int64_t block_begin, int64_t block_end, uint8_t* codes,
+                                             double* lo, double* hi);
+
+/* window().rows[slot] restricted to blocks [block_begin, block_end): the
+ * Σ min(per_block_k, len_b) entries of those blocks, global int64 indices
+ * (ascending) and values widened to fp64. */
+MA_API ma_status ma_read_window_blocks(ma_handle* h, int64_t slot, int64_t block_begin, int64_t block_end,
+                                       int64_t* indices, double* values);
+
 /* window().rows[slot] in the reference layout: row_width global int64 indices
  * (ascending) and values widened to fp64. Returns MA_ERR_INVALID_ARG for slot
  * out of range. An unwritten row reads back as zeros. */
@@ -250,7 +263,9 @@ MA_API const char* ma_last_error(void);
 MA_API const char* ma_version(void);
 
 /* Synthetic gradient generator on device (include/ma_synth.h stream rounded
- * to dtype), for benches: out[i] = round(value(seed, step, offset + i)). */
+ * to dtype), for benches: out[i] = round(value(seed, step, offset + i));
+ * levels = 0 Gaussian-like, 1 the 16-level tie-heavy stream, 2 heavy-tailed
+ * with per-block scales (ma_synth_heavy). */
 MA_API ma_status ma_fill_synthetic(void* d_out, int32_t dtype, int64_t n, uint64_t seed, uint64_t step,
                             int64_t offset, int32_t levels, void* stream);
 

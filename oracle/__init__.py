@@ -349,10 +349,13 @@ class Reference:
                      last_idx, last_val)
 
 
-def synth(seed: int, step: int, offset: int, n: int, dtype: str = "f64", levels: bool = False) -> np.ndarray:
-    """The include/ma_synth.h stream, rounded to dtype (float64 array)."""
+def synth(seed: int, step: int, offset: int, n: int, dtype: str = "f64", levels: bool = False,
+          heavy: bool = False) -> np.ndarray:
+    """The include/ma_synth.h stream, rounded to dtype (float64 array): Gaussian-like,
+    16 tie-heavy levels (levels=True) or heavy-tailed per-block-scaled (heavy=True)."""
     out = np.empty(n, np.float64)
-    oracle_lib().mo_synth_fill(seed, step, offset, n, DTYPES[dtype], int(levels), out)
+    mode = 2 if heavy else (1 if levels else 0)
+    oracle_lib().mo_synth_fill(seed, step, offset, n, DTYPES[dtype], mode, out)
     return out
 
 

@@ -392,8 +392,7 @@ const double* mo_win_val(const mo_opt* o) { return o->win_val; }
 void mo_synth_fill(uint64_t seed, uint64_t step, int64_t offset, int64_t n, int dtype, int levels,
                    double* out) {
     for (int64_t i = 0; i < n; ++i) {
-        double v = levels ? ma_synth_levels(seed, step, (uint64_t)(offset + i))
-                          : ma_synth_normal(seed, step, (uint64_t)(offset + i));
+        double v = ma_synth_value(levels, seed, step, (uint64_t)(offset + i));
         out[i] = mo_round(v, dtype);
     }
 }

@@ -27,7 +27,7 @@ EXPORTED = [
     "ma_read_window_row", "ma_write_state", "ma_set_params", "ma_get_layout",
     "ma_kernel_launches", "ma_last_error", "ma_version", "ma_fill_synthetic", "ma_debug_counters",
     "ma_save_checkpoint", "ma_load_checkpoint", "ma_step_front", "ma_scatter_rows", "ma_step_stats",
-    "ma_read_error_vector", "ma_step_reduce",
+    "ma_read_error_vector", "ma_step_reduce", "ma_read_error_buffer_blocks", "ma_read_window_blocks",
 ]
 
 
@@ -96,6 +96,8 @@ def lib():
     L.ma_get_counters.argtypes = [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(C.c_int64)]
     L.ma_read_error_buffer.argtypes = [vp, vp, vp, vp]
     L.ma_read_window_row.argtypes = [vp, C.c_int64, vp, vp]
+    L.ma_read_error_buffer_blocks.argtypes = [vp, C.c_int64, C.c_int64, vp, vp, vp]
+    L.ma_read_window_blocks.argtypes = [vp, C.c_int64, C.c_int64, C.c_int64, vp, vp]
     L.ma_read_error_vector.argtypes = [vp, vp]
     L.ma_write_state.argtypes = [vp, vp, vp, vp, C.c_int64, C.c_int64, vp, vp, vp]
     L.ma_set_params.argtypes = [vp, vp]

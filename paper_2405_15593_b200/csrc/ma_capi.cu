@@ -949,6 +949,34 @@ ma_status ma_read_error_buffer(ma_handle* h, uint8_t* codes, double* lo, double*
     return MA_OK;
 }
 
+ma_status ma_read_error_buffer_blocks(ma_handle* h, int64_t block_begin, int64_t block_end, uint8_t* codes,
+                                      double* lo, double* hi) {
+    if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
+    if (h->d_dense) return fail(MA_ERR_STATE, "error_buffer: engine uses dense error storage");
+    const Shape& s = h->shape;
+    if (s.global) return fail(MA_ERR_UNSUPPORTED, "error_buffer_blocks: blockwise handles only");
+    if (block_begin < 0 || block_end > s.b1 - s.b0 || block_begin >= block_end)
+        return fail(MA_ERR_INVALID_ARG, "block range outside the handle");
+    DeviceGuard g(h->device);
+    { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
+    const int64_t e0 = block_begin * s.block, e1 = std::min(s.dim, block_end * s.block);
+    const int64_t bits = h->cfg.hp.bits;
+    if (codes) {
+        const int64_t c0 = (e0 * bits) / 8, c1 = (e1 * bits + 7) / 8;
+        MA_CUDA(cudaMemcpy(codes, h->d_codes + c0, size_t(c1 - c0), cudaMemcpyDeviceToHost));
+    }
+    if (lo || hi) {
+        const int64_t q0 = e0 / s.bucket, q1 = (e1 + s.bucket - 1) / s.bucket;
+        std::vector<double2> meta(size_t(q1 - q0));
+        MA_CUDA(cudaMemcpy(meta.data(), h->d_meta + q0, meta.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < meta.size(); ++i) {
+            if (lo) lo[i] = meta[i].x;
+            if (hi) hi[i] = meta[i].y;
+        }
+    }
+    return MA_OK;
+}
+
 namespace {
 double widen(const void* p, int dt, size_t i) {
     if (dt == MA_F64) return static_cast<const double*>(p)[i];
@@ -984,6 +1012,38 @@ ma_status ma_read_error_vector(ma_handle* h, double* out) {
         for (int k = 1; 8 * k < int(pos & 7) + bits; ++k) w |= uint32_t(codes[size_t((pos >> 3) + k)]) << (8 * k);
         const double c = double((w >> (pos & 7)) & ((1u << bits) - 1u));
         out[i] = c * level + m.x;
+    }
+    return MA_OK;
+}
+
+ma_status ma_read_window_blocks(ma_handle* h, int64_t slot, int64_t block_begin, int64_t block_end,
+                                int64_t* indices, double* values) {
+    if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
+    if (slot < 0 || slot >= h->cfg.hp.window) return fail(MA_ERR_INVALID_ARG, "slot out of range");
+    const Shape& s = h->shape;
+    if (s.global) return fail(MA_ERR_UNSUPPORTED, "window_blocks: blockwise handles only");
+    if (block_begin < 0 || block_end > s.b1 - s.b0 || block_begin >= block_end)
+        return fail(MA_ERR_INVALID_ARG, "block range outside the handle");
+    DeviceGuard g(h->device);
+    { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
+    const int64_t nb = block_end - block_begin, m = h->cfg.hp.window, kbs = s.kb_stride;
+    const size_t vsz = dtype_size(h->cfg.value_dtype);
+    std::vector<int16_t> idx(size_t(nb * kbs));
+    std::vector<unsigned char> val(size_t(nb * kbs) * vsz);
+    const int64_t q = (block_begin * m + slot) * kbs;
+    MA_CUDA(cudaMemcpy2D(idx.data(), size_t(kbs) * 2, h->d_win_idx + q, size_t(m * kbs) * 2, size_t(kbs) * 2,
+                         size_t(nb), cudaMemcpyDeviceToHost));
+    MA_CUDA(cudaMemcpy2D(val.data(), size_t(kbs) * vsz, static_cast<char*>(h->d_win_val) + size_t(q) * vsz,
+                         size_t(m * kbs) * vsz, size_t(kbs) * vsz, size_t(nb), cudaMemcpyDeviceToHost));
+    int64_t n = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t start = (block_begin + b) * s.block;
+        const int64_t len = std::min(s.block, s.dim - start);
+        const int64_t kb = std::min(s.per_block_k, len);
+        for (int64_t j = 0; j < kb; ++j, ++n) {
+            if (indices) indices[n] = s.elem0 + start + idx[size_t(b * kbs + j)];
+            if (values) values[n] = widen(val.data(), h->cfg.value_dtype, size_t(b * kbs + j));
+        }
     }
     return MA_OK;
 }

@@ -478,7 +478,7 @@ __global__ void fill_synthetic_kernel(void* out, int dt, int64_t n, uint64_t see
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const uint64_t gi = static_cast<uint64_t>(offset + i);
-        const double v = levels ? ma_synth_levels(seed, step, gi) : ma_synth_normal(seed, step, gi);
+        const double v = ma_synth_value(levels, seed, step, gi);
         st_val(out, dt, i, v);
     }
 }

@@ -236,6 +236,32 @@ class _Handle:
         _ok(lib().ma_read_error_buffer(self._h, codes.ctypes.data, lo.ctypes.data, hi.ctypes.data))
         return QuantizedErrorBuffer(lay.dim, self.cfg.hp.bits, self.cfg.hp.bucket, codes, lo, hi)
 
+    def error_buffer_blocks(self, block_begin: int, block_end: int):
+        """error_buffer() of blocks [block_begin, block_end): (codes, lo, hi)."""
+        lay = self.layout
+        e0 = block_begin * lay.block
+        e1 = min(lay.dim, block_end * lay.block)
+        bits, bucket = self.cfg.hp.bits, self.cfg.hp.bucket
+        codes = np.zeros((e1 * bits + 7) // 8 - (e0 * bits) // 8, np.uint8)
+        nq = (e1 + bucket - 1) // bucket - e0 // bucket
+        lo = np.zeros(nq)
+        hi = np.zeros(nq)
+        _ok(lib().ma_read_error_buffer_blocks(self._h, block_begin, block_end, codes.ctypes.data,
+                                              lo.ctypes.data, hi.ctypes.data))
+        return codes, lo, hi
+
+    def window_blocks(self, slot: int, block_begin: int, block_end: int):
+        """window().rows[slot] restricted to blocks [block_begin, block_end): (indices, values)."""
+        lay = self.layout
+        n = 0
+        for b in range(block_begin, block_end):
+            n += min(lay.per_block_k, min(lay.block, lay.dim - b * lay.block))
+        idx = np.zeros(n, np.int64)
+        val = np.zeros(n, np.float64)
+        _ok(lib().ma_read_window_blocks(self._h, slot, block_begin, block_end, idx.ctypes.data,
+                                        val.ctypes.data))
+        return idx, val
+
     def write_state(self, codes, lo, hi, step, head, stamps, win_idx, win_val) -> None:
         a = [np.ascontiguousarray(codes, np.uint8), np.ascontiguousarray(lo, np.float64),
              np.ascontiguousarray(hi, np.float64), np.ascontiguousarray(stamps, np.int64),

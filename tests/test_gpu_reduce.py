@@ -133,3 +133,39 @@ def test_fused_reduce_on_block_shards():
         torch.cuda.synchronize()
         for eng, e0, e1, p in shards:
             assert torch.equal(p.view(torch.int16), p_full[e0:e1].view(torch.int16)), f"shard θ @ {s}"
+
+
+@pytest.mark.parametrize("dt,nsrc", [("bf16", 4), ("f32", 3)])
+def test_fused_reduce_matches_oracle(dt, nsrc):
+    """ma_step_reduce against the composed oracle fed the torch-reduced gradient
+    (optim.cpp:166-168: the step's a = g + e with g the reduced gradient)."""
+    import torch
+
+    import oracle
+    from paper_2405_15593_b200 import MicroAdam
+    oracle.build()
+    d, hp = 36 * BLK + 700, dict(lr=1e-3, window=4)
+    th0 = oracle.synth(1, 0, 0, d, dt)
+    eng = MicroAdam(d, hp, param_dtype=dt, grad_dtype=dt, value_dtype="bf16")
+    orc = oracle.Oracle(th0, hp, param_dtype=dt, value_dtype="bf16")
+    p = torch.from_numpy(th0).to(_tdt(dt)).cuda()
+    for s in range(1, 9):
+        srcs = [torch.from_numpy(oracle.synth(42 + r, s, 0, d, heavy=s % 2 == 0) * (0.5 + r)).to(_tdt(dt)).cuda()
+                for r in range(nsrc)]
+        out = torch.empty_like(srcs[0])
+        eng.step_reduce(p, out, srcs, 1.0 / nsrc, hp["lr"])
+        g = _reduce(srcs, 1.0 / nsrc).to(torch.float64).cpu().numpy()
+        orc.step(g, hp["lr"])
+        torch.cuda.synchronize()
+        so = orc.state()
+        assert np.array_equal(out.to(torch.float64).cpu().numpy().view(np.uint64), g.view(np.uint64))
+        assert np.array_equal(p.to(torch.float64).cpu().numpy().view(np.uint64), so.params.view(np.uint64)), \
+            f"θ vs oracle @ {s}"
+        eb = eng.error_buffer()
+        assert np.array_equal(eb.codes, so.codes), f"EF codes vs oracle @ {s}"
+        assert np.array_equal(eb.lo.view(np.uint64), so.lo.view(np.uint64))
+        assert np.array_equal(eb.hi.view(np.uint64), so.hi.view(np.uint64))
+        win = eng.window()
+        for r in range(so.filled):
+            assert np.array_equal(win.indices[r], so.win_idx[r]), f"row {r} @ {s}"
+            assert np.array_equal(win.values[r].view(np.uint64), so.win_val[r].view(np.uint64))

@@ -93,3 +93,45 @@ def test_split_calls_out_of_order_are_rejected():
     stage = eng.stage_buffers(4)
     with pytest.raises(RuntimeError, match="no ma_step_front"):
         eng.scatter_rows(stage, 0, 4)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_simulated_ranks_match_oracle(world):
+    """Sparse propagation across simulated ranks against the composed oracle
+    (not against the library's own ma_step): every replica's θ, window rows and
+    each rank's EF blocks after every step. Anchors: optim.cpp:183-187 (update
+    support ⊆ window rows), window.cpp:28-46."""
+    import torch
+    from paper_2405_15593_b200 import sharding
+    oracle.build()
+    d, hp = BLK * 18, dict(lr=1e-2, window=5)
+    nb = d // BLK
+    th0 = oracle.synth(1, 0, 0, d, "bf16")
+    orc = oracle.Oracle(th0, hp, param_dtype="bf16", value_dtype="bf16")
+    ranks = []
+    for r in range(world):
+        b0, b1, e0, e1 = sharding.partition_blocks(d, BLK, world, r)
+        eng = _eng(d, hp)
+        ranks.append(dict(eng=eng, b0=b0, b1=b1, e0=e0, e1=e1, p=_dev(th0), stage=eng.stage_buffers(b1 - b0)))
+    for s in range(1, 11):
+        gh = oracle.synth(42, s, 0, d, "bf16", heavy=True)
+        g = _dev(gh)
+        orc.step(gh, 1e-2)
+        for rk in ranks:
+            rk["eng"].step_front(g[rk["e0"]:rk["e1"]].clone(), rk["b0"], rk["b1"], rk["stage"])
+        gathered = (torch.cat([rk["stage"][0] for rk in ranks]), torch.cat([rk["stage"][1] for rk in ranks]))
+        for rk in ranks:
+            rk["eng"].scatter_rows(gathered, 0, nb)
+            rk["eng"].step_stats(rk["p"], 1e-2)
+        torch.cuda.synchronize()
+        so = orc.state()
+        for rk in ranks:
+            got = rk["p"].to(torch.float64).cpu().numpy()
+            assert np.array_equal(got.view(np.uint64), so.params.view(np.uint64)), f"θ replica vs oracle @ {s}"
+            win = rk["eng"].window()
+            for r in range(so.filled):
+                assert np.array_equal(win.indices[r], so.win_idx[r]), f"row {r} @ {s}"
+            codes, lo, _ = rk["eng"].error_buffer_blocks(rk["b0"], rk["b1"])
+            c0, c1 = rk["e0"] // 2, rk["e1"] // 2
+            assert np.array_equal(codes, so.codes[c0:c1]), f"EF codes of rank blocks @ {s}"
+            assert np.array_equal(lo.view(np.uint64), so.lo[rk["e0"] // 64: rk["e1"] // 64].view(np.uint64))
