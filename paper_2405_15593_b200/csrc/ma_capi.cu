@@ -176,6 +176,7 @@ struct ma_handle {
     bool fast = false;  // ma_fast.cu / ma_warp.cu kernel (else the generic ma_kernels.cu kernel)
     bool warp = false;  // fast path runs the warp-per-block kernel (ma_warp.cu)
     bool warp_exact = false;  // MA_WARP_EXACT=1: never the fp32-screened (lean) warp kernel
+    bool tile = false;  // ma_tile.cu kernel where it applies (MA_TILE=0: the warp kernels)
     int persist_grid = 0;
     int device = 0;
     uint8_t* d_codes = nullptr;
@@ -384,8 +385,9 @@ cudaError_t launch(ma_handle* h, ma::StepArgs& a, int64_t nblocks, cudaStream_t 
     if (nfull > 0) {
         a.block_count = nfull;
         const int64_t grid = std::min<int64_t>(nfull, h->persist_grid);
-        cudaError_t e = (h->warp && ma::warp_can_run(a)) ? ma::launch_step_warp(a, st)
-                                                        : ma::launch_step_fast(a, h->variant, int(grid), st);
+        cudaError_t e = (h->tile && ma::tile_ok(a))               ? ma::launch_step_tile(a, st)
+                        : (h->warp && ma::warp_can_run(a)) ? ma::launch_step_warp(a, st)
+                                                           : ma::launch_step_fast(a, h->variant, int(grid), st);
         if (e != cudaSuccess) return e;
     }
     if (tail_partial) {
@@ -634,13 +636,17 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         h->warp = true;
     const char* warp_exact = std::getenv("MA_WARP_EXACT");
     h->warp_exact = warp_exact && warp_exact[0] == '1';
+    // MA_TILE=1: the TMA-fed CTA-per-block kernel (ma_tile.cu) where it applies;
+    // the lean warp kernel stays the default (faster on B200)
+    const char* tile_env = std::getenv("MA_TILE");
+    h->tile = h->warp && !h->warp_exact && tile_env && tile_env[0] == '1';
     if (!h->fast) h->variant = h->tail_variant;
     if (s.global) {
-        h->fast = h->warp = false;
+        h->fast = h->warp = h->tile = false;
         smem = ma::global_requant_smem(s.bucket);
     }
     if (cfg->lossless_error || cfg->hp.bits != 4) {  // dense EF / other code widths: the generic kernel
-        h->fast = h->warp = false;
+        h->fast = h->warp = h->tile = false;
         h->variant = h->tail_variant;
     }
     if (smem > size_t(smem_max)) {

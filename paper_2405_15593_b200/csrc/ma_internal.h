@@ -128,6 +128,10 @@ bool warp_path_ok(int block, int bucket, int kb, int m, int kb_stride, int g_dty
                   int v_dtype);
 size_t warp_smem_bytes(int bucket);
 cudaError_t launch_step_warp(const StepArgs& a, cudaStream_t s);
+// Tile kernel (ma_tile.cu, the default): persistent 128-thread CTAs, one
+// B_d = 4096 / B_q = 64 block at a time, TMA-fed double-buffered stages.
+bool tile_ok(const StepArgs& a);
+cudaError_t launch_step_tile(const StepArgs& a, cudaStream_t s);
 // Whether the warp kernels run this step (the exact one needs k_b <= 64).
 bool warp_can_run(const StepArgs& a);
 // Lean kernel split for sparse parameter propagation (ph 1 = front, 2 = stats).

@@ -1066,10 +1066,12 @@ __device__ __noinline__ bool dup_chunks(const StepArgs* pp, unsigned char* ws, i
         s_dpref[lane * 4 + k] = run;
         run += __popc(dv[k]);
     }
-    // running sums of up to zcap coordinates at a time (pass-2 tables are dead)
+    // running sums of up to zcap coordinates at a time in the dead pass-2
+    // tables and selection bits (ll, llf, sel) — NOT into wpref (s_dpref) or
+    // dup (s_dup), which this loop still reads
     double2* zz = reinterpret_cast<double2*>(ws + L.ll);
     int16_t* zc = reinterpret_cast<int16_t*>(ws + L.cidx);
-    const int zcap = min(static_cast<int>((L.cval - L.ll) / 16), static_cast<int>((L.misc - L.cidx) / 2));
+    const int zcap = min(static_cast<int>((L.wpref - L.ll) / 16), static_cast<int>((L.misc - L.cidx) / 2));
     __syncwarp();
     for (int id0 = 0; id0 < ndupc; id0 += zcap) {
         const int nz = min(zcap, ndupc - id0);
