@@ -9,12 +9,17 @@ A "step" is one MicroAdamOptimizer::step (optim.cpp:164-190) over the whole
 workload vector: EF decode + accumulate, block Top-K, 4-bit re-quantization,
 window-ring write, ADAM_STATS + update — one fused kernel launch per step.
 At N>1 (torchrun, one rank per GPU) the parameter space is block-sharded.
---mode shard (default): rank r steps blocks [r nb, (r+1) nb) of an N x 7B
-vector — the step partitions with no data-path exchange, so no collective
-runs inside the timed loop (weak scaling). --mode allgather: the 7B vector is
-split over the ranks (paper_2405_15593_b200/sharding.py) and every step ends
-with the NCCL all-gather of the updated bf16 θ shards into each rank's full
-replica (strong scaling, the north star's ZeRO-1 layout).
+--mode allgather (default, the north star's layout): the 7B vector's blocks
+are split over the ranks (paper_2405_15593_b200/sharding.py) and every step
+is the rank's shard step followed by the NCCL all-gather of the updated bf16
+θ shards into each rank's full replica — ma_step_allgather's two halves
+(ma_step + ma_allgather_params) through the C ABI on the library's own NCCL
+communicator (strong scaling; step_only and the collective's GB/s are in the
+same line). --mode sparse: the EF / Top-K front is sharded, the new window
+rows are all-gathered (ma_exchange_rows) and ADAM_STATS + update run on every
+rank's replica. --mode shard: rank r steps its own 7B-sized block range of an
+N x 7B vector with no collective (weak scaling). Every timed step runs with a
+full window: max(W, m) untimed steps come first.
 
 Default workload = BASELINE.json configs[3] (Llama-2-7B-sized vector,
 6,738,415,616 params, bf16 θ/g) — the config the headline metric is quoted on;
@@ -70,14 +75,19 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-shard-blocks", type=int, default=128)
-    ap.add_argument("--mode", default="shard", choices=["shard", "allgather", "sparse"],
-                    help="N>1: 'shard' = each rank steps its own workload-sized block range of an "
-                         "N x workload vector, no data-path collective (weak scaling); 'allgather' = "
-                         "the workload split across ranks + NCCL all-gather of bf16 θ each step "
-                         "(strong scaling, ZeRO-1 style); 'sparse' = the workload split across ranks "
-                         "for the EF / Top-K front, NCCL all-gather of the new window rows only, "
-                         "ADAM_STATS + update replicated on every rank's θ (strong scaling)")
+    ap.add_argument("--cpu-shard-blocks", type=int, default=256)
+    ap.add_argument("--mode", default="allgather", choices=["shard", "allgather", "sparse"],
+                    help="N>1: 'allgather' (default, the north star's layout) = the workload's blocks "
+                         "split across ranks, each step = the rank's shard step + the NCCL all-gather "
+                         "of the updated bf16 θ shards into every rank's replica (ma_step_allgather's "
+                         "two halves through the C ABI; strong scaling); 'sparse' = the workload split "
+                         "across ranks for the EF / Top-K front, NCCL all-gather of the new window rows "
+                         "only (ma_exchange_rows), ADAM_STATS + update replicated on every rank's θ "
+                         "(strong scaling); 'shard' = each rank steps its own workload-sized block range "
+                         "of an N x workload vector, no collective (weak scaling)")
+    ap.add_argument("--grad-stream", default="normal", choices=["normal", "heavy"],
+                    help="synthetic gradients: 'normal' (ma_synth Irwin-Hall(4)) or 'heavy' "
+                         "(heavy-tailed, per-block scales: ma_synth_heavy)")
     return ap.parse_args()
 
 
@@ -104,11 +114,44 @@ def dist_env():
 # ---------------------------------------------------------------------------
 # CPU reference timing (oracle/_ref = unmodified reference sources)
 # ---------------------------------------------------------------------------
-def cpu_reference_time(wl, args, steps=2, warmup=1, threads=None):
+def host_cpu():
+    """(model name, physical cores, logical CPUs) of this host (/proc/cpuinfo)."""
+    model, cores = "unknown", set()
+    phys = core = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                k, _, v = line.partition(":")
+                k, v = k.strip(), v.strip()
+                if k == "model name":
+                    model = v
+                elif k == "physical id":
+                    phys = v
+                elif k == "core id":
+                    core = v
+                elif not k and phys is not None:
+                    cores.add((phys, core))
+                    phys = core = None
+        if phys is not None:
+            cores.add((phys, core))
+    except OSError:
+        pass
+    logical = os.cpu_count() or 1
+    return model, (len(cores) or logical), logical
+
+
+def cpu_reference_time(wl, args, steps, warmup, threads=None):
+    """Time the reference's own step (oracle/_ref = the unmodified reference
+    sources; the C restatement if the reference was not built) on this host:
+    one MicroAdamOptimizer(blockwise=true) per thread over a block-aligned shard
+    of the workload (bit-identical to the unsharded run),
+    `warmup` untimed steps (at least m, so every timed step runs with a full
+    window, like the GPU arm) then `steps` consecutive timed steps."""
     import numpy as np
     import oracle
     threads = threads or os.cpu_count() or 1
     shard = args.cpu_shard_blocks * 4096
+    warmup = max(warmup, args.window)
     kind = "reference" if oracle.reference_available() else "port"
     if kind == "reference":
         L = oracle.ref_lib()
@@ -119,20 +162,23 @@ def cpu_reference_time(wl, args, steps=2, warmup=1, threads=None):
             raise RuntimeError("reference CPU timing failed")
     else:  # the C restatement, single thread (no reference build on this host)
         threads = 1
-        g = oracle.synth(42, 1, 0, shard, wl["dtype"])
         o = oracle.Oracle(oracle.synth(1, 0, 0, shard, wl["dtype"]),
                           dict(density=args.density, window=args.window))
-        o.step(g)
+        for s in range(warmup):
+            o.step(oracle.synth(42, s + 1, 0, shard, wl["dtype"]))
         t0 = time.perf_counter()
         for s in range(steps):
-            o.step(oracle.synth(42, s + 2, 0, shard, wl["dtype"]))
+            o.step(oracle.synth(42, warmup + s + 1, 0, shard, wl["dtype"]))
         t = (time.perf_counter() - t0) / steps
     value = threads * shard / t
-    sample = (f"{threads} threads x {shard:,}-param block-aligned shard of the {wl['desc']} "
-              f"({args.cpu_shard_blocks} blocks of 4096), {warmup} warm-up + {steps} timed steps each; "
-              f"value = {threads}*{shard}/max per-thread s/step ({t:.3f} s)")
+    model, phys, logical = host_cpu()
+    sample = (f"{threads} threads on {model} ({phys} physical cores, {logical} logical CPUs); each thread "
+              f"owns a {shard:,}-param block-aligned shard of the {wl['desc']} ({args.cpu_shard_blocks} "
+              f"blocks of 4096) and runs {warmup} untimed steps (window full from step {args.window}) then "
+              f"{steps} consecutive timed steps ({warmup + 1}..{warmup + steps}); value = "
+              f"{threads}*{shard}/max over threads of mean s/step ({t:.4f} s)")
     return {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
-            "s_per_step_per_thread": t}
+            "s_per_step_per_thread": t, "cpu_model": model, "physical_cores": phys, "logical_cpus": logical}
 
 
 def run_reference(args):
@@ -140,28 +186,20 @@ def run_reference(args):
     if rank != 0:
         return 0
     wl = WORKLOADS[args.workload]
-    per_step = []
-    for _ in range(max(1, args.warmup // 5)):
-        cpu_reference_time(wl, args, steps=1, warmup=1)
-    base = None
-    for _ in range(args.steps):
-        # one timed step after one warm-up step of a fresh optimizer per shard
-        base = cpu_reference_time(wl, args, steps=1, warmup=1)
-        per_step.append(base["s_per_step_per_thread"])
-    per_step.sort()
-    med = per_step[len(per_step) // 2]
-    shard = args.cpu_shard_blocks * 4096
-    value = base["cores"] * shard / med
-    base["value"] = value
+    base = cpu_reference_time(wl, args, steps=args.steps, warmup=args.warmup)
+    value = base["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": med * 1e3,
+        "steps": args.steps, "warmup": max(args.warmup, args.window), "warmup_requested": args.warmup,
+        "ms_per_step": wl["dim"] / value * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (include/ma_synth.h stream, bf16-representable)",
+        "data": "synthetic (include/ma_synth.h stream, rounded to the workload dtype)",
         "config": {"workload": f"{args.workload}: {wl['desc']}, density {args.density}, "
                                f"m={args.window}, 4-bit EF, B_d=4096, B_q=64, blockwise",
-                   "dim": wl["dim"], "sample": base["sample"]},
-        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                   "dim": wl["dim"], "sample": base["sample"],
+                   "ms_per_step_note": "full-workload step time implied by the sampled shards' rate"},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                               "physical_cores", "logical_cpus")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -277,6 +315,14 @@ def run_ours(args):
     hp = ma.HyperParams(density=args.density, window=args.window, lr=1e-3)
     gather = world > 1 and args.mode == "allgather"
     sparse = args.mode == "sparse"
+    levels = 2 if args.grad_stream == "heavy" else 0
+    comm = None
+    if world > 1 and args.mode in ("allgather", "sparse"):
+        # the library's own NCCL communicator (ma_comm_init); torch.distributed only
+        # carries the 128-byte unique id and the timing reductions
+        uid = [ma.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = ma.Comm(uid[0], world, rank, local)
     if sparse:  # strong scaling, window-row exchange: a whole-vector handle per rank
         if d % hp.block:
             raise SystemExit("--mode sparse needs a whole-block workload")
@@ -298,8 +344,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def fill(t, seed, step, offset, count):
-        ma._capi.check(lib.ma_fill_synthetic(t.data_ptr(), MA_DT[dt], count, seed, step, offset, 0,
-                                             stream.cuda_stream))
+        ma._capi.check(lib.ma_fill_synthetic(t.data_ptr(), MA_DT[dt], count, seed, step, offset,
+                                             levels if seed == 42 else 0, stream.cuda_stream))
 
     if sparse:  # every rank holds the full θ replica; rows travel, θ does not
         full = None
@@ -335,23 +381,33 @@ def run_ours(args):
     nb_all = d // hp.block
 
     def one_step(i, ev=None):
+        # ev = (start, after the step kernel(s), after the collective)
         if ev is not None:
             ev[0].record()
         if sparse:
             eng.step_front(grad_view(i), b0, b1, stage, stream=stream.cuda_stream)
-            if world > 1:
-                dist.all_gather_into_tensor(rows[0], stage[0])
-                dist.all_gather_into_tensor(rows[1], stage[1])
-                eng.scatter_rows(rows, 0, nb_all, stream=stream.cuda_stream)
+            if ev is not None:
+                ev[1].record()
+            if comm is not None:
+                eng.exchange_rows(stage, rows, comm, stream=stream.cuda_stream)  # ma_exchange_rows
+            if ev is not None:
+                ev[2].record()
             eng.step_stats(params, 1e-3, stream=stream.cuda_stream)
         else:
+            # ma_step_allgather = this step + ma_allgather_params; called as its two
+            # halves so the collective is timed on its own
             eng.step(params, grad_view(i), 1e-3, stream=stream.cuda_stream)
-        if ev is not None:
-            ev[1].record()
-        if gather:
-            dist.all_gather_into_tensor(full, full[rank * stride: (rank + 1) * stride])
+            if ev is not None:
+                ev[1].record()
+            if gather:
+                eng.allgather_params(full, comm, stream=stream.cuda_stream)
+            if ev is not None:
+                ev[2].record()
 
-    for i in range(args.warmup):
+    # untimed warm-up: at least m steps, so every timed step runs with a full
+    # window (filled = m) like a training run past its first m steps
+    warm = max(args.warmup, args.window)
+    for i in range(warm):
         one_step(i)
     torch.cuda.synchronize()
     if world > 1:
@@ -360,15 +416,14 @@ def run_ours(args):
     clocks.start()
     time.sleep(0.3)
     launches0 = eng.kernel_launches()
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    kev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0.record()
     for i in range(args.steps):
-        one_step(args.warmup + i, kev[i])
+        one_step(warm + i, kev[i])
     t1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -377,11 +432,15 @@ def run_ours(args):
     launches = eng.kernel_launches() - launches0
     eng.synchronize()
     elapsed = t0.elapsed_time(t1) / 1e3
-    kern = sum(a.elapsed_time(b) for a, b in kev) / 1e3 / args.steps
+    coll = sum(b.elapsed_time(c) for a, b, c in kev) / 1e3 / args.steps
+    if sparse:  # front + stats kernels: the step minus the row exchange
+        kern = elapsed / args.steps - coll
+    else:
+        kern = sum(a.elapsed_time(b) for a, b, c in kev) / 1e3 / args.steps
     if world > 1:
-        tt = torch.tensor([elapsed, kern], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([elapsed, kern, coll], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed, kern = float(tt[0]), float(tt[1])
+        elapsed, kern, coll = float(tt[0]), float(tt[1]), float(tt[2])
     s_per_step = elapsed / args.steps
     value = dim_total / s_per_step
 
@@ -455,8 +514,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_time(wl, args)
-            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cb = cpu_reference_time(wl, args, steps=3, warmup=args.window)
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                      "physical_cores", "logical_cpus")}
         except Exception as exc:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
@@ -464,21 +524,26 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": s_per_step * 1e3,
+            "steps": args.steps, "warmup": warm, "warmup_requested": args.warmup,
+            "ms_per_step": s_per_step * 1e3,
             "higher_is_better": True, "scaling": "strong" if (gather or sparse) else "weak",
             "vs_baseline": None,
             "dtype": dt,
-            "data": f"synthetic (include/ma_synth.h Irwin-Hall stream, generated on device; step i reads "
-                    f"a shifted window of resident buffer i % {n_grads}, so no step repeats a gradient)",
+            "data": f"synthetic (include/ma_synth.h " + (
+                "heavy-tailed per-block-scaled stream" if levels == 2 else "Irwin-Hall(4) stream") +
+                    f", generated on device; step i reads a shifted window of resident buffer i % "
+                    f"{n_grads}, so no step repeats a gradient; {warm} untimed steps first, so every "
+                    f"timed step runs with a full window)",
             "config": {
                 "workload": f"{args.workload}: {wl['desc']}, {d:,} params, {dt} θ/g, bf16 window "
                             f"values, density {args.density}, m={args.window}, 4-bit EF, "
                             f"B_d=4096, B_q=64, blockwise Top-K",
                 "dim": d, "dim_total": dim_total,
                 "parallelism": f"block-sharded dp{world}" + (
-                    " + NCCL all_gather of bf16 θ each step" if gather else
-                    (" EF/Top-K front + NCCL all_gather of the new window rows, ADAM_STATS + update "
-                     "replicated on each rank's θ" if sparse else None) or
+                    " + NCCL all-gather of the updated bf16 θ shards each step (ma_allgather_params)"
+                    if gather else
+                    (" EF/Top-K front + NCCL all-gather of the new window rows (ma_exchange_rows), "
+                     "ADAM_STATS + update replicated on each rank's θ" if sparse else None) or
                     (", one workload-sized block range per rank, no data-path collective"
                      if world > 1 else "")),
                 "l2": "no flush: every step streams ~%.0f GB >> 126 MB L2" % (
@@ -490,7 +555,7 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "bytes_per_param": bytes_launch / n,
                          "kernel_ms": kern * 1e3,
-                         "kernel_ms_per_step": [round(a.elapsed_time(b_), 3) for a, b_ in kev],
+                         "kernel_ms_per_step": [round(a.elapsed_time(b_), 3) for a, b_, _ in kev],
                          "peak_source": peak_src,
                          "traffic_source": traffic_src,
                          "kernel": "microadam_step_lean (one warp per B_d=4096 Top-K block: fp32-screened EF "
@@ -501,9 +566,21 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk,
         }
-        if gather:
+        if gather or (sparse and comm is not None):
+            psz = DT_BYTES[pdt]
+            recv = ((world - 1) * stride * psz if gather else
+                    (world - 1) * (stride // hp.block) * lay.kb_stride * (2 + DT_BYTES[vdt]))
             line["step_only"] = {"value": d / kern, "ms": kern * 1e3}
+            line["collective"] = {
+                "op": ("ncclAllGather of the bf16 θ shards (ma_allgather_params)" if gather else
+                       "ncclAllGather of the new window rows (ma_exchange_rows)"),
+                "ms": coll * 1e3, "bytes_received_per_rank": recv,
+                "algbw_gbs": recv / coll / 1e9 if coll > 0 else None,
+                "timing": "CUDA events around the collective on the step stream, mean over the timed "
+                          "steps, max over ranks"}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

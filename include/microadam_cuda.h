@@ -245,6 +245,48 @@ MA_API ma_status ma_scatter_rows(ma_handle* h, const void* d_rows_idx, const voi
                           int64_t block_begin, int64_t block_end, void* stream);
 MA_API ma_status ma_step_stats(ma_handle* h, void* d_params, double lr, void* stream);
 
+/* ---- Data-parallel collectives over NCCL ----------------
+ * One process (or thread) per GPU, one shard handle per rank: rank r of N owns
+ * blocks [r*per, min((r+1)*per, num_blocks)) with per = ceil(num_blocks / N)
+ * (paper_2405_15593_b200/sharding.py), i.e. elements from r*per*block on. The
+ * step itself exchanges nothing (the Top-K partitions by block,
+ * compress.cpp:73-85; the replicated host counters keep the bias correction of
+ * window.cpp:43 global), so a sharded run is bit-identical to the unsharded one.
+ * NCCL is loaded at run time (libnccl.so.2 already in the process, e.g.
+ * torch's, else the system one; MA_NCCL_LIB overrides); failures return
+ * MA_ERR_NCCL. The reference has no distributed path. */
+typedef struct ma_comm ma_comm;
+
+/* ncclGetUniqueId: 128 bytes rank 0 hands to every rank (any out-of-band channel). */
+MA_API ma_status ma_comm_unique_id(uint8_t* id /* 128 bytes */);
+/* ncclCommInitRank on `device` (collective across the nranks callers). */
+MA_API ma_status ma_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, int device, ma_comm** out);
+/* Use an existing ncclComm_t (not destroyed by ma_comm_destroy). */
+MA_API ma_status ma_comm_wrap(void* nccl_comm, ma_comm** out);
+MA_API ma_status ma_comm_destroy(ma_comm* comm);
+MA_API ma_status ma_comm_info(const ma_comm* comm, int32_t* nranks, int32_t* rank);
+
+/* The north star's ZeRO-1 step: ma_step on this rank's shard of the full θ
+ * replica d_params_full (the shard starts at element r*per*block), then the
+ * NCCL all-gather of the updated θ shards into every rank's replica, all on
+ * `stream`. full_elems >= N*per*block (padded layout): one in-place
+ * ncclAllGather; full_elems == dim: grouped in-place ncclBroadcast of each
+ * rank's shard. d_grads covers this rank's shard only. With a report, the
+ * StepReport sums are all-reduced first, so every rank gets the global one. */
+MA_API ma_status ma_step_allgather(ma_handle* h, void* d_params_full, int64_t full_elems, const void* d_grads,
+                                   double lr, ma_comm* comm, void* stream, ma_step_report* report);
+/* The all-gather of ma_step_allgather alone. */
+MA_API ma_status ma_allgather_params(ma_handle* h, void* d_params_full, int64_t full_elems, ma_comm* comm,
+                                     void* stream);
+/* Sparse parameter propagation's exchange (between ma_step_front and
+ * ma_step_stats on whole-vector handles): ncclAllGather of every rank's stage
+ * rows ([stage_blocks][kb_stride] int16 indices + values, stage_blocks =
+ * ceil(num_blocks / N)) into d_rows_* ([N*stage_blocks][kb_stride]), then
+ * ma_scatter_rows of all blocks into the window ring. */
+MA_API ma_status ma_exchange_rows(ma_handle* h, const void* d_stage_idx, const void* d_stage_val,
+                                  int64_t stage_blocks, void* d_rows_idx, void* d_rows_val, ma_comm* comm,
+                                  void* stream);
+
 /* For ma_step_host: replace the device copy of θ from a host buffer. */
 MA_API ma_status ma_set_params(ma_handle* h, const void* h_params);
 

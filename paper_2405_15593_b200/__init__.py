@@ -8,11 +8,11 @@ reference optimizer interface (see optim.py) on that ABI; there is no CPU
 fallback.
 """
 from ._capi import LIB_PATH, MicroAdamError, lib
-from .optim import (GradientWindow, HyperParams, InvalidArgument, MicroAdam, MicroAdamOptimizer,
+from .optim import (Comm, GradientWindow, HyperParams, InvalidArgument, MicroAdam, MicroAdamOptimizer,
                     QuantizedErrorBuffer, SparseSelection, StepReport, layout)
 
 __all__ = [
-    "LIB_PATH", "MicroAdamError", "lib", "GradientWindow", "HyperParams", "InvalidArgument",
+    "LIB_PATH", "MicroAdamError", "lib", "Comm", "GradientWindow", "HyperParams", "InvalidArgument",
     "MicroAdam", "MicroAdamOptimizer", "QuantizedErrorBuffer", "SparseSelection", "StepReport",
     "layout",
 ]

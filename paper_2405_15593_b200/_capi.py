@@ -28,6 +28,8 @@ EXPORTED = [
     "ma_kernel_launches", "ma_last_error", "ma_version", "ma_fill_synthetic", "ma_debug_counters",
     "ma_save_checkpoint", "ma_load_checkpoint", "ma_step_front", "ma_scatter_rows", "ma_step_stats",
     "ma_read_error_vector", "ma_step_reduce", "ma_read_error_buffer_blocks", "ma_read_window_blocks",
+    "ma_comm_unique_id", "ma_comm_init", "ma_comm_wrap", "ma_comm_destroy", "ma_comm_info",
+    "ma_step_allgather", "ma_allgather_params", "ma_exchange_rows",
 ]
 
 
@@ -93,6 +95,14 @@ def lib():
     L.ma_step_host.argtypes = [vp, vp, vp, C.c_double, P(Report)]
     L.ma_step_reduce.argtypes = [vp, vp, vp, P(vp), C.c_int32, C.c_float, C.c_double, vp, P(Report)]
     L.ma_sync.argtypes = [vp]
+    L.ma_comm_unique_id.argtypes = [vp]
+    L.ma_comm_init.argtypes = [vp, C.c_int32, C.c_int32, C.c_int, P(vp)]
+    L.ma_comm_wrap.argtypes = [vp, P(vp)]
+    L.ma_comm_destroy.argtypes = [vp]
+    L.ma_comm_info.argtypes = [vp, P(C.c_int32), P(C.c_int32)]
+    L.ma_step_allgather.argtypes = [vp, vp, C.c_int64, vp, C.c_double, vp, vp, P(Report)]
+    L.ma_allgather_params.argtypes = [vp, vp, C.c_int64, vp, vp]
+    L.ma_exchange_rows.argtypes = [vp, vp, vp, C.c_int64, vp, vp, vp, vp]
     L.ma_get_counters.argtypes = [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(C.c_int64)]
     L.ma_read_error_buffer.argtypes = [vp, vp, vp, vp]
     L.ma_read_window_row.argtypes = [vp, C.c_int64, vp, vp]

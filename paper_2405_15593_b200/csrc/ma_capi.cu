@@ -227,6 +227,8 @@ struct ma_handle {
     cudaEvent_t done_ev = nullptr;
     // ma_step_host chunk events, created once and reused across calls
     std::vector<cudaEvent_t> host_ev;
+    // ma_step_allgather with a report: the report sums are all-reduced over it
+    const ma_comm* report_comm = nullptr;
 };
 
 namespace {
@@ -400,9 +402,15 @@ cudaError_t launch(ma_handle* h, ma::StepArgs& a, int64_t nblocks, cudaStream_t 
     return cudaSuccess;
 }
 
+ma_status allreduce_report(ma_handle* h, cudaStream_t st);  // after struct ma_comm (below)
+
 ma_status finish_report(ma_handle* h, cudaStream_t st, ma_step_report* report) {
     MA_CUDA(ma::launch_report_reduce(h->d_partials, h->shape.b1 - h->shape.b0, h->d_report, st));
     ++h->launches;
+    if (h->report_comm) {  // ma_step_allgather: the five sums over all ranks' shards
+        ma_status rs = allreduce_report(h, st);
+        if (rs != MA_OK) return rs;
+    }
     double r[ma::kReportFields];
     MA_CUDA(cudaMemcpyAsync(r, h->d_report, sizeof(r), cudaMemcpyDeviceToHost, st));
     MA_CUDA(cudaStreamSynchronize(st));
@@ -1530,6 +1538,232 @@ ma_status ma_step_stats(ma_handle* h, void* d_params, double lr, void* stream) {
     h->pending = nullptr;
     return mark_done(h, st);
 }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Data-parallel collectives over NCCL (north star: "each GPU
+// owns its slice ... only the updated bf16 parameters are all-gathered with
+// NCCL over NVLink"). A shard handle (ma_create_shard) owns the block range
+// sharding.py assigns to its rank: ranks take per = ceil(num_blocks / nranks)
+// whole blocks each (the last rank the remainder), so rank r's elements start
+// at r * per * block. The step itself needs no exchange (block sharding is
+// bit-exact: compress.cpp:73-85 partitions the Top-K by block; the host
+// counters, hence the bias correction of window.cpp:43, are replicated).
+// ---------------------------------------------------------------------------
+struct ma_comm {
+    ma::nccl::Comm comm = nullptr;
+    int nranks = 1, rank = 0;
+    bool owned = false;
+    int device = 0;
+};
+
+namespace {
+
+const ma::nccl::Api* nccl_api() {
+    std::string err;
+    const ma::nccl::Api* a = ma::nccl::api(&err);
+    if (!a) fail(MA_ERR_NCCL, err);
+    return a;
+}
+
+#define MA_NCCL(api, call)                                                         \
+    do {                                                                           \
+        const int _r = (call);                                                     \
+        if (_r != 0) return fail(MA_ERR_NCCL, ma::nccl::describe((api), _r) + " in " #call); \
+    } while (0)
+
+// The rank's partition (sharding.py:partition_blocks) must be the handle's range.
+ma_status check_partition(const ma_handle* h, const ma_comm* c, int64_t* per_out) {
+    const Shape& s = h->shape;
+    if (s.global) return fail(MA_ERR_UNSUPPORTED, "collectives: global Top-K mode is not block-sharded");
+    const int64_t nbg = s.nblocks_global;
+    const int64_t per = (nbg + c->nranks - 1) / c->nranks;
+    const int64_t b0 = int64_t(c->rank) * per, b1 = std::min(b0 + per, nbg);
+    if (per * (c->nranks - 1) >= nbg)
+        return fail(MA_ERR_INVALID_ARG, "collectives: some rank would own no block");
+    if (s.b0 != b0 || s.b1 != b1)
+        return fail(MA_ERR_INVALID_ARG, "collectives: the handle's block range is not this rank's partition "
+                                        "(ranks own ceil(num_blocks / nranks) blocks each)");
+    *per_out = per;
+    return MA_OK;
+}
+
+}  // namespace
+
+
+namespace {
+ma_status allreduce_report(ma_handle* h, cudaStream_t st) {
+    const ma::nccl::Api* a = nccl_api();
+    if (!a) return MA_ERR_NCCL;
+    MA_NCCL(a, a->AllReduce(h->d_report, h->d_report, ma::kReportFields, ma::nccl::kFloat64, ma::nccl::kSum,
+                            h->report_comm->comm, st));
+    return MA_OK;
+}
+}  // namespace
+
+extern "C" {
+
+ma_status ma_comm_unique_id(uint8_t* id) {
+    if (!id) return fail(MA_ERR_INVALID_ARG, "null argument");
+    const ma::nccl::Api* a = nccl_api();
+    if (!a) return MA_ERR_NCCL;
+    ma::nccl::IdBytes u;
+    MA_NCCL(a, a->GetUniqueId(&u));
+    std::memcpy(id, u.internal, sizeof(u.internal));
+    return MA_OK;
+}
+
+ma_status ma_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, int device, ma_comm** out) {
+    if (!id || !out) return fail(MA_ERR_INVALID_ARG, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(MA_ERR_INVALID_ARG, "comm: bad rank / nranks");
+    *out = nullptr;
+    const ma::nccl::Api* a = nccl_api();
+    if (!a) return MA_ERR_NCCL;
+    DeviceGuard g(device);
+    ma::nccl::IdBytes u;
+    std::memcpy(u.internal, id, sizeof(u.internal));
+    ma::nccl::Comm cm = nullptr;
+    MA_NCCL(a, a->CommInitRank(&cm, nranks, u, rank));
+    ma_comm* c = new (std::nothrow) ma_comm;
+    if (!c) {
+        a->CommDestroy(cm);
+        return fail(MA_ERR_INVALID_ARG, "out of host memory");
+    }
+    c->comm = cm;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->owned = true;
+    c->device = device;
+    *out = c;
+    return MA_OK;
+}
+
+ma_status ma_comm_wrap(void* nccl_comm, ma_comm** out) {
+    if (!nccl_comm || !out) return fail(MA_ERR_INVALID_ARG, "null argument");
+    *out = nullptr;
+    const ma::nccl::Api* a = nccl_api();
+    if (!a) return MA_ERR_NCCL;
+    ma_comm* c = new (std::nothrow) ma_comm;
+    if (!c) return fail(MA_ERR_INVALID_ARG, "out of host memory");
+    c->comm = static_cast<ma::nccl::Comm>(nccl_comm);
+    int n = 0, r = 0;
+    const int e1 = a->CommCount(c->comm, &n), e2 = a->CommUserRank(c->comm, &r);
+    if (e1 || e2) {
+        delete c;
+        return fail(MA_ERR_NCCL, ma::nccl::describe(a, e1 ? e1 : e2) + " in ma_comm_wrap");
+    }
+    c->nranks = n;
+    c->rank = r;
+    cudaGetDevice(&c->device);
+    *out = c;
+    return MA_OK;
+}
+
+ma_status ma_comm_destroy(ma_comm* c) {
+    if (!c) return MA_OK;
+    ma_status st = MA_OK;
+    if (c->owned && c->comm) {
+        const ma::nccl::Api* a = nccl_api();
+        if (a) {
+            DeviceGuard g(c->device);
+            const int r = a->CommDestroy(c->comm);
+            if (r) st = fail(MA_ERR_NCCL, ma::nccl::describe(a, r) + " in ncclCommDestroy");
+        }
+    }
+    delete c;
+    return st;
+}
+
+ma_status ma_comm_info(const ma_comm* c, int32_t* nranks, int32_t* rank) {
+    if (!c) return fail(MA_ERR_INVALID_ARG, "null comm");
+    if (nranks) *nranks = c->nranks;
+    if (rank) *rank = c->rank;
+    return MA_OK;
+}
+
+ma_status ma_allgather_params(ma_handle* h, void* d_params_full, int64_t full_elems, ma_comm* c, void* stream) {
+    if (!h || !d_params_full || !c) return fail(MA_ERR_INVALID_ARG, "null argument");
+    int64_t per = 0;
+    { ma_status st = check_partition(h, c, &per); if (st != MA_OK) return st; }
+    const ma::nccl::Api* a = nccl_api();
+    if (!a) return MA_ERR_NCCL;
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const Shape& s = h->shape;
+    const size_t psz = dtype_size(h->cfg.param_dtype);
+    const int64_t stride = per * s.block;  // elements per (padded) shard
+    unsigned char* full = static_cast<unsigned char*>(d_params_full);
+    if (c->nranks == 1) return MA_OK;
+    if (full_elems >= stride * c->nranks) {
+        // equal chunks of the padded layout: one in-place all-gather
+        MA_NCCL(a, a->AllGather(full + size_t(c->rank) * size_t(stride) * psz, full, size_t(stride) * psz,
+                                ma::nccl::kUint8, c->comm, st));
+    } else if (full_elems == s.dim_global) {
+        // exact-length θ: every rank broadcasts its (possibly shorter, last) shard in place
+        MA_NCCL(a, a->GroupStart());
+        for (int r = 0; r < c->nranks; ++r) {
+            const int64_t e0 = int64_t(r) * stride, e1 = std::min(e0 + stride, s.dim_global);
+            const int rc = a->Broadcast(full + size_t(e0) * psz, full + size_t(e0) * psz, size_t(e1 - e0) * psz,
+                                        ma::nccl::kUint8, r, c->comm, st);
+            if (rc) {
+                a->GroupEnd();
+                return fail(MA_ERR_NCCL, ma::nccl::describe(a, rc) + " in ncclBroadcast");
+            }
+        }
+        MA_NCCL(a, a->GroupEnd());
+    } else {
+        return fail(MA_ERR_INVALID_ARG, "allgather_params: full_elems must be dim or >= nranks * shard stride");
+    }
+    return mark_done(h, st);
+}
+
+ma_status ma_step_allgather(ma_handle* h, void* d_params_full, int64_t full_elems, const void* d_grads, double lr,
+                            ma_comm* c, void* stream, ma_step_report* report) {
+    if (!h || !d_params_full || !d_grads || !c) return fail(MA_ERR_INVALID_ARG, "null argument");
+    int64_t per = 0;
+    { ma_status st = check_partition(h, c, &per); if (st != MA_OK) return st; }
+    if (full_elems < h->shape.dim_global) return fail(MA_ERR_INVALID_ARG, "step_allgather: full θ too short");
+    const ma::nccl::Api* a = nccl_api();
+    if (!a) return MA_ERR_NCCL;
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    void* shard = static_cast<unsigned char*>(d_params_full) + size_t(h->shape.elem0) * dtype_size(h->cfg.param_dtype);
+    h->report_comm = c->nranks > 1 ? c : nullptr;
+    const ma_status rs = run_step(h, shard, d_grads, lr, st, report);
+    h->report_comm = nullptr;
+    if (rs != MA_OK) return rs;
+    return ma_allgather_params(h, d_params_full, full_elems, c, stream);
+}
+
+ma_status ma_exchange_rows(ma_handle* h, const void* d_stage_idx, const void* d_stage_val, int64_t stage_blocks,
+                           void* d_rows_idx, void* d_rows_val, ma_comm* c, void* stream) {
+    if (!h || !d_stage_idx || !d_stage_val || !d_rows_idx || !d_rows_val || !c)
+        return fail(MA_ERR_INVALID_ARG, "null argument");
+    if (!h->pending) return fail(MA_ERR_STATE, "exchange_rows: no ma_step_front in flight");
+    const Shape& s = h->shape;
+    const int64_t nb = s.b1 - s.b0;
+    const int64_t per = (nb + c->nranks - 1) / c->nranks;
+    if (stage_blocks != per)
+        return fail(MA_ERR_INVALID_ARG, "exchange_rows: stage_blocks must be ceil(num_blocks / nranks)");
+    const ma::nccl::Api* a = nccl_api();
+    if (!a) return MA_ERR_NCCL;
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t vsz = dtype_size(h->cfg.value_dtype);
+    const size_t ent = size_t(per) * size_t(s.kb_stride);
+    if (c->nranks == 1) return ma_scatter_rows(h, d_stage_idx, d_stage_val, 0, nb, stream);
+    MA_NCCL(a, a->GroupStart());
+    int rc = a->AllGather(d_stage_idx, d_rows_idx, ent * 2, ma::nccl::kUint8, c->comm, st);
+    if (!rc) rc = a->AllGather(d_stage_val, d_rows_val, ent * vsz, ma::nccl::kUint8, c->comm, st);
+    const int rc2 = a->GroupEnd();
+    if (rc || rc2) return fail(MA_ERR_NCCL, ma::nccl::describe(a, rc ? rc : rc2) + " in exchange_rows");
+    return ma_scatter_rows(h, d_rows_idx, d_rows_val, 0, nb, stream);
+}
+
+}  // extern "C"
+
+extern "C" {
 
 ma_status ma_get_layout(const ma_handle* h, ma_layout_info* out) {
     if (!h || !out) return fail(MA_ERR_INVALID_ARG, "null argument");

@@ -158,3 +158,35 @@ cudaError_t launch_fill_synthetic(void* out, int dtype, int64_t n, uint64_t seed
                                   int64_t offset, int levels, cudaStream_t s);
 
 }  // namespace ma
+
+#include <string>
+
+// NCCL entry points resolved at run time (ma_nccl.cpp). Opaque types keep this
+// header free of nccl.h: comm = ncclComm_t, id = ncclUniqueId (128 bytes),
+// enums passed as int (ncclDataType_t / ncclRedOp_t / ncclResult_t values).
+namespace ma {
+namespace nccl {
+struct IdBytes {
+    char internal[128];
+};
+using Comm = struct ncclComm*;
+struct Api {
+    int (*GetUniqueId)(IdBytes*);
+    int (*CommInitRank)(Comm*, int, IdBytes, int);
+    int (*CommDestroy)(Comm);
+    int (*CommCount)(const Comm, int*);
+    int (*CommUserRank)(const Comm, int*);
+    int (*AllGather)(const void*, void*, size_t, int, Comm, cudaStream_t);
+    int (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t);
+    int (*Broadcast)(const void*, void*, size_t, int, int, Comm, cudaStream_t);
+    int (*GroupStart)();
+    int (*GroupEnd)();
+    const char* (*GetErrorString)(int);
+    int (*GetVersion)(int*);
+};
+constexpr int kUint8 = 1, kFloat64 = 8, kSum = 0;  // ncclUint8, ncclFloat64, ncclSum
+// nullptr (and *err set) when no NCCL library can be loaded.
+const Api* api(std::string* err);
+std::string describe(const Api* a, int rc);
+}  // namespace nccl
+}  // namespace ma

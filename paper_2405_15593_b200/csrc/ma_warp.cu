@@ -842,6 +842,9 @@ cudaError_t launch_kw(const StepArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+#ifdef MA_PROBE_HOT  // SASS-inspection builds (tools/sass_probe.sh): the bench's dtypes only
+#define MA_WARP_DTYPES(X) X(BF16, BF16, BF16)
+#else
 #define MA_WARP_DTYPES(X)         \
     X(BF16, BF16, BF16)           \
     X(F32, F32, BF16)             \
@@ -849,6 +852,7 @@ cudaError_t launch_kw(const StepArgs& a, cudaStream_t s) {
     X(BF16, F32, BF16)            \
     X(BF16, BF16, F32)            \
     X(F64, F64, F64)
+#endif
 
 constexpr int dtype_key_w(int g, int p, int v) { return g * 9 + p * 3 + v; }
 
@@ -997,16 +1001,17 @@ template <class KT>
 struct UniqueUpd {
     static constexpr bool kScreen = KT::PDT == BF16 && KT::VDT != F64;
     float th = 0.0f, v = 0.0f;
-    __device__ __forceinline__ void load(const StepArgs& p, int64_t base, const unsigned char* gwv, int e, int idx) {
+    // thb: the block's θ (element 0 = block element 0); gwv: its value ring
+    __device__ __forceinline__ void load(const void* thb, const unsigned char* gwv, int e, int idx) {
         if constexpr (kScreen) {
-            th = __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(p.params)[base + idx]) << 16);
+            th = __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(thb)[idx]) << 16);
             v = KT::VDT == BF16
                     ? __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(gwv)[e]) << 16)
                     : reinterpret_cast<const float*>(gwv)[e];
         }
     }
-    __device__ __forceinline__ void finish(const StepArgs& p, int64_t base, const unsigned char* gwv, int e, int r,
-                                           int idx) {
+    __device__ __forceinline__ void finish(const StepArgs& p, int64_t base, void* thb, const unsigned char* gwv,
+                                           int e, int r, int idx) {
         if constexpr (kScreen) {
             const float den = __fmaf_rn(fabsf(v), p.c2[r], p.eps32);
             const float u = __fdividef(p.c1[r] * v, den);
@@ -1016,16 +1021,15 @@ struct UniqueUpd {
             const int mid = static_cast<int>(xb & 0xFFFFu) - 0x8000;
             const bool ok = ex >= 27u && ex <= 227u && den < 0x1p120f &&
                             fabsf(p.lr32 * u) <= __uint_as_float((ex + 4u) << 23) && (mid > 512 || mid < -512);
-            if (ok) static_cast<uint16_t*>(p.params)[base + idx] =
-                        static_cast<uint16_t>((xb + 0x7FFFu + ((xb >> 16) & 1u)) >> 16);
+            if (ok) static_cast<uint16_t*>(thb)[idx] = static_cast<uint16_t>((xb + 0x7FFFu + ((xb >> 16) & 1u)) >> 16);
             else exact_update<KT>(&p, base, gwv, e, r, idx);
         } else {
             const double vv = ld_t<KT::VDT>(gwv, e);
-            const double t = ld_t<KT::PDT>(p.params, base + idx);
+            const double t = ld_t<KT::PDT>(thb, idx);
             const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r], vv)), p.scale1);
             const double vhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w2[r], __dmul_rn(vv, vv))), p.scale2);
             const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
-            st_t<KT::PDT>(p.params, base + idx, __dsub_rn(t, __dmul_rn(p.lr, u)));
+            st_t<KT::PDT>(thb, idx, __dsub_rn(t, __dmul_rn(p.lr, u)));
         }
     }
 };
@@ -1649,28 +1653,30 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     // Entry t = row r (physical slot) * k_b + position pos; each lane walks
     // t = lane, lane + 32, ... with (r, pos) advanced incrementally.
     const int nent = filled * kb;
-    int r0 = 0, pos0 = lane;
-    while (pos0 >= kb) {
-        pos0 -= kb;
-        ++r0;
-    }
+    // Entry t = lane + 32 i sits at (row r, position pos); 32 entries later it
+    // is (r + dq, pos + dr) plus at most one carry (dq = 32 / k_b, dr = 32 % k_b).
+    const int r0 = lane / kb, pos0 = lane - r0 * kb;
+    const int dq = 32 / kb, dr = 32 - dq * kb;
     auto advance = [&](int& r, int& pos) {
-        pos += 32;
-        while (pos >= kb) {
+        pos += dr;
+        r += dq;
+        if (pos >= kb) {
             pos -= kb;
             ++r;
         }
     };
+    const int16_t* __restrict__ wi = gwi;  // this block's [m][kbs] index ring
     {
         int r = r0, pos = pos0;
+#pragma unroll 1
         for (int t = lane; t < nent; t += 64) {
             const int ea = r * kbs + pos;
             advance(r, pos);
             const bool hb = t + 32 < nent;
-            const int eb = r * kbs + pos;
+            const int eb = hb ? r * kbs + pos : ea;
             advance(r, pos);
-            const int ia = gwi[ea];
-            const int ib = hb ? gwi[eb] : ia;
+            const int ia = wi[ea];
+            const int ib = wi[eb];
             uint32_t bit = 1u << (ia & 31);
             if (atomicOr(&s_seen[ia >> 5], bit) & bit) atomicOr(&s_dup[ia >> 5], bit);
             if (hb) {
@@ -1686,18 +1692,21 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     int* dupl = reinterpret_cast<int*>(s_cval);
     int ndup = 0;
     {
+        void* thb = static_cast<unsigned char*>(p.params) + base * psz;  // this block's θ
         int r = r0, pos = pos0;
         constexpr int SB = MA_LEAN_SB;  // entries per lane in flight
-        for (int t0 = 0; t0 < nent; t0 += 32 * SB) {
+        const int dup_max = static_cast<int>((L.cidx - L.cval) / 4);
+#pragma unroll 1
+        for (int t0 = lane; t0 < nent + lane; t0 += 32 * SB) {
             int e[SB], idx[SB], rr[SB], ps[SB];
             bool act[SB], mine[SB];
 #pragma unroll
             for (int k = 0; k < SB; ++k) {
-                act[k] = t0 + 32 * k + lane < nent;
+                act[k] = t0 + 32 * k < nent;
                 rr[k] = r;
                 ps[k] = pos;
                 e[k] = r * kbs + pos;
-                idx[k] = act[k] ? gwi[e[k]] : 0;
+                idx[k] = act[k] ? wi[e[k]] : 0;
                 advance(r, pos);
             }
             UniqueUpd<KT> u[SB];
@@ -1705,15 +1714,17 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
             for (int k = 0; k < SB; ++k) {
                 const bool dup = act[k] && ((s_dup[idx[k] >> 5] >> (idx[k] & 31)) & 1u);
                 mine[k] = act[k] && !dup;
-                if (mine[k]) u[k].load(p, base, gwv, e[k], idx[k]);
+                if (mine[k]) u[k].load(thb, gwv, e[k], idx[k]);
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
-                const int qd = ndup + __popc(bal & lanemask_lt());
-                if (dup && qd < static_cast<int>((L.cidx - L.cval) / 4)) dupl[qd] = (idx[k] << 16) | (rr[k] << 8) | ps[k];
-                ndup += __popc(bal);
+                if (bal) {
+                    const int qd = ndup + __popc(bal & lanemask_lt());
+                    if (dup && qd < dup_max) dupl[qd] = (idx[k] << 16) | (rr[k] << 8) | ps[k];
+                    ndup += __popc(bal);
+                }
             }
 #pragma unroll
             for (int k = 0; k < SB; ++k)
-                if (mine[k]) u[k].finish(p, base, gwv, e[k], rr[k], idx[k]);
+                if (mine[k]) u[k].finish(p, base, thb, gwv, e[k], rr[k], idx[k]);
         }
     }
     __syncwarp();
@@ -1780,12 +1791,16 @@ cudaError_t launch_kl(const StepArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+#ifdef MA_PROBE_HOT
+#define MA_LEAN_DTYPES(X) X(BF16, BF16, BF16)
+#else
 #define MA_LEAN_DTYPES(X) \
     X(BF16, BF16, BF16)   \
     X(F32, F32, BF16)     \
     X(F32, F32, F32)      \
     X(BF16, F32, BF16)    \
     X(BF16, BF16, F32)
+#endif
 
 // k_b <= 64: 4 candidate slots per lane; up to 256 (densities to 6.25%): 16.
 constexpr int kWideKb = 32 * 16 / 2;

@@ -357,6 +357,34 @@ class MicroAdam(_Handle):
                                  C.byref(rep) if report else None))
         return StepReport.from_c(rep) if report else None
 
+    def step_allgather(self, params_full, grads, comm: "Comm", lr: Optional[float] = None, stream=None,
+                       report: bool = False) -> Optional[StepReport]:
+        """ZeRO-1 data-parallel step (ma_step_allgather): this shard engine steps
+        its slice of the full θ replica `params_full`, then NCCL all-gathers the
+        updated shards into every rank's replica. `params_full` holds dim
+        elements (grouped broadcasts) or nranks * shard stride (one all-gather);
+        `grads` covers this engine's blocks only."""
+        rep = _capi.Report()
+        n = params_full.numel() if hasattr(params_full, "numel") else int(params_full[1])
+        ptr = params_full.data_ptr() if hasattr(params_full, "data_ptr") else int(params_full[0])
+        _ok(lib().ma_step_allgather(self._h, ptr, n, self._ptr(grads, self.grad_dtype, "grads"),
+                                    self.hp.lr if lr is None else lr, comm.handle,
+                                    C.c_void_p(self._stream(stream)), C.byref(rep) if report else None))
+        return StepReport.from_c(rep) if report else None
+
+    def allgather_params(self, params_full, comm: "Comm", stream=None) -> None:
+        """The all-gather half of step_allgather (ma_allgather_params)."""
+        _ok(lib().ma_allgather_params(self._h, params_full.data_ptr(), params_full.numel(), comm.handle,
+                                      C.c_void_p(self._stream(stream))))
+
+    def exchange_rows(self, stage, rows, comm: "Comm", stream=None) -> None:
+        """Sparse propagation's exchange (ma_exchange_rows): NCCL all-gather of every
+        rank's stage rows into `rows`, then scatter them into this step's window slot."""
+        kbs = self.layout.kb_stride
+        _ok(lib().ma_exchange_rows(self._h, stage[0].data_ptr(), stage[1].data_ptr(), stage[0].numel() // kbs,
+                                   rows[0].data_ptr(), rows[1].data_ptr(), comm.handle,
+                                   C.c_void_p(self._stream(stream))))
+
     def step_host(self, h_params, h_grads, lr: Optional[float] = None,
                   report: bool = False) -> Optional[StepReport]:
         """Reference-facing host path (ma_step_host): host θ in/out, host g in.
@@ -430,6 +458,38 @@ class MicroAdam(_Handle):
         (checkpoint.cpp:88-140 format), e.g. one written by the reference."""
         on_dev, ptr = _buffer(params) if params is not None else (0, None)
         _ok(lib().ma_load_checkpoint(self._h, ptr, on_dev, os.fsencode(path)))
+
+
+class Comm:
+    """An NCCL communicator owned through the C ABI (ma_comm_*): rank 0 calls
+    unique_id(), every rank receives those 128 bytes (any channel, e.g.
+    torch.distributed.broadcast_object_list) and builds Comm(id, nranks, rank, device)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int = 0):
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _ok(lib().ma_comm_init(buf, nranks, rank, device, C.byref(h)))
+        self.handle = h
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _ok(lib().ma_comm_unique_id(buf))
+        return bytes(buf)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _ok(lib().ma_comm_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _buffer(x):
