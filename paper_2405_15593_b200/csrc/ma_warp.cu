@@ -883,6 +883,19 @@ constexpr int dtype_key_w(int g, int p, int v) { return g * 9 + p * 3 + v; }
 // ===========================================================================
 
 constexpr float kTwo23 = 8388608.0f;
+
+// prmt with an immediate selector SEL | k (the constant operand stays in a register).
+template <uint32_t SEL>
+__device__ __forceinline__ uint32_t prmt_imm(uint32_t a, uint32_t b, int k) {
+    uint32_t d;
+    switch (k) {
+        case 0: asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL | 0u)); break;
+        case 1: asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL | 1u)); break;
+        case 2: asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL | 2u)); break;
+        default: asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL | 3u)); break;
+    }
+    return d;
+}
 #ifndef MA_LEAN_CAPL
 #define MA_LEAN_CAPL 4  // lean kernel: exact-stage candidate slots per lane
 #endif
@@ -975,6 +988,121 @@ __device__ __forceinline__ double exact_a_raw(const Raw8<DT>& r, uint32_t cw, in
     return __dadd_rn(g, __dadd_rn(__dmul_rn(static_cast<double>((cw >> (4 * i)) & 15u), ll.y), ll.x));
 }
 
+// ---- pass 2 of the lean kernel: fp32 with exact fallbacks -----------------
+// Lane l of iteration j owns the 16 elements [512 j + 16 l, +16): one B_q =
+// 64 bucket is 4 lanes (2 for B_q = 32). With the previous grid (lo, level)
+// and E = E_q of the pass-1 bound, the residual r32 = sel ? 0 : a32 obeys
+// |r32 - r| <= eps := E + max|r32| 2^-23 over the bucket (0 for selected).
+// For the bucket's fp32 extremes mn, mx the exact lo' = min r, hi' = max r
+// lie within eps of them. With k2 = 30 / rd(mx - mn) (2-ulp division) and
+// c2 = rn(257 + G - mn k2), y = rn(r32 k2 + c2) ∈ [256, 512) satisfies
+//   y - 256 ∈ [1 + 2T, 1 + 2T + 2G],  T = 15 (r - lo') / (hi' - lo'),
+// whenever G >= 121 eps / den + 30·2^-21 + |c2| 2^-24 + 2^-16 (den =
+// rd(mx - mn) - 2 eps, the error of k2, of r32 - mn, of c2 and of y), which
+// the kernel bounds by G = 128 eps / den + cmag 2^-23 + 2^-13. Let N =
+// floor(y) - 256 (mantissa bits 22..15): an element whose y has fraction
+// >= 2G has code floor(T + 0.5) = N >> 1 exactly (also against the
+// reference's fp64 quotient, 2^-48 away from T). Elements with a smaller
+// fraction are flagged: N even = a code boundary, recoded by the IEEE
+// quotient (quantize.cpp:51-53) with the exact lo', level'; N = 1 holds every
+// candidate for the exact minimum (T = 0 gives y - 256 ∈ [1, 1 + 2G]) and
+// N = 31 every candidate for the maximum, whose exact fp64 residuals give
+// (lo', hi'). Buckets with G > 1/16, R outside [2^-100, 2^100] or a
+// non-finite bound run exactly in fp64 (exact_bucket16). The code of a
+// fast-path element sits in byte 2 of y (bits 19..16 = N >> 1).
+template <int DT>
+struct Raw16 {
+    static constexpr int N = DT == BF16 ? 2 : 4;
+    uint4 v[N];
+};
+template <int DT, bool NC>
+__device__ __forceinline__ Raw16<DT> load_raw16(const unsigned char* gp) {
+    Raw16<DT> r;
+    const uint4* q = reinterpret_cast<const uint4*>(gp);
+#pragma unroll
+    for (int k = 0; k < Raw16<DT>::N; ++k) {
+        if constexpr (NC) r.v[k] = __ldg(q + k);
+        else r.v[k] = q[k];
+    }
+    return r;
+}
+template <int DT>
+__device__ __forceinline__ float g32_of(const Raw16<DT>& r, int i) {  // i: compile-time after unrolling
+    if constexpr (DT == BF16) {
+        const uint4 v = r.v[i >> 3];
+        const int k = (i >> 1) & 3;
+        const uint32_t w = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+        return __uint_as_float((i & 1) ? (w & 0xFFFF0000u) : (w << 16));
+    } else {
+        const uint4 v = r.v[i >> 2];
+        const int k = i & 3;
+        return __uint_as_float(k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w)));
+    }
+}
+
+// a32 of one block element, recomputed exactly as the packed decode does it.
+template <class KT>
+__device__ __forceinline__ float a32_at_w(const StepArgs& p, int64_t base, int e, float lo32, float lv32) {
+    const uint32_t byte = p.codes[(base + e) >> 1];
+    const float c = static_cast<float>((byte >> ((e & 1) * 4)) & 15u);
+    float g;
+    if constexpr (KT::GDT == BF16)
+        g = __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(p.grads)[base + e]) << 16);
+    else
+        g = static_cast<const float*>(p.grads)[base + e];
+    return __fadd_rn(g, __fmaf_rn(c, lv32, lo32));
+}
+
+// a at one block element with its bucket's exact (lo, level) given.
+template <class KT>
+__device__ __forceinline__ double recompute_a_q(const StepArgs& p, int64_t base, int e, double2 q) {
+    const uint32_t byte = p.codes[(base + e) >> 1];
+    const double ev = __dadd_rn(__dmul_rn(static_cast<double>((byte >> ((e & 1) * 4)) & 15u), q.y), q.x);
+    return __dadd_rn(ld_t<KT::GDT>(p.grads, base + e), ev);
+}
+
+struct Bucket16 {
+    uint32_t w0, w1;
+    double lo, hi;
+};
+// The exact fp64 path for a lane's 16 elements of a bucket the fp32 bounds do
+// not cover (quantize.cpp:15-24, 42-55 in the reference's operation order);
+// `bm` = the bucket's lanes (they all call this together).
+template <class KT>
+__device__ __noinline__ Bucket16 exact_bucket16(const StepArgs* pp, int64_t base, int e0, uint32_t sel16, double2 ll,
+                                                uint32_t bm, int lpb) {
+    const StepArgs& p = *pp;
+    double lo = CUDART_INF, hi = -CUDART_INF;
+    for (int i = 0; i < 16; ++i) {
+        const double r = ((sel16 >> i) & 1u) ? 0.0 : recompute_a_q<KT>(p, base, e0 + i, ll);
+        lo = r < lo ? r : lo;
+        hi = r > hi ? r : hi;
+    }
+    for (int off = 1; off < lpb; off <<= 1) {
+        const double ol = __shfl_xor_sync(bm, lo, off), oh = __shfl_xor_sync(bm, hi, off);
+        lo = ol < lo ? ol : lo;
+        hi = oh > hi ? oh : hi;
+    }
+    Bucket16 o{0u, 0u, lo, hi};
+    if (lo != hi) {
+        const double level = __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+        for (int i = 15; i >= 0; --i) {
+            const double r = ((sel16 >> i) & 1u) ? 0.0 : recompute_a_q<KT>(p, base, e0 + i, ll);
+            const uint32_t c = exact_code_w(r, lo, level);
+            if (i >= 8) o.w1 = (o.w1 << 4) | c;
+            else o.w0 = (o.w0 << 4) | c;
+        }
+    }
+    return o;
+}
+
+// Codes from byte 2 of eight y words (bits 19..16 = N >> 1), low nibble first.
+__device__ __forceinline__ uint32_t pack_codes8(const uint32_t* y) {
+    const uint32_t ev = __byte_perm(__byte_perm(y[0], y[2], 0x0062u), __byte_perm(y[4], y[6], 0x0062u), 0x5410u);
+    const uint32_t od = __byte_perm(__byte_perm(y[1], y[3], 0x0062u), __byte_perm(y[5], y[7], 0x0062u), 0x5410u);
+    return (ev & 0x0F0F0F0Fu) | ((od << 4) & 0xF0F0F0F0u);
+}
+
 // ADAM_STATS + update of a coordinate held by exactly one window entry
 // (row r, entry e): window.cpp:28-46 with one term, optim.cpp:183-187, in the
 // reference's fp64 operation order. Out of line for the bf16-θ screen below.
@@ -1033,6 +1161,53 @@ struct UniqueUpd {
         }
     }
 };
+
+// ADAM_STATS + update of a coordinate held by one window entry, with θ (or the
+// 4-byte word holding a bf16 θ) staged at `sth` and the value in the staged
+// rows `swv` (same arithmetic and screen as UniqueUpd).
+template <class KT>
+__device__ __forceinline__ void unique_update_smem(const StepArgs& p, int64_t base, void* thb, const unsigned char* gwv,
+                                                   const unsigned char* swv, const unsigned char* sth, int e, int r,
+                                                   int idx) {
+    if constexpr (KT::PDT == BF16 && KT::VDT != F64) {
+        const uint32_t word = *reinterpret_cast<const uint32_t*>(sth);
+        const float th = __uint_as_float((idx & 1) ? (word & 0xFFFF0000u) : (word << 16));
+        const float v = KT::VDT == BF16
+                            ? __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(swv)[e]) << 16)
+                            : reinterpret_cast<const float*>(swv)[e];
+        const float den = __fmaf_rn(fabsf(v), p.c2[r], p.eps32);
+        const float u = __fdividef(p.c1[r] * v, den);
+        const float x = __fmaf_rn(-p.lr32, u, th);
+        const uint32_t xb = __float_as_uint(x);
+        const uint32_t ex = (xb >> 23) & 0xFFu;
+        const int mid = static_cast<int>(xb & 0xFFFFu) - 0x8000;
+        const bool ok = ex >= 27u && ex <= 227u && den < 0x1p120f &&
+                        fabsf(p.lr32 * u) <= __uint_as_float((ex + 4u) << 23) && (mid > 512 || mid < -512);
+        if (ok) static_cast<uint16_t*>(thb)[idx] = static_cast<uint16_t>((xb + 0x7FFFu + ((xb >> 16) & 1u)) >> 16);
+        else exact_update<KT>(&p, base, gwv, e, r, idx);
+    } else {
+        const double vv = ld_t<KT::VDT>(swv, e);
+        const double t = KT::PDT == BF16 ? static_cast<double>(__uint_as_float(
+                                               (idx & 1) ? (*reinterpret_cast<const uint32_t*>(sth) & 0xFFFF0000u)
+                                                         : (*reinterpret_cast<const uint32_t*>(sth) << 16)))
+                                         : ld_t<KT::PDT>(sth, 0);
+        const double mhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w1[r], vv)), p.scale1);
+        const double vhat = __dmul_rn(__dadd_rn(0.0, __dmul_rn(p.w2[r], __dmul_rn(vv, vv))), p.scale2);
+        const double u = __ddiv_rn(mhat, __dadd_rn(p.eps, __dsqrt_rn(vhat)));
+        st_t<KT::PDT>(thb, idx, __dsub_rn(t, __dmul_rn(p.lr, u)));
+    }
+}
+
+// The block's m window rows -> shared memory by two 1-D bulk copies completing
+// on one mbarrier (lane 0; phase 0 is awaited before the rows are used).
+__device__ __forceinline__ void stage_rows(uint64_t* bar, void* s_idx, const void* g_idx, void* s_val, const void* g_val,
+                                           uint32_t bytes_idx, uint32_t bytes_val) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(bar, bytes_idx + bytes_val);
+    bulk_g2s(s_idx, g_idx, bytes_idx, bar);
+    bulk_g2s(s_val, g_val, bytes_val, bar);
+}
 
 // Duplicated coordinates beyond one warp's worth of list entries
 // (window.cpp:32-39: terms summed in physical slot order). The ordered entry
@@ -1176,7 +1351,14 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     const int64_t b = p.block_offset + bl;
     const int64_t base = b * kBlk;
     const LLayout L(BUCKET, KT::CAPL);
-    unsigned char* ws = smem + warp * L.total;
+    // PH & 2: the block's m window rows (indices, then values) are staged after
+    // the warp's LLayout area by one bulk copy issued in the prologue
+    const uint32_t wrow_i = (PH & 2) ? static_cast<uint32_t>(align_up(size_t(p.m) * p.kb_stride * 2, 16)) : 0u;
+    const uint32_t wrow_v = (PH & 2) ? static_cast<uint32_t>(align_up(size_t(p.m) * p.kb_stride * vsz, 16)) : 0u;
+    unsigned char* ws = smem + warp * (L.total + wrow_i + wrow_v);
+    int16_t* s_widx = reinterpret_cast<int16_t*>(ws + L.total);
+    unsigned char* s_wval = ws + L.total + wrow_i;
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(ws + L.misc + 48);
     double2* s_ll = reinterpret_cast<double2*>(ws + L.ll);
     float4* s_llf = reinterpret_cast<float4*>(ws + L.llf);
     uint32_t* s_sel = reinterpret_cast<uint32_t*>(ws + L.sel);
@@ -1238,6 +1420,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         if constexpr (!KT::RS) prefetch_l2_keep(static_cast<const unsigned char*>(p.grads) + base * gsz, kBlk * gsz);
         prefetch_l2_keep(p.codes + base / 2, kBlk / 2);
         prefetch_l2(p.meta + base / BUCKET, NBK * 16);
+        if constexpr (PH & 2) stage_rows(s_bar, s_widx, gwi, s_wval, gwv, m * kbs * 2, m * kbs * vsz);
     }
     const uint32_t tstate = __ldg(p.thresh + b);
     const uint32_t T = tstate & 0xFFFFu;
@@ -1253,7 +1436,8 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         float Tf = CUDART_INF_F;  // T == 0: no carried threshold, no screen hits
         if (T != 0) Tf = __double2float_rd((VT - static_cast<double>(E)) * (1.0 - 0x1p-22));
         if (!(Tf > 0.0f)) Tf = 0.0f;
-        s_llf[i] = make_float4(__double2float_rn(mt.x), __double2float_rn(level), E, Tf);
+        // pass 1 tests a32² - T2 >= 0 with T2 = rd(Tf²) <= Tf² (stored negated)
+        s_llf[i] = make_float4(__double2float_rn(mt.x), __double2float_rn(level), E, -__fmul_rd(Tf, Tf));
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -1266,29 +1450,55 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     if (p.dbg) prof_mark(p, 1);
 #endif
     // ---- pass 1: fp32 screen of a = g + decode(EF) against the carried threshold ----
+    // Packed fp32 (FFMA2 / FADD2): c as a float by a byte permute into 2^23 + c,
+    // a32 = g + (c·level32 + lo32); hit <=> a32² - T2 >= 0 (T2 = rd(Tf²): a
+    // superset of |a32| >= Tf; inf / NaN give +inf / the canonical +NaN, hits).
+    // The sign bytes of 8 squares are gathered by byte permutes into one word:
+    // byte k, bit 2·(3 - jj) + h holds MISS of element k + 4h of iteration
+    // 4w + jj; four iterations fill cm_w (bits inverted at the end).
     uint32_t cm0 = 0, cm1 = 0, cm2 = 0, cm3 = 0;
     {
-        Raw8<KT::GDT> nr = load_raw8<KT::GDT, !KT::RS>(p.grads, base + lane * 8);
-        uint32_t ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + lane * 8) >> 1));
+        const unsigned char* gp = static_cast<const unsigned char*>(p.grads) + (base + lane * 8) * gsz;
+        const uint32_t* cp = reinterpret_cast<const uint32_t*>(p.codes + ((base + lane * 8) >> 1));
+        const float4* lf = s_llf + (lane * 8) / BUCKET;
+        uint32_t kmag;  // 0x4B000000 held in a register: the permutes below take immediate selectors
+        asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(kmag));
+        const float2 m23 = make_float2(-kTwo23, -kTwo23);
 #pragma unroll 1
-        for (int j = 0; j < kIter; ++j) {
-            const int e0 = j * 256 + lane * 8;
-            const Raw8<KT::GDT> r = nr;
-            const uint32_t cw = ncw;
-            if (j + 1 < kIter) {
-                nr = load_raw8<KT::GDT, !KT::RS>(p.grads, base + e0 + 256);
-                ncw = *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0 + 256) >> 1));
-            }
-            const float4 f = s_llf[e0 / BUCKET];
-            float a[8];
-            a32x8<KT::GDT>(r, cw, f.x, f.y, a);
-            uint32_t m8 = 0;
+        for (int w = 0; w < 4; ++w) {
+            uint32_t acc = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) m8 |= static_cast<uint32_t>(!(fabsf(a[i]) < f.w)) << i;
-            cm0 = __funnelshift_r(cm0, cm1, 8);
-            cm1 = __funnelshift_r(cm1, cm2, 8);
-            cm2 = __funnelshift_r(cm2, cm3, 8);
-            cm3 = (cm3 >> 8) | (m8 << 24);
+            for (int jj = 0; jj < 4; ++jj) {
+                const int j = w * 4 + jj;
+                const Raw8<KT::GDT> r = load_raw8<KT::GDT, !KT::RS>(gp + size_t(j) * 256 * gsz, 0);
+                const uint32_t cw = cp[j * 32];
+                const float4 f = lf[j * (256 / BUCKET)];
+                const uint32_t ce = cw & 0x0F0F0F0Fu, co = (cw >> 4) & 0x0F0F0F0Fu;
+                float g[8];
+                g32x8<KT::GDT>(r, g);
+                const float2 lv2 = make_float2(f.y, f.y), lo2 = make_float2(f.x, f.x), t2 = make_float2(f.w, f.w);
+                uint32_t sg[8];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float2 c = make_float2(__uint_as_float(prmt_imm<0x7540u>(ce, kmag, k)),
+                                           __uint_as_float(prmt_imm<0x7540u>(co, kmag, k)));
+                    c = __fadd2_rn(c, m23);
+                    const float2 a = __fadd2_rn(make_float2(g[2 * k], g[2 * k + 1]), __ffma2_rn(c, lv2, lo2));
+                    const float2 d = __ffma2_rn(a, a, t2);
+                    sg[2 * k] = __float_as_uint(d.x);
+                    sg[2 * k + 1] = __float_as_uint(d.y);
+                }
+                // top (sign) bytes of elements 0..3 and 4..7
+                const uint32_t w0 = __byte_perm(__byte_perm(sg[0], sg[1], 0x0073u), __byte_perm(sg[2], sg[3], 0x0073u), 0x5410u);
+                const uint32_t w1 = __byte_perm(__byte_perm(sg[4], sg[5], 0x0073u), __byte_perm(sg[6], sg[7], 0x0073u), 0x5410u);
+                // byte k: bit 0 = sign of element k, bit 1 = sign of element k + 4
+                const uint32_t b = ((w0 >> 7) & 0x01010101u) | ((w1 >> 6) & 0x02020202u);
+                acc = (acc << 2) | b;
+            }
+            cm0 = cm1;
+            cm1 = cm2;
+            cm2 = cm3;
+            cm3 = ~acc;
         }
     }
     const int nmine = __popc(cm0) + __popc(cm1) + __popc(cm2) + __popc(cm3);
@@ -1300,7 +1510,9 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
             while (bits) {
                 const int sb = __ffs(bits) - 1;
                 bits &= bits - 1;
-                f((w * 4 + (sb >> 3)) * 256 + lane * 8 + (sb & 7));
+                // byte k = sb >> 3; within it bit 2·(3 - jj) + h -> element k + 4h of iteration 4w + jj
+                const int jj = 3 - ((sb & 7) >> 1);
+                f((w * 4 + jj) * 256 + lane * 8 + (sb >> 3) + 4 * (sb & 1));
             }
         }
     };
@@ -1516,6 +1728,12 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     }
     __syncwarp();
     const int64_t row0 = static_cast<int64_t>(slot) * kbs;
+    if constexpr (PH & 2) {
+        // the staged copy of the ring (issued in the prologue) must land before
+        // this step's row overwrites slot `slot` in it
+        while (!mbar_try_wait(s_bar, 0)) {
+        }
+    }
     if (ncand >= 0) {
 #pragma unroll
         for (int s = 0; s < KT::CAPL; ++s)
@@ -1525,6 +1743,10 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                 const int pos = s_wpref[e >> 5] + __popc(s_sel[e >> 5] & ((1u << (e & 31)) - 1u));
                 gwi[row0 + pos] = static_cast<int16_t>(e);
                 st_t<KT::VDT>(gwv, row0 + pos, s_cval[q]);
+                if constexpr ((PH & 2) != 0) {
+                    s_widx[row0 + pos] = static_cast<int16_t>(e);
+                    st_t<KT::VDT>(s_wval, row0 + pos, s_cval[q]);
+                }
                 if constexpr (PH == 1) {
                     const int64_t so = (b - p.stage_b0) * kbs + pos;
                     p.stage_idx[so] = static_cast<int16_t>(e);
@@ -1541,6 +1763,10 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                 gwi[row0 + pos] = static_cast<int16_t>(e);
                 const double av = recompute_a<KT>(p, base, s_ll, e);
                 st_t<KT::VDT>(gwv, row0 + pos, av);
+                if constexpr ((PH & 2) != 0) {
+                    s_widx[row0 + pos] = static_cast<int16_t>(e);
+                    st_t<KT::VDT>(s_wval, row0 + pos, av);
+                }
                 if constexpr (PH == 1) {
                     const int64_t so = (b - p.stage_b0) * kbs + pos;
                     p.stage_idx[so] = static_cast<int16_t>(e);
@@ -1557,84 +1783,162 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     if (p.dbg) prof_mark(p, 4);
 #endif
     // ---- pass 2: residual (compress.cpp:95-102) + 4-bit re-quantization
-    //      (quantize.cpp:15-24, 42-55, 102-114, 142-162), exact fp64 ----
+    //      (quantize.cpp:15-24, 42-55, 102-114, 142-162): fp32 with exact
+    //      fallbacks (see the bound above exact_bucket16) ----
+    {
+        constexpr int LP2 = BUCKET / 16;  // lanes per bucket in this pass
+        const uint32_t bm = ((1u << LP2) - 1u) << (lane & ~(LP2 - 1));
+        // 2 KB of scratch: the word-prefix / seen, duplicate and candidate areas
+        // (re-zeroed below before ADAM_STATS uses them)
+        unsigned char* s_scr = ws + L.wpref;
+        const unsigned char* gp = static_cast<const unsigned char*>(p.grads) + base * gsz;
+        uint32_t kmag;
+        asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(kmag));
+        const float2 m23 = make_float2(-kTwo23, -kTwo23);
 #pragma unroll 1
-    for (int j = 0; j < kIter; ++j) {
-        const int e0 = j * 256 + lane * 8;
-        if ((PH & 2) && j == kIter / 2 && lane == 0) {
-            prefetch_l2(gwi, uint32_t(m * kbs * 2));
-            prefetch_l2(gwv, uint32_t(m * kbs * vsz));
-            prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
-        }
-        double a[8];
-        widen8<KT::GDT>(load_raw8<KT::GDT, !KT::RS>(p.grads, base + e0), a);
-        add_decoded8(a, *reinterpret_cast<const uint32_t*>(p.codes + ((base + e0) >> 1)), s_ll[e0 / BUCKET]);
-        const uint32_t sel8 = (s_sel[e0 >> 5] >> (e0 & 31)) & 0xFFu;
+        for (int j = 0; j < kBlk / 512; ++j) {
+            const int e0 = j * 512 + lane * 16;
+            if ((PH & 2) && j == 4 && lane == 0)
+                prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
+            const Raw16<KT::GDT> raw = load_raw16<KT::GDT, !KT::RS>(gp + size_t(e0) * gsz);
+            const uint2 cw = *reinterpret_cast<const uint2*>(p.codes + ((base + e0) >> 1));
+            const float4 f = s_llf[e0 / BUCKET];
+            const uint32_t sel16 = (s_sel[e0 >> 5] >> (e0 & 31)) & 0xFFFFu;
+            float r[16];
+            {
+                const float2 lv2 = make_float2(f.y, f.y), lo2 = make_float2(f.x, f.x);
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if ((sel8 >> i) & 1u) a[i] = 0.0;
-        double l4[4], h4[4];
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t c = h ? cw.y : cw.x;
+                    const uint32_t ce = c & 0x0F0F0F0Fu, co = (c >> 4) & 0x0F0F0F0Fu;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const bool lt = a[2 * k] < a[2 * k + 1];
-            l4[k] = lt ? a[2 * k] : a[2 * k + 1];
-            h4[k] = lt ? a[2 * k + 1] : a[2 * k];
-        }
-        double lo = l4[0] < l4[1] ? l4[0] : l4[1];
-        const double lo2 = l4[2] < l4[3] ? l4[2] : l4[3];
-        lo = lo < lo2 ? lo : lo2;
-        double hi = h4[0] > h4[1] ? h4[0] : h4[1];
-        const double hi2 = h4[2] > h4[3] ? h4[2] : h4[3];
-        hi = hi > hi2 ? hi : hi2;
-#pragma unroll
-        for (int off = 1; off < LPB; off <<= 1) {
-            const double ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
-            const double oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
-            lo = ol < lo ? ol : lo;
-            hi = oh > hi ? oh : hi;
-        }
-        // code = clamp(floor((r - lo) / level + 0.5)): t = (r - lo) * k with
-        // k = 15 / (hi - lo) to fp32 accuracy (relative error < 2^-21). One DFMA
-        // forms 2^24 + t + 0.5 + G 2^-28, whose low word holds the code in bits
-        // 28..31 and a 28-bit fraction; |t - q| < 2^-16.5 < G 2^-28 (G = 2^13).
-        // A fraction within G of an integer sends the 8 codes to the IEEE
-        // quotient (quantize.cpp:51-53).
-        const double rng = __dsub_rn(hi, lo);
-        uint32_t word = 0;
-        if (rng != 0.0) {
-            const float r32 = __double2float_rn(rng);
-            bool bad = true;
-            if (r32 >= 0x1p-100f && r32 <= 0x1p100f) {
-                const double k64 = static_cast<double>(__fdividef(15.0f, r32));
-                const double add = 0x1p24 + 0.5 + 0x1p-15;
-                bad = false;
-#pragma unroll
-                for (int i = 7; i >= 0; --i) {
-                    const uint32_t y = static_cast<uint32_t>(__double_as_longlong(__fma_rn(__dsub_rn(a[i], lo), k64, add)));
-                    word = __funnelshift_l(y, word, 4);
-                    bad |= (y << 4) < (2u << 17);  // fraction < 2G = 2^14 (of 2^28)
+                    for (int k = 0; k < 4; ++k) {
+                        float2 cc = make_float2(__uint_as_float(prmt_imm<0x7540u>(ce, kmag, k)),
+                                                __uint_as_float(prmt_imm<0x7540u>(co, kmag, k)));
+                        cc = __fadd2_rn(cc, m23);
+                        const int i = 8 * h + 2 * k;
+                        const float2 a = __fadd2_rn(make_float2(g32_of<KT::GDT>(raw, i), g32_of<KT::GDT>(raw, i + 1)),
+                                                    __ffma2_rn(cc, lv2, lo2));
+                        r[i] = a.x;
+                        r[i + 1] = a.y;
+                    }
                 }
             }
-            if (bad) {  // rare: the exact quotient
-                const double level = __ddiv_rn(rng, 15.0);
-                word = 0;
 #pragma unroll
-                for (int i = 7; i >= 0; --i) word = (word << 4) | exact_code_w(a[i], lo, level);
-                if (p.dbg) atomicAdd(p.dbg + 1, 8u);
+            for (int i = 0; i < 16; ++i)
+                if ((sel16 >> i) & 1u) r[i] = 0.0f;
+            float mn = r[0], mx = r[0];
+#pragma unroll
+            for (int i = 1; i < 16; ++i) {
+                mn = fminf(mn, r[i]);
+                mx = fmaxf(mx, r[i]);
             }
+#pragma unroll
+            for (int off = 1; off < LP2; off <<= 1) {
+                mn = fminf(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, off));
+                mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+            }
+            const float eps = __fmaf_ru(fmaxf(fabsf(mn), fabsf(mx)), 0x1p-23f, f.z);
+            const float R = __fsub_rd(mx, mn);
+            const float den = __fsub_rd(R, 2.0f * eps);
+            const float k2 = __fdividef(30.0f, R);
+            const float cmag = 258.0f + fabsf(mn * k2);
+            const float G = __fmaf_ru(128.0f, __fdividef(eps, den), __fmaf_ru(cmag, 0x1p-23f, 0x1p-13f));
+            const bool fast = R >= 0x1p-100f && R <= 0x1p100f && den > 0.0f && G <= 0.0625f;  // bucket-uniform
+            uint32_t w0 = 0, w1 = 0, bnd = 0;
+            bool bad = false;
+            double lmin = CUDART_INF, lmax = -CUDART_INF;
+            if (fast) {
+                const float c2 = __fmaf_rn(-mn, k2, 257.0f + G);
+                const uint32_t Gu = static_cast<uint32_t>(__fmaf_ru(2.0f, G, 0x1p-13f) * 32768.0f) + 1u;
+                uint32_t yb[16];
+                const float2 k22 = make_float2(k2, k2), c22 = make_float2(c2, c2);
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    const float2 y = __ffma2_rn(make_float2(r[i], r[i + 1]), k22, c22);
+                    yb[i] = __float_as_uint(y.x);
+                    yb[i + 1] = __float_as_uint(y.y);
+                }
+                w0 = pack_codes8(yb);
+                w1 = pack_codes8(yb + 8);
+                uint32_t fl = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) fl |= static_cast<uint32_t>((yb[i] & 0x7FFFu) < Gu) << i;
+                if (fl) {  // min / max candidates and code boundaries (~2 per bucket)
+                    // this lane's raw gradients -> its 64-byte scratch slot (dead
+                    // candidate / bitmap area) so flagged elements index them
+                    uint4* slot = reinterpret_cast<uint4*>(s_scr) + lane * (64 / 16);
+#pragma unroll
+                    for (int k = 0; k < Raw16<KT::GDT>::N; ++k) slot[k] = raw.v[k];
+                    const double2 q = s_ll[e0 / BUCKET];
+                    do {
+                        const int i = __ffs(fl) - 1;
+                        fl &= fl - 1;
+                        const bool s = (sel16 >> i) & 1u;
+                        const uint32_t c = ((i < 8 ? cw.x : cw.y) >> (4 * (i & 7))) & 15u;
+                        const float g = KT::GDT == BF16
+                                            ? __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(slot)[i]) << 16)
+                                            : reinterpret_cast<const float*>(slot)[i];
+                        const float r32 = s ? 0.0f : __fadd_rn(g, __fmaf_rn(static_cast<float>(c), f.y, f.x));
+                        const uint32_t N = (__float_as_uint(__fmaf_rn(r32, k2, c2)) >> 15) & 0xFFu;
+                        if (N == 0u || N > 31u) {
+                            bad = true;
+                        } else if (N == 1u || N == 31u) {
+                            const double rx = s ? 0.0
+                                                : __dadd_rn(static_cast<double>(g),
+                                                            __dadd_rn(__dmul_rn(static_cast<double>(c), q.y), q.x));
+                            if (N == 1u) lmin = rx < lmin ? rx : lmin;
+                            else lmax = rx > lmax ? rx : lmax;
+                        } else if ((N & 1u) == 0u) {
+                            bnd |= 1u << i;
+                        }
+                    } while (fl);
+                }
+            }
+#pragma unroll
+            for (int off = 1; off < LP2; off <<= 1) {  // the bucket's exact extremes (all lanes)
+                const double ol = __shfl_xor_sync(0xFFFFFFFFu, lmin, off), oh = __shfl_xor_sync(0xFFFFFFFFu, lmax, off);
+                lmin = ol < lmin ? ol : lmin;
+                lmax = oh > lmax ? oh : lmax;
+                bad |= __shfl_xor_sync(0xFFFFFFFFu, bad, off);
+            }
+            bad = bad || !fast || !(lmin < CUDART_INF) || !(lmax > -CUDART_INF);  // bucket-uniform
+            double lo_n = lmin, hi_n = lmax;
+            if (bad) {
+                const Bucket16 o = exact_bucket16<KT>(&p, base, e0, sel16, s_ll[e0 / BUCKET], bm, LP2);
+                w0 = o.w0;
+                w1 = o.w1;
+                lo_n = o.lo;
+                hi_n = o.hi;
+                if (p.dbg) atomicAdd(p.dbg + 1, 16u);
+            } else if (bnd) {  // rare: quotients within the guard band of a code boundary
+                const double level = __ddiv_rn(__dsub_rn(hi_n, lo_n), 15.0);
+                const double2 q = s_ll[e0 / BUCKET];
+                while (bnd) {
+                    const int i = __ffs(bnd) - 1;
+                    bnd &= bnd - 1;
+                    const double rx = ((sel16 >> i) & 1u) ? 0.0 : recompute_a_q<KT>(p, base, e0 + i, q);
+                    const uint32_t c = exact_code_w(rx, lo_n, level);
+                    if (i < 8) w0 = (w0 & ~(15u << (4 * i))) | (c << (4 * i));
+                    else w1 = (w1 & ~(15u << (4 * (i - 8)))) | (c << (4 * (i - 8)));
+                }
+                if (p.dbg) atomicAdd(p.dbg + 1, 1u);
+            }
+            __stcs(reinterpret_cast<uint2*>(p.codes + ((base + e0) >> 1)), make_uint2(w0, w1));
+            if ((lane & (LP2 - 1)) == 0) __stcs(p.meta + (base + e0) / BUCKET, make_double2(lo_n, hi_n));
         }
-        __stcs(reinterpret_cast<unsigned int*>(p.codes + ((base + e0) >> 1)), word);
-        if ((lane & (LPB - 1)) == 0) __stcs(p.meta + (base + e0) / BUCKET, make_double2(lo, hi));
     }
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) s_seen[lane * 4 + k] = 0;
+    for (int k = 0; k < 4; ++k) {
+        s_seen[lane * 4 + k] = 0;
+        s_dup[lane * 4 + k] = 0;
+    }
     __syncwarp();
     }  // PH & 1
     if constexpr (PH == 2) {
         if (lane == 0) {
-            prefetch_l2(gwi, uint32_t(m * kbs * 2));
-            prefetch_l2(gwv, uint32_t(m * kbs * vsz));
+            stage_rows(s_bar, s_widx, gwi, s_wval, gwv, m * kbs * 2, m * kbs * vsz);
             prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
         }
 #pragma unroll
@@ -1643,6 +1947,8 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
             s_dup[lane * 4 + k] = 0;
         }
         __syncwarp();
+        while (!mbar_try_wait(s_bar, 0)) {
+        }
     }
     if constexpr (PH & 2) {
 
@@ -1665,7 +1971,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
             ++r;
         }
     };
-    const int16_t* __restrict__ wi = gwi;  // this block's [m][kbs] index ring
+    // the block's ring rows are staged in shared memory (s_widx / s_wval)
     {
         int r = r0, pos = pos0;
 #pragma unroll 1
@@ -1675,8 +1981,8 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
             const bool hb = t + 32 < nent;
             const int eb = hb ? r * kbs + pos : ea;
             advance(r, pos);
-            const int ia = wi[ea];
-            const int ib = wi[eb];
+            const int ia = s_widx[ea];
+            const int ib = s_widx[eb];
             uint32_t bit = 1u << (ia & 31);
             if (atomicOr(&s_seen[ia >> 5], bit) & bit) atomicOr(&s_dup[ia >> 5], bit);
             if (hb) {
@@ -1692,39 +1998,52 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     int* dupl = reinterpret_cast<int*>(s_cval);
     int ndup = 0;
     {
+        // Coordinates held by one entry: θ of a chunk of entries is fetched with
+        // one round of cp.async (LDGSTS) into the dead pass-2 tables (ll, llf),
+        // then every entry is updated from shared memory.
         void* thb = static_cast<unsigned char*>(p.params) + base * psz;  // this block's θ
-        int r = r0, pos = pos0;
-        constexpr int SB = MA_LEAN_SB;  // entries per lane in flight
+        constexpr int tsz = psz < 4 ? 4 : psz;                             // copy granule per entry
+        unsigned char* s_th = ws + L.ll;
+        const int chunk = static_cast<int>((L.sel - L.ll) / tsz);          // entries per round
         const int dup_max = static_cast<int>((L.cidx - L.cval) / 4);
+        int r = r0, pos = pos0;
 #pragma unroll 1
-        for (int t0 = lane; t0 < nent + lane; t0 += 32 * SB) {
-            int e[SB], idx[SB], rr[SB], ps[SB];
-            bool act[SB], mine[SB];
-#pragma unroll
-            for (int k = 0; k < SB; ++k) {
-                act[k] = t0 + 32 * k < nent;
-                rr[k] = r;
-                ps[k] = pos;
-                e[k] = r * kbs + pos;
-                idx[k] = act[k] ? wi[e[k]] : 0;
-                advance(r, pos);
+        for (int c0 = 0; c0 < nent; c0 += chunk) {
+            const int c1 = min(nent, c0 + chunk);
+            // round 1: the θ words of this lane's unique entries
+            {
+                int rr = r, pp = pos;
+#pragma unroll 1
+                for (int t = c0 + lane; t < c1; t += 32) {
+                    const int e = rr * kbs + pp;
+                    advance(rr, pp);
+                    const int idx = s_widx[e];
+                    if (!((s_dup[idx >> 5] >> (idx & 31)) & 1u)) {
+                        const unsigned char* src = static_cast<const unsigned char*>(thb) +
+                                                   (psz < 4 ? (static_cast<uint32_t>(idx) * psz) & ~3u
+                                                            : static_cast<uint32_t>(idx) * psz);
+                        cp_async_g2s<tsz>(s_th + (t - c0) * tsz, src);
+                    }
+                }
+                cp_async_wait_all();
             }
-            UniqueUpd<KT> u[SB];
-#pragma unroll
-            for (int k = 0; k < SB; ++k) {
-                const bool dup = act[k] && ((s_dup[idx[k] >> 5] >> (idx[k] & 31)) & 1u);
-                mine[k] = act[k] && !dup;
-                if (mine[k]) u[k].load(thb, gwv, e[k], idx[k]);
+            // round 2: updates (and the ordered list of duplicated entries)
+#pragma unroll 1
+            for (int t0 = c0 + lane; t0 < c1 + lane; t0 += 32) {
+                const bool act = t0 < c1;
+                const int e = r * kbs + pos;
+                const int rr = r, pp = pos;
+                advance(r, pos);
+                const int idx = act ? s_widx[e] : 0;
+                const bool dup = act && ((s_dup[idx >> 5] >> (idx & 31)) & 1u);
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
                 if (bal) {
                     const int qd = ndup + __popc(bal & lanemask_lt());
-                    if (dup && qd < dup_max) dupl[qd] = (idx[k] << 16) | (rr[k] << 8) | ps[k];
+                    if (dup && qd < dup_max) dupl[qd] = (idx << 16) | (rr << 8) | pp;
                     ndup += __popc(bal);
                 }
+                if (act && !dup) unique_update_smem<KT>(p, base, thb, gwv, s_wval, s_th + (t0 - c0) * tsz, e, rr, idx);
             }
-#pragma unroll
-            for (int k = 0; k < SB; ++k)
-                if (mine[k]) u[k].finish(p, base, thb, gwv, e[k], rr[k], idx[k]);
         }
     }
     __syncwarp();
@@ -1744,7 +2063,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         const int idx = x >> 16, r = (x >> 8) & 0xFF, pos = x & 0xFF;
         double t1 = 0.0, t2 = 0.0;
         if (has) {
-            const double v = ld_t<KT::VDT>(gwv, r * kbs + pos);
+            const double v = ld_t<KT::VDT>(s_wval, r * kbs + pos);
             t1 = __dmul_rn(p.w1[r], v);
             t2 = __dmul_rn(p.w2[r], __dmul_rn(v, v));
         }
@@ -1781,7 +2100,13 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
 
 template <class KT, int PH = 3>
 cudaError_t launch_kl(const StepArgs& a, cudaStream_t s) {
-    const size_t smem = size_t(kWarps) * LLayout(KT::BUCKET, KT::CAPL).total;
+    constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
+    // per warp: the LLayout area + (PH & 2) the staged window rows (indices, values)
+    const size_t rows = (PH & 2) ? align_up(size_t(a.m) * a.kb_stride * 2, 16) +
+                                       align_up(size_t(a.m) * a.kb_stride * vsz, 16)
+                                 : 0;
+    const size_t smem = size_t(kWarps) * (LLayout(KT::BUCKET, KT::CAPL).total + rows);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     auto k = microadam_step_lean<KT, PH>;
     cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem));

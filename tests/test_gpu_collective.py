@@ -115,11 +115,11 @@ def _rank_main(rank, world, port, d, steps, out_dir):
         g = _dev(oracle.synth(42, s, e0, e1 - e0, "bf16"))  # only this rank's gradient shard
         eng.step(full[e0:e1], g, 1e-2)
         # the all-gather of the updated shards (ma_step_allgather's exchange), staged through gloo
-        mine = torch.zeros(stride, dtype=torch.int16)
-        mine[: e1 - e0] = full[e0:e1].view(torch.int16).cpu()
-        parts = [torch.empty(stride, dtype=torch.int16) for _ in range(world)]
+        mine = torch.zeros(2 * stride, dtype=torch.uint8)  # bf16 bytes (gloo has no 16-bit ints)
+        mine[: 2 * (e1 - e0)] = full[e0:e1].view(torch.uint8).cpu()
+        parts = [torch.empty(2 * stride, dtype=torch.uint8) for _ in range(world)]
         dist.all_gather(parts, mine)
-        full.copy_(torch.cat(parts)[:d].view(torch.bfloat16).cuda())
+        full.copy_(torch.cat(parts)[: 2 * d].view(torch.bfloat16).cuda())
     torch.cuda.synchronize()
     eb = eng.error_buffer()
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), theta=full.view(torch.int16).cpu().numpy(),

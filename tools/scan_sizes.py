@@ -32,7 +32,7 @@ for d in sizes:
         if dbgon:
             cur = eng.debug_counters()
             if prev is not None:
-                per.append({k: cur[k] - prev[k] for k in cur})
+                per.append({k: cur[k] - prev[k] for k in cur if k != "phase_cycles"})
             prev = cur
     t = sorted(times[6:])[len(times[6:]) // 2]
     dbg = eng.debug_counters() if os.environ.get("MA_DEBUG_COUNTERS") == "1" else {}
@@ -42,6 +42,6 @@ for d in sizes:
     for i, c in enumerate(per):
         print(f"   step {i + 2:3d}: misses {c['threshold_misses'] / nb:6.3f}  too_low {c['threshold_too_low'] / nb:6.3f}"
               f"  exactq/blk {c['exact_quotient_elems'] / nb:6.2f}  fallback {c['select_fallback_blocks']}"
-              f"  refine {c['threshold_refinements'] / nb:6.3f}  dup/blk {c['dup_entries'] / nb:6.1f}  dup-overflow {c['dup_list_overflow_blocks'] / nb:6.3f}")
+              f"  flagged/blk {c['select_fallback_blocks'] / nb:7.2f}  refine {c['threshold_refinements'] / nb:6.3f}  dup/blk {c['dup_entries'] / nb:6.1f}  dup-overflow {c['dup_list_overflow_blocks'] / nb:6.3f}")
     del eng, p, g
     torch.cuda.empty_cache()
