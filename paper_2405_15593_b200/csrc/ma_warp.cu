@@ -193,6 +193,18 @@ __device__ __noinline__ int tie_rank_w(const double* cval, const int16_t* cidx, 
     return extra;
 }
 
+// rn(x / 15) (QuantParams level, quantize.cpp:12) without the fp64 division
+// sequence: q0 = rn(x c), c = rn(1/15); the remainder x - 15 q0 is exact by
+// FMA and rn(q0 + r c) is the correctly rounded quotient (Markstein; checked
+// against x / 15 on 4e8 random normal x). Outside [2^-960, 2^1000] (and for
+// non-finite x) the IEEE division.
+__device__ __forceinline__ double div15_w(double x) {
+    if (!(x >= 0x1p-960 && x <= 0x1p1000)) return __ddiv_rn(x, 15.0);
+    const double c = 0x1.1111111111111p-4;
+    const double q0 = __dmul_rn(x, c);
+    return __fma_rn(__fma_rn(-q0, 15.0, x), c, q0);
+}
+
 // The IEEE path of quantize_nearest (quantize.cpp:51-53) for an element whose
 // fixed-point estimate fell in the guard band. Out of line: rare.
 __device__ __noinline__ uint32_t exact_code_w(double x, double lo, double level) {
@@ -1085,7 +1097,7 @@ __device__ __noinline__ Bucket16 exact_bucket16(const StepArgs* pp, int64_t base
     }
     Bucket16 o{0u, 0u, lo, hi};
     if (lo != hi) {
-        const double level = __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+        const double level = div15_w(__dsub_rn(hi, lo));
         for (int i = 15; i >= 0; --i) {
             const double r = ((sel16 >> i) & 1u) ? 0.0 : recompute_a_q<KT>(p, base, e0 + i, ll);
             const uint32_t c = exact_code_w(r, lo, level);
@@ -1428,7 +1440,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     const double VT = __longlong_as_double(static_cast<long long>(static_cast<uint64_t>(T) << 48));
     for (int i = lane; i < NBK; i += 32) {
         const double2 mt = p.meta[base / BUCKET + i];
-        const double level = (mt.x == mt.y) ? 0.0 : __ddiv_rn(__dsub_rn(mt.y, mt.x), 15.0);
+        const double level = (mt.x == mt.y) ? 0.0 : div15_w(__dsub_rn(mt.y, mt.x));
         s_ll[i] = make_double2(mt.x, level);
         const double M = fmax(fabs(mt.x), fabs(mt.y));
         float E = __double2float_ru(M * 0x1p-21 + 0x1p-120);
@@ -1912,7 +1924,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                 hi_n = o.hi;
                 if (p.dbg) atomicAdd(p.dbg + 1, 16u);
             } else if (bnd) {  // rare: quotients within the guard band of a code boundary
-                const double level = __ddiv_rn(__dsub_rn(hi_n, lo_n), 15.0);
+                const double level = div15_w(__dsub_rn(hi_n, lo_n));
                 const double2 q = s_ll[e0 / BUCKET];
                 while (bnd) {
                     const int i = __ffs(bnd) - 1;
