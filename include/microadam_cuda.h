@@ -190,7 +190,8 @@ MA_API ma_status ma_read_error_vector(ma_handle* h, double* out);
 /* error_buffer() restricted to blocks [block_begin, block_end) of the handle:
  * their packed codes (elements [block_begin*block, min(block_end*block, dim)),
  * byte-aligned since block*bits is a multiple of 8) and their buckets' (lo, hi).
- * For parity checks of sampled block ranges of very large handles. */
+ * For parity checks of sampled block ranges of very large handles. On a
+ * global Top-K handle (blockwise = 0) a "block" is a 4096-element chunk. */
 MA_API ma_status ma_read_error_buffer_blocks(ma_handle* h, int64_t block_begin, int64_t block_end, uint8_t* codes,
                                              double* lo, double* hi);
 

@@ -110,8 +110,6 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
     }
     if (!cfg->blockwise && s.block > ma::kMaxBlock) {
         // Global Top-K over the whole vector (compress.cpp:66-71): ma_global.cu
-        if (dim >= (int64_t(1) << 31))
-            return fail(MA_ERR_UNSUPPORTED, "global mode: dim >= 2^31 not supported on device");
         if (4096 % hp.bucket != 0)
             return fail(MA_ERR_UNSUPPORTED, "global mode on device needs bucket | 4096");
         if (b0 != 0 || (b1 >= 0 && b1 != 1))
@@ -163,7 +161,7 @@ void fill_layout(const Shape& s, const ma_config& cfg, ma_layout_info* o) {
     o->code_bytes = s.code_bytes;
     o->kb_stride = s.kb_stride;
     const int64_t went = o->num_blocks * cfg.hp.window * s.kb_stride;
-    o->state_bytes = s.code_bytes + s.nbuckets * 16 + went * (2 + int64_t(dtype_size(cfg.value_dtype)));
+    o->state_bytes = s.code_bytes + s.nbuckets * 16 + went * ((s.global ? 8 : 2) + int64_t(dtype_size(cfg.value_dtype)));
 }
 
 }  // namespace
@@ -196,7 +194,7 @@ struct ma_handle {
     int2* g_selinfo = nullptr;
     unsigned long long* g_selstate = nullptr;
     uint64_t* g_cand = nullptr;
-    int32_t* g_cand_idx = nullptr;
+    int64_t* g_cand_idx = nullptr;
     int32_t* g_ovf = nullptr;
     unsigned cand_cap = 0;
     int32_t* g_bounds = nullptr;
@@ -460,7 +458,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.codes = h->d_codes;
     g.meta = h->d_meta;
     g.level = h->g_level;
-    g.win_idx = reinterpret_cast<int32_t*>(h->d_win_idx);
+    g.win_idx = reinterpret_cast<int64_t*>(h->d_win_idx);
     g.win_val = h->d_win_val;
     g.selbits = h->g_selbits;
     g.hist = h->g_hist;
@@ -616,14 +614,16 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     int smem_max = 0;
     cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     const char* force_generic = std::getenv("MA_FORCE_GENERIC");
-    const ma::Variant fv = ma::pick_fast_variant(int(s.block), int(s.bucket), int(cfg->hp.window),
+    // global Top-K handles (block = d, possibly >= 2^31) never use these kernels
+    const int blk_i = s.global ? 4096 : int(s.block);
+    const ma::Variant fv = ma::pick_fast_variant(blk_i, int(s.bucket), int(cfg->hp.window),
                                                  int(s.kb_stride), cfg->grad_dtype,
                                                  cfg->param_dtype, cfg->value_dtype);
-    h->tail_variant = ma::pick_variant(static_cast<int>(s.block));
-    size_t smem = ma::step_smem_bytes(h->tail_variant.nt, h->tail_variant.ept, int(s.block),
+    h->tail_variant = ma::pick_variant(blk_i);
+    size_t smem = ma::step_smem_bytes(h->tail_variant.nt, h->tail_variant.ept, blk_i,
                                       int(s.bucket), int(cfg->hp.window), int(s.kb_stride), int(cfg->hp.bits));
     if (fv.nt && !(force_generic && force_generic[0] == '1')) {
-        const size_t fs = ma::fast_smem_bytes(fv, int(s.block), int(s.bucket), int(cfg->hp.window),
+        const size_t fs = ma::fast_smem_bytes(fv, blk_i, int(s.bucket), int(cfg->hp.window),
                                               int(s.kb_stride), cfg->grad_dtype, cfg->param_dtype,
                                               cfg->value_dtype);
         const int per_sm = fs <= size_t(smem_max) ? ma::fast_blocks_per_sm(fv, int(s.bucket), fs) : 0;
@@ -638,7 +638,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     }
     const char* force_cta = std::getenv("MA_FAST_CTA");  // A/B: the CTA-per-block fast kernel
     if (h->fast && !(force_cta && force_cta[0] == '1') &&
-        ma::warp_path_ok(int(s.block), int(s.bucket), int(s.per_block_k), int(cfg->hp.window),
+        ma::warp_path_ok(blk_i, int(s.bucket), int(s.per_block_k), int(cfg->hp.window),
                          int(s.kb_stride), cfg->grad_dtype, cfg->param_dtype, cfg->value_dtype) &&
         ma::warp_smem_bytes(int(s.bucket)) <= size_t(smem_max))
         h->warp = true;
@@ -668,7 +668,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
     };
     alloc(reinterpret_cast<void**>(&h->d_codes), size_t(s.code_bytes));
     alloc(reinterpret_cast<void**>(&h->d_meta), size_t(s.nbuckets) * sizeof(double2));
-    alloc(reinterpret_cast<void**>(&h->d_win_idx), went * (s.global ? sizeof(int32_t) : sizeof(int16_t)));
+    alloc(reinterpret_cast<void**>(&h->d_win_idx), went * (s.global ? sizeof(int64_t) : sizeof(int16_t)));
     if (s.global) {
         const int64_t nch = ma::global_chunks(s.dim);
         alloc(reinterpret_cast<void**>(&h->g_level), size_t(s.nbuckets) * sizeof(double));
@@ -682,7 +682,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         const char* cc = std::getenv("MA_GLOBAL_CAND_CAP");
         h->cand_cap = cc ? static_cast<unsigned>(std::strtoul(cc, nullptr, 10)) : kGlobalCandCap;
         alloc(reinterpret_cast<void**>(&h->g_cand), size_t(h->cand_cap) * sizeof(uint64_t));
-        alloc(reinterpret_cast<void**>(&h->g_cand_idx), size_t(h->cand_cap) * sizeof(int32_t));
+        alloc(reinterpret_cast<void**>(&h->g_cand_idx), size_t(h->cand_cap) * sizeof(int64_t));
         alloc(reinterpret_cast<void**>(&h->g_bounds), size_t(cfg->hp.window) * size_t(nch + 1) * sizeof(int32_t));
     }
     alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));
@@ -968,12 +968,14 @@ ma_status ma_read_error_buffer_blocks(ma_handle* h, int64_t block_begin, int64_t
     if (!h) return fail(MA_ERR_INVALID_ARG, "null handle");
     if (h->d_dense) return fail(MA_ERR_STATE, "error_buffer: engine uses dense error storage");
     const Shape& s = h->shape;
-    if (s.global) return fail(MA_ERR_UNSUPPORTED, "error_buffer_blocks: blockwise handles only");
-    if (block_begin < 0 || block_end > s.b1 - s.b0 || block_begin >= block_end)
+    // global Top-K handles: "blocks" are 4096-element chunks of the vector
+    const int64_t unit = s.global ? 4096 : s.block;
+    const int64_t nunits = s.global ? (s.dim + unit - 1) / unit : s.b1 - s.b0;
+    if (block_begin < 0 || block_end > nunits || block_begin >= block_end)
         return fail(MA_ERR_INVALID_ARG, "block range outside the handle");
     DeviceGuard g(h->device);
     { ma_status ws = wait_done(h); if (ws != MA_OK) return ws; }
-    const int64_t e0 = block_begin * s.block, e1 = std::min(s.dim, block_end * s.block);
+    const int64_t e0 = block_begin * unit, e1 = std::min(s.dim, block_end * unit);
     const int64_t bits = h->cfg.hp.bits;
     if (codes) {
         const int64_t c0 = (e0 * bits) / 8, c1 = (e1 * bits + 7) / 8;
@@ -1070,11 +1072,11 @@ ma_status ma_read_window_row(ma_handle* h, int64_t slot, int64_t* indices, doubl
     const Shape& s = h->shape;
     const int64_t nb = s.b1 - s.b0, m = h->cfg.hp.window, kbs = s.kb_stride;
     const size_t vsz = dtype_size(h->cfg.value_dtype);
-    if (s.global) {  // [m][kb_stride] int32 global indices
-        std::vector<int32_t> gi(static_cast<size_t>(s.row_width));
+    if (s.global) {  // [m][kb_stride] int64 global indices
+        std::vector<int64_t> gi(static_cast<size_t>(s.row_width));
         std::vector<unsigned char> gv(size_t(s.row_width) * vsz);
-        MA_CUDA(cudaMemcpy(gi.data(), reinterpret_cast<const int32_t*>(h->d_win_idx) + slot * kbs,
-                           gi.size() * 4, cudaMemcpyDeviceToHost));
+        MA_CUDA(cudaMemcpy(gi.data(), reinterpret_cast<const int64_t*>(h->d_win_idx) + slot * kbs,
+                           gi.size() * 8, cudaMemcpyDeviceToHost));
         MA_CUDA(cudaMemcpy(gv.data(), static_cast<const char*>(h->d_win_val) + size_t(slot * kbs) * vsz, gv.size(),
                            cudaMemcpyDeviceToHost));
         for (int64_t j = 0; j < s.row_width; ++j) {
@@ -1176,7 +1178,7 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
         }
     };
     if (s.global) {
-        std::vector<int32_t> gi(static_cast<size_t>(m * kbs), 0);
+        std::vector<int64_t> gi(static_cast<size_t>(m * kbs), 0);
         std::vector<unsigned char> gv(size_t(m * kbs) * vsz, 0);
         for (int64_t r = 0; r < m; ++r)
             for (int64_t j = 0; j < s.row_width; ++j) {
@@ -1185,11 +1187,11 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
                     return fail(MA_ERR_INVALID_ARG, "window index outside the vector");
                 if (stamps[r] != 0 && j > 0 && idx <= win_indices[r * s.row_width + j - 1])
                     return fail(MA_ERR_INVALID_ARG, "window row indices are not strictly increasing");
-                gi[size_t(r * kbs + j)] = int32_t(idx < 0 ? 0 : idx);
+                gi[size_t(r * kbs + j)] = idx < 0 ? 0 : idx;
                 put_val(&gv[size_t(r * kbs + j) * vsz], win_values[r * s.row_width + j]);
             }
         { ma_status cs = commit_ef(); if (cs != MA_OK) return cs; }
-        MA_CUDA(cudaMemcpy(h->d_win_idx, gi.data(), gi.size() * 4, cudaMemcpyHostToDevice));
+        MA_CUDA(cudaMemcpy(h->d_win_idx, gi.data(), gi.size() * 8, cudaMemcpyHostToDevice));
         MA_CUDA(cudaMemcpy(h->d_win_val, gv.data(), gv.size(), cudaMemcpyHostToDevice));
         h->step = step;
         h->head = head;

@@ -22,7 +22,7 @@
 //   G6  the update θ -= lr · mhat / (eps + sqrt(vhat)) (optim.cpp:183-187) for
 //       every coordinate with a nonzero accumulator (u = 0 elsewhere).
 // Passes over d read the gradient and codes 8 elements per thread (g_a8).
-// Window rows: int32 global indices [m][row stride] + values.
+// Window rows: int64 global indices [m][row stride] + values (any d).
 #include <math_constants.h>
 
 #include <cstdlib>
@@ -178,7 +178,7 @@ __global__ void g_hist(GlobalArgs p, int shift, int nbins, int collect, int from
                 if ((inm >> e) & 1u) {
                     if (base < p.cand_cap) {
                         p.cand[base] = key_of(a[e]);
-                        p.cand_idx[base] = static_cast<int32_t>(gi * 8 + e);
+                        p.cand_idx[base] = gi * 8 + e;
                     }
                     ++base;
                 }
@@ -283,10 +283,10 @@ __global__ void g_emit(GlobalArgs p) {
         }
     int tot;
     int pos = cs.x + cta_excl_scan(__popc(selm), s_tmp, tot);
-    int32_t* ri = p.win_idx + int64_t(p.slot) * p.row_stride;
+    int64_t* ri = p.win_idx + int64_t(p.slot) * p.row_stride;
     for (int j = 0; j < kPer; ++j)
         if ((selm >> j) & 1u) {
-            ri[pos] = static_cast<int32_t>(e0 + j);
+            ri[pos] = e0 + j;
             st_val(p.win_val, p.v_dtype, int64_t(p.slot) * p.row_stride + pos, av[j]);
             ++pos;
         }
@@ -520,10 +520,10 @@ __global__ void g_bounds(GlobalArgs p, int filled) {
     const int64_t n = int64_t(filled) * p.k;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n; t += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = t / p.k, j = t - r * p.k;
-        const int32_t* ri = p.win_idx + r * p.row_stride;
+        const int64_t* ri = p.win_idx + r * p.row_stride;
         int32_t* bd = p.bounds + r * (nch + 1);
-        const int64_t c = int64_t(ri[j]) / kChunk;
-        const int64_t cp = j > 0 ? int64_t(ri[j - 1]) / kChunk : -1;
+        const int64_t c = ri[j] / kChunk;
+        const int64_t cp = j > 0 ? ri[j - 1] / kChunk : -1;
         for (int64_t cc = cp + 1; cc <= c; ++cc) bd[cc] = static_cast<int32_t>(j);
         if (j == p.k - 1)
             for (int64_t cc = c + 1; cc <= nch; ++cc) bd[cc] = static_cast<int32_t>(p.k);

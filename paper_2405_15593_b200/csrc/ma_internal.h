@@ -70,7 +70,7 @@ struct GlobalArgs {
     uint8_t* codes;
     double2* meta;
     double* level;       // [nbuckets] level of the EF being decoded
-    int32_t* win_idx;    // [m][row_stride] global indices
+    int64_t* win_idx;    // [m][row_stride] global indices (int64: d may exceed 2^31)
     void* win_val;       // [m][row_stride] values (v_dtype)
     uint16_t* selbits;   // selection bits, 16 elements per word
     uint32_t* hist;      // [2048] radix histogram
@@ -78,7 +78,7 @@ struct GlobalArgs {
     int2* sel_info;        // [chunks] (row offset, ties taken)
     unsigned long long* sel_state;  // radix select on device: [0] key prefix (K* at the end), [1] mask, [2] ties left
     uint64_t* cand;       // keys sharing the prefix after three digits (cand_cap entries)
-    int32_t* cand_idx;    // their indices
+    int64_t* cand_idx;    // their indices
     unsigned int* cand_n;
     unsigned int cand_cap;
     int32_t* bounds;     // [m][chunks + 1] first entry of each 4096-chunk per row

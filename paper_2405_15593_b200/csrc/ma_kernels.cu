@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
     for (int t = tid; t < nent; t += NT) {
         const int r = t / kb;
         const int e = r * kbs + (t - r * kb);
-        s_owner[s_eidx[e]] = e;
+        atomicExch(&s_owner[s_eidx[e]], e);  // any entry of the coordinate may own it
     }
     __syncthreads();
     for (int t = tid; t < nent; t += NT) {

@@ -170,12 +170,14 @@ def test_oracle_not_imported_by_product():
 
 
 def test_global_mode_shapes(ma):
-    # blockwise = false (the reference default) runs on device for any d < 2^31
-    # with bucket | 4096 (ma_global.cu); d <= 8192 stays a single block
+    # blockwise = false (the reference default) runs on device for any d
+    # (int64 window indices) with bucket | 4096 (ma_global.cu); d <= 8192 stays
+    # a single block
     assert _validate(ma, dim=100_000, blockwise=0) == ma._capi.MA_OK
     assert _validate(ma, dim=5_000, blockwise=0, bucket=100) == ma._capi.MA_OK
     assert _validate(ma, dim=100_000, blockwise=0, bucket=100) == ma._capi.MA_ERR_UNSUPPORTED
-    assert _validate(ma, dim=3_000_000_000, blockwise=0) == ma._capi.MA_ERR_UNSUPPORTED
+    assert _validate(ma, dim=3_000_000_000, blockwise=0) == ma._capi.MA_OK
+    assert _validate(ma, dim=13_015_864_320, blockwise=0) == ma._capi.MA_OK
 
 
 def test_lossless_blockwise_is_supported(ma):
