@@ -52,6 +52,7 @@ struct Shape {
     int64_t code_bytes = 0;
     int64_t kb_stride = 0;
     bool global = false;     // global Top-K over d > kMaxBlock (ma_global.cu)
+    bool split = false;      // blockwise with B_q not dividing B_d: per-bucket re-quantization kernel
 };
 
 // HyperParams::validate (optim.cpp:7-21) — same checks, same order.
@@ -122,9 +123,15 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
         return fail(MA_ERR_UNSUPPORTED, "block > 8192 not supported on device");
     }
     s.nblocks_global = (dim + s.block - 1) / s.block;
-    if (s.nblocks_global > 1 && (s.block % hp.bucket != 0 || s.block % 2 != 0))
-        return fail(MA_ERR_UNSUPPORTED,
-                    "device path needs bucket | block and an even block when d > block");
+    if (!s.global && s.nblocks_global > 1 && (s.block % hp.bucket != 0 || s.block % 2 != 0)) {
+        // Buckets straddle Top-K blocks (quantize.cpp:142-162 buckets the whole
+        // vector): the step selects per block, then re-quantizes per bucket.
+        if (hp.bits != 4 || cfg->lossless_error)
+            return fail(MA_ERR_UNSUPPORTED, "bucket not dividing block: 4-bit quantized EF only on device");
+        if (b0 != 0 || (b1 >= 0 && b1 != s.nblocks_global))
+            return fail(MA_ERR_UNSUPPORTED, "bucket not dividing block: whole-vector handles only");
+        s.split = true;
+    }
     if (b1 < 0) b1 = s.nblocks_global;
     if (b0 < 0 || b0 >= b1 || b1 > s.nblocks_global)
         return fail(MA_ERR_INVALID_ARG, "shard block range out of bounds");
@@ -199,6 +206,9 @@ struct ma_handle {
     unsigned cand_cap = 0;
     int32_t* g_bounds = nullptr;
     double* d_dense = nullptr;  // lossless error feedback (fp64 residual, dim elements)
+    // bucket-split mode: second codes buffer (swapped every step) + selection bits
+    uint8_t* d_codes2 = nullptr;
+    uint32_t* d_split_sel = nullptr;
     // host counters (window.hpp:10-33)
     int64_t step = 0, head = 0, filled = 0;
     std::vector<int64_t> stamps;
@@ -272,6 +282,8 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_ovf);
     cudaFree(h->g_bounds);
     cudaFree(h->d_dense);
+    cudaFree(h->d_codes2);
+    cudaFree(h->d_split_sel);
     if (h->done_ev) cudaEventDestroy(h->done_ev);
     for (cudaEvent_t e : h->host_ev) cudaEventDestroy(e);
     if (h->host_stream) cudaStreamDestroy(h->host_stream);
@@ -371,6 +383,7 @@ void base_args(ma_handle* h, ma::StepArgs* a) {
     a->eps = h->cfg.hp.eps;
     a->force_exact = h->warp_exact ? 1 : 0;
     a->dense = h->d_dense;
+    a->split_sel = h->shape.split ? h->d_split_sel : nullptr;
     a->bits = static_cast<int32_t>(h->cfg.hp.bits);
 }
 
@@ -541,9 +554,21 @@ ma_status run_step(ma_handle* h, void* d_params, const void* d_grads, double lr,
     a.lr32 = static_cast<float>(lr);
     a.partials = report ? h->d_partials : nullptr;
     const CounterSnap snap = snap_counters(h);
+    const Shape& s = h->shape;
+    if (s.split) {
+        MA_CUDA(cudaMemsetAsync(h->d_split_sel, 0, size_t((s.dim + 31) / 32) * 4, st));
+        MA_CUDA(cudaMemsetAsync(h->d_codes2, 0, size_t(s.code_bytes + 3) / 4 * 4, st));
+    }
     push_and_weights(h, &a);
-    MA_CUDA_ROLLBACK(h, snap, launch(h, a, h->shape.b1 - h->shape.b0, st));
+    MA_CUDA_ROLLBACK(h, snap, launch(h, a, s.b1 - s.b0, st));
     ++h->launches;
+    if (s.split) {  // per-bucket re-quantization from the old codes into the second buffer
+        MA_CUDA_ROLLBACK(h, snap, ma::launch_requant_buckets(d_grads, h->cfg.grad_dtype, h->d_codes, h->d_codes2,
+                                                             h->d_meta, h->d_split_sel, s.dim, s.bucket,
+                                                             report ? h->d_partials + 3 : nullptr, st));
+        ++h->launches;
+        std::swap(h->d_codes, h->d_codes2);
+    }
     ma_status ms = mark_done(h, st);
     if (ms != MA_OK) return ms;
     if (report) return finish_report(h, st, report);
@@ -653,7 +678,7 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         h->fast = h->warp = h->tile = false;
         smem = ma::global_requant_smem(s.bucket);
     }
-    if (cfg->lossless_error || cfg->hp.bits != 4) {  // dense EF / other code widths: the generic kernel
+    if (cfg->lossless_error || cfg->hp.bits != 4 || s.split) {  // dense EF / other widths / split: generic kernel
         h->fast = h->warp = h->tile = false;
         h->variant = h->tail_variant;
     }
@@ -666,7 +691,11 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         if (e == cudaSuccess) e = cudaMalloc(p, bytes ? bytes : 16);
         if (e == cudaSuccess) e = cudaMemset(*p, 0, bytes ? bytes : 16);
     };
-    alloc(reinterpret_cast<void**>(&h->d_codes), size_t(s.code_bytes));
+    alloc(reinterpret_cast<void**>(&h->d_codes), size_t(s.code_bytes + 3) / 4 * 4);
+    if (s.split) {
+        alloc(reinterpret_cast<void**>(&h->d_codes2), size_t(s.code_bytes + 3) / 4 * 4);
+        alloc(reinterpret_cast<void**>(&h->d_split_sel), size_t((s.dim + 31) / 32) * 4);
+    }
     alloc(reinterpret_cast<void**>(&h->d_meta), size_t(s.nbuckets) * sizeof(double2));
     alloc(reinterpret_cast<void**>(&h->d_win_idx), went * (s.global ? sizeof(int64_t) : sizeof(int16_t)));
     if (s.global) {
@@ -786,7 +815,7 @@ ma_status ma_step_host(ma_handle* h, void* h_params, const void* h_grads, double
         if (st != MA_OK) return st;
     }
     cudaStream_t st = h->host_stream;
-    if (h->cfg.finite_mode == MA_FINITE_STRICT || report || s.global) {
+    if (h->cfg.finite_mode == MA_FINITE_STRICT || report || s.global || s.split) {
         // Whole-vector path: strict pre-scan / report need the full gradient;
         // global Top-K (ma_global.cu) selects over the whole vector at once.
         MA_CUDA(cudaMemcpyAsync(h->d_gstage, h_grads, size_t(s.dim) * gsz, cudaMemcpyHostToDevice, st));

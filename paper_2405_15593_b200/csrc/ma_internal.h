@@ -61,6 +61,11 @@ struct StepArgs {
     const void* rs_src[kMaxRanks];
     int32_t rs_n;
     float rs_scale;
+    // bucket-split mode (B_q does not divide B_d, quantize.cpp:142-162 buckets
+    // the whole vector): the generic kernel skips the re-quantization and
+    // marks its selection here (1 bit per element, zeroed before the step);
+    // launch_requant_buckets then re-quantizes bucket by bucket
+    uint32_t* split_sel;
 };
 
 // Global Top-K mode (ma_global.cu, blockwise = false with d > kMaxBlock).
@@ -152,6 +157,13 @@ cudaError_t launch_gather_window_theta(const int16_t* win_idx, const void* theta
 // gradients, fp64 for f64): the unfused reduce-scatter of ma_step_reduce.
 cudaError_t launch_reduce_grads(const void* const* srcs, int nsrc, float scale, int gdt, void* dst, int64_t e0,
                                 int64_t e1, cudaStream_t s);
+// Bucket-split mode: per bucket q of the whole vector, a = g + decode(old
+// codes, meta[q]) (codes_old), zero the elements marked in `sel`, exact
+// (lo, hi), 4-bit codes by the guarded quotient into codes_new (zeroed before),
+// meta[q] = (lo, hi); Σ e_new² added to *err2 when non-null (StepReport).
+cudaError_t launch_requant_buckets(const void* grads, int gdt, const uint8_t* codes_old, uint8_t* codes_new,
+                                   double2* meta, const uint32_t* sel, int64_t dim, int64_t bucket, double* err2,
+                                   cudaStream_t s);
 // lean kernel with the fused reduce (B_q = 64, k_b <= 64, bf16/bf16/bf16 or f32/f32/f32)
 bool lean_rs_ok(const StepArgs& a);
 cudaError_t launch_fill_synthetic(void* out, int dtype, int64_t n, uint64_t seed, uint64_t step,

@@ -21,6 +21,8 @@
 #include "ma_device.cuh"
 #include "ma_internal.h"
 
+#include <math_constants.h>
+
 namespace ma {
 namespace {
 
@@ -41,7 +43,7 @@ struct SmemLayout {
     }
     // code_w: bytes per staged code (1 for bits <= 8, 4 up to 24)
     __host__ __device__ SmemLayout(int nt, int ept, int block, int bucket, int m, int kbs, int code_w = 1) {
-        const size_t nbk = size_t((block + bucket - 1) / bucket);
+        const size_t nbk = size_t((block + bucket - 1) / bucket) + 1;  // +1: buckets may straddle blocks
         const size_t ent = size_t(m) * size_t(kbs);
         size_t off = 0;
         lo = take(off, nbk * 8);
@@ -172,8 +174,8 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
     const int64_t base = b * static_cast<int64_t>(block);
     const int len = static_cast<int>(min(static_cast<int64_t>(block), p.dim - base));
     const int kb = min(p.per_block_k, len);
-    const int nbk = (len + bucket - 1) / bucket;
-    const int64_t bk0 = base / bucket;
+    const int64_t bk0 = base / bucket;  // bucket of the block's first element (buckets may straddle blocks)
+    const int nbk = static_cast<int>((base + len - 1) / bucket - bk0 + 1);
     const bool want_report = p.partials != nullptr;
     const int bits = p.bits;
     const double max_code = static_cast<double>((1u << bits) - 1u);  // QuantParams::max_code
@@ -201,13 +203,19 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
         if (e < len) {
             double g0, g1 = 0.0;
             const bool two = e + 1 < len;
-            if (two)
+            const bool odd = (base & 1) != 0;  // odd B_d (bucket-split mode): pairs straddle words / code bytes
+            if (two && !odd) {
                 ld_pair(p.grads, p.g_dtype, base + e, g0, g1);
-            else
+            } else {
                 g0 = ld_val(p.grads, p.g_dtype, base + e);
-            const uint32_t byte = (p.dense || bits != 4) ? 0u : p.codes[(base + e) >> 1];
+                if (two) g1 = ld_val(p.grads, p.g_dtype, base + e + 1);
+            }
+            const uint32_t byte = (p.dense || bits != 4) ? 0u
+                                  : (odd ? (uint32_t(p.codes[(base + e) >> 1]) >> 4) |
+                                               (two ? uint32_t(p.codes[(base + e + 1) >> 1] & 15u) << 4 : 0u)
+                                         : p.codes[(base + e) >> 1]);
             const uint32_t c0 = bits == 4 ? (byte & 15u) : (p.dense ? 0u : read_code(p.codes, base + e, bits));
-            const int bA = e / bucket;
+            const int bA = static_cast<int>((base + e) / bucket - bk0);
             const double e0 = p.dense ? p.dense[base + e]
                                       : __dadd_rn(__dmul_rn(static_cast<double>(c0), s_lvl[bA]), s_lo[bA]);
             a[2 * j] = __dadd_rn(g0, e0);
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
                 rep[1] += a[2 * j] * a[2 * j];
             }
             if (two) {
-                const int bB = (e + 1) / bucket;
+                const int bB = static_cast<int>((base + e + 1) / bucket - bk0);
                 const uint32_t c1 = bits == 4 ? (byte >> 4) : (p.dense ? 0u : read_code(p.codes, base + e + 1, bits));
                 const double e1 = p.dense ? p.dense[base + e + 1]
                                           : __dadd_rn(__dmul_rn(static_cast<double>(c1), s_lvl[bB]), s_lo[bB]);
@@ -252,6 +260,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
         const int e = elem(i);
         if ((sel >> i) & 1u) {
             const int pos = rank[i];
+            if (p.split_sel) atomicOr(p.split_sel + ((base + e) >> 5), 1u << ((base + e) & 31));
             p.win_idx[wrow + pos] = static_cast<int16_t>(e);
             st_val(p.win_val, p.v_dtype, wrow + pos, a[i]);
             s_eidx[slot * kbs + pos] = static_cast<int16_t>(e);
@@ -282,7 +291,8 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
         }
     }
     // ---- P4: re-quantize the residual (quantize.cpp:15-24, 42-55, 142-162) ----
-    for (int bk = p.dense ? nbk : warp; bk < nbk; bk += NW) {
+    // (bucket-split mode: launch_requant_buckets does it over the whole vector)
+    for (int bk = (p.dense || p.split_sel) ? nbk : warp; bk < nbk; bk += NW) {
         const int s = bk * bucket;
         const int n = min(bucket, len - s);
         double lo = s_a[s], hi = s_a[s];
@@ -330,7 +340,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
 
     // ---- P5: pack (quantize.cpp:102-114): LSB-first bit stream; the block
     // starts on a byte boundary (block * bits % 8 == 0, checked at create) ----
-    if (!p.dense && bits != 4) {
+    if (!p.dense && !p.split_sel && bits != 4) {
         const int nbytes = (len * bits + 7) / 8;
         for (int jb = tid; jb < nbytes; jb += NT) {
             uint32_t byte = 0;
@@ -343,7 +353,7 @@ __global__ void __launch_bounds__(NT) microadam_step_kernel(const __grid_constan
             p.codes[(base * bits) / 8 + jb] = static_cast<uint8_t>(byte & 0xFFu);
         }
     }
-    for (int i = (p.dense || bits != 4) ? (len + 1) / 2 : tid; i < (len + 1) / 2; i += NT) {
+    for (int i = (p.dense || p.split_sel || bits != 4) ? (len + 1) / 2 : tid; i < (len + 1) / 2; i += NT) {
         const uint32_t lo4 = s_code[2 * i];
         const uint32_t hi4 = (2 * i + 1 < len) ? s_code[2 * i + 1] : 0u;
         p.codes[(base >> 1) + i] = static_cast<uint8_t>(lo4 | (hi4 << 4));
@@ -473,6 +483,69 @@ __global__ void gather_window_theta_kernel(const int16_t* win_idx, const void* t
     }
 }
 
+// Bucket-split re-quantization (quantize.cpp:15-24, 42-55, 102-114, 142-162
+// over the whole vector): one warp per bucket, two passes over its elements —
+// exact fp64 (lo, hi) of the residual, then the codes by the guarded
+// reciprocal / IEEE quotient of the generic kernel's P4. Nibbles go to the
+// zeroed codes_new with atomicOr (an odd bucket shares a byte with the next).
+__global__ void requant_buckets_kernel(const void* grads, int gdt, const uint8_t* codes_old, uint8_t* codes_new,
+                                       double2* meta, const uint32_t* sel, int64_t dim, int64_t bucket,
+                                       double* err2) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nq = (dim + bucket - 1) / bucket;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    double e2 = 0.0;
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += warps) {
+        const int64_t s0 = q * bucket, s1 = s0 + bucket < dim ? s0 + bucket : dim;
+        const double2 old = meta[q];
+        const double lvl0 = old.x == old.y ? 0.0 : __ddiv_rn(__dsub_rn(old.y, old.x), 15.0);
+        auto resid = [&](int64_t i) {
+            if ((sel[i >> 5] >> (i & 31)) & 1u) return 0.0;
+            const uint32_t c = (codes_old[i >> 1] >> ((i & 1) * 4)) & 15u;
+            return __dadd_rn(ld_val(grads, gdt, i), __dadd_rn(__dmul_rn(static_cast<double>(c), lvl0), old.x));
+        };
+        double lo = CUDART_INF, hi = -CUDART_INF;
+        for (int64_t i = s0 + lane; i < s1; i += 32) {
+            const double r = resid(i);
+            lo = r < lo ? r : lo;
+            hi = r > hi ? r : hi;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ol = __shfl_xor_sync(0xFFFFFFFFu, lo, off), oh = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+            lo = ol < lo ? ol : lo;
+            hi = oh > hi ? oh : hi;
+        }
+        const double level = lo == hi ? 0.0 : __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+        const bool fast = level >= 0x1p-1000;
+        const double rinv = fast ? __drcp_rn(level) : 0.0;
+        const double guard = fmax(1e-12, 15.0 * 0x1p-44);
+        for (int64_t i = s0 + lane; i < s1; i += 32) {
+            uint32_t c = 0;
+            if (level != 0.0) {
+                const double d = __dsub_rn(resid(i), lo);
+                const double t = __dadd_rn(__dmul_rn(d, rinv), 0.5);
+                double f = floor(t);
+                const double fr = __dsub_rn(t, f);
+                if (!fast || fr < guard || fr > 1.0 - guard) f = floor(__dadd_rn(__ddiv_rn(d, level), 0.5));
+                f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+                c = static_cast<uint32_t>(f);
+            }
+            if (c) atomicOr(reinterpret_cast<unsigned int*>(codes_new) + (i >> 3), c << (4 * (i & 7)));
+            if (err2) {
+                const double en = __dadd_rn(__dmul_rn(static_cast<double>(c), level), lo);
+                e2 += en * en;
+            }
+        }
+        if (lane == 0) meta[q] = make_double2(lo, hi);
+    }
+    if (err2) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) e2 += __shfl_xor_sync(0xFFFFFFFFu, e2, off);
+        if (lane == 0 && e2 != 0.0) atomicAdd(err2, e2);
+    }
+}
+
 __global__ void fill_synthetic_kernel(void* out, int dt, int64_t n, uint64_t seed, uint64_t step,
                                       int64_t offset, int levels) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
@@ -518,6 +591,16 @@ cudaError_t launch_step(const StepArgs& a, Variant v, int64_t nblocks, cudaStrea
         case 512: return launch_variant<512, 16>(a, nblocks, s);
         default: return cudaErrorInvalidConfiguration;
     }
+}
+
+cudaError_t launch_requant_buckets(const void* grads, int gdt, const uint8_t* codes_old, uint8_t* codes_new,
+                                   double2* meta, const uint32_t* sel, int64_t dim, int64_t bucket, double* err2,
+                                   cudaStream_t s) {
+    const int64_t nq = (dim + bucket - 1) / bucket;
+    const int64_t want = (nq + 7) / 8;
+    const unsigned grid = static_cast<unsigned>(want < 148 * 32 ? want : 148 * 32);
+    requant_buckets_kernel<<<grid, 256, 0, s>>>(grads, gdt, codes_old, codes_new, meta, sel, dim, bucket, err2);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_finite_scan(const void* g, int dtype, int64_t n, unsigned int* flag,

@@ -2156,9 +2156,19 @@ cudaError_t launch_ldt(const StepArgs& a, cudaStream_t s) {
     }
 }
 
+// Shared memory of the fused lean kernel: per warp the LLayout area plus the
+// block's staged window rows (indices + values).
+size_t lean_smem_bytes(const StepArgs& a) {
+    const int capl = a.per_block_k > kCap / 2 ? 16 : kLCapL;
+    const size_t vsz = a.v_dtype == F64 ? 8 : (a.v_dtype == F32 ? 4 : 2);
+    const size_t rows = align_up(size_t(a.m) * a.kb_stride * 2, 16) + align_up(size_t(a.m) * a.kb_stride * vsz, 16);
+    return size_t(kWarps) * (LLayout(8 * (a.bucket / 8), capl).total + rows);
+}
+
 bool lean_ok(const StepArgs& a) {
     if (a.partials || a.force_exact || (a.bucket != 32 && a.bucket != 64)) return false;
     if (a.per_block_k > kWideKb) return false;
+    if (lean_smem_bytes(a) > 227 * 1024) return false;  // huge windows: the exact warp kernel
     switch (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype)) {
 #define MA_CASE(G_, P_, V_) case dtype_key_w(G_, P_, V_): return true;
         MA_LEAN_DTYPES(MA_CASE)

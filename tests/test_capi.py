@@ -115,11 +115,19 @@ def test_k_exceeding_dim_rejected(ma):  # optim.cpp:23-26
     assert _validate(ma, dim=5, k=7) == ma._capi.MA_ERR_INVALID_ARG
 
 
-@pytest.mark.parametrize("kw", [dict(block=16384), dict(bucket=100),
-                                dict(block=4095), dict(window=300),
-                                dict(lossless_error=1, blockwise=0)])
+@pytest.mark.parametrize("kw", [dict(block=16384), dict(window=300),
+                                dict(lossless_error=1, blockwise=0),
+                                dict(bucket=100, bits=3), dict(bucket=100, lossless_error=1)])
 def test_unsupported_device_shapes_are_explicit(ma, kw):
     assert _validate(ma, dim=100_000, **kw) == ma._capi.MA_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("kw", [dict(bucket=100), dict(block=4095), dict(bucket=100_000),
+                                dict(block=1001, bucket=7)])
+def test_buckets_straddling_blocks_are_supported(ma, kw):
+    # quantize.cpp:142-162 buckets the whole vector: B_q need not divide B_d
+    # (the paper's B_q = 100,000): per-bucket re-quantization kernel
+    assert _validate(ma, dim=300_000, **kw) == ma._capi.MA_OK
 
 
 def test_single_block_allows_any_bucket(ma):
