@@ -87,7 +87,7 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
         if (dt < MA_F64 || dt > MA_BF16) return fail(MA_ERR_INVALID_ARG, "unknown dtype");
     if (cfg->finite_mode < MA_FINITE_FLAG || cfg->finite_mode > MA_FINITE_OFF)
         return fail(MA_ERR_INVALID_ARG, "unknown finite_mode");
-    if (hp.window > ma::kMaxWindow) return fail(MA_ERR_UNSUPPORTED, "window > 256 not supported on device");
+    if (hp.window > ma::kMaxWindow) return fail(MA_ERR_UNSUPPORTED, "window > 1024 not supported on device");
 
     Shape s;
     s.dim_global = dim;
@@ -118,6 +118,7 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
         if (cfg->lossless_error)
             return fail(MA_ERR_UNSUPPORTED, "global mode with lossless_error is not on the device path");
         if (hp.bits != 4) return fail(MA_ERR_UNSUPPORTED, "global mode on device implements bits = 4");
+        if (hp.window > ma::kMaxWindowGlobal) return fail(MA_ERR_UNSUPPORTED, "global mode on device: window <= 256");
         s.global = true;
     } else if (s.block > ma::kMaxBlock) {
         return fail(MA_ERR_UNSUPPORTED, "block > 8192 not supported on device");
@@ -645,9 +646,13 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
                                                  int(s.kb_stride), cfg->grad_dtype,
                                                  cfg->param_dtype, cfg->value_dtype);
     h->tail_variant = ma::pick_variant(blk_i);
-    size_t smem = ma::step_smem_bytes(h->tail_variant.nt, h->tail_variant.ept, blk_i,
-                                      int(s.bucket), int(cfg->hp.window), int(s.kb_stride), int(cfg->hp.bits));
-    if (fv.nt && !(force_generic && force_generic[0] == '1')) {
+    // the generic kernel's shared memory (needed for a partial tail block or when
+    // no other kernel runs this shape)
+    const size_t generic_smem = ma::step_smem_bytes(h->tail_variant.nt, h->tail_variant.ept, blk_i, int(s.bucket),
+                                                    int(cfg->hp.window), int(s.kb_stride), int(cfg->hp.bits));
+    size_t smem = 0;
+    const bool no_generic_env = !(force_generic && force_generic[0] == '1');
+    if (fv.nt && no_generic_env) {
         const size_t fs = ma::fast_smem_bytes(fv, blk_i, int(s.bucket), int(cfg->hp.window),
                                               int(s.kb_stride), cfg->grad_dtype, cfg->param_dtype,
                                               cfg->value_dtype);
@@ -662,11 +667,17 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         }
     }
     const char* force_cta = std::getenv("MA_FAST_CTA");  // A/B: the CTA-per-block fast kernel
-    if (h->fast && !(force_cta && force_cta[0] == '1') &&
-        ma::warp_path_ok(blk_i, int(s.bucket), int(s.per_block_k), int(cfg->hp.window),
-                         int(s.kb_stride), cfg->grad_dtype, cfg->param_dtype, cfg->value_dtype) &&
-        ma::warp_smem_bytes(int(s.bucket)) <= size_t(smem_max))
-        h->warp = true;
+    const bool warp_ok = !(force_cta && force_cta[0] == '1') &&
+                         ma::warp_path_ok(blk_i, int(s.bucket), int(s.per_block_k), int(cfg->hp.window),
+                                          int(s.kb_stride), cfg->grad_dtype, cfg->param_dtype, cfg->value_dtype) &&
+                         ma::warp_smem_bytes(int(s.bucket)) <= size_t(smem_max);
+    if (h->fast && warp_ok) h->warp = true;
+    // long windows (m * k_b beyond the CTA kernel's staging): the warp kernels alone
+    // (the exact one reads the rows from global memory; k_b <= 64)
+    if (!h->fast && no_generic_env && warp_ok && s.per_block_k <= 64) {
+        h->fast = h->warp = true;
+        h->variant = h->tail_variant;
+    }
     const char* warp_exact = std::getenv("MA_WARP_EXACT");
     h->warp_exact = warp_exact && warp_exact[0] == '1';
     // MA_TILE=1: the TMA-fed CTA-per-block kernel (ma_tile.cu) where it applies;
@@ -682,6 +693,8 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         h->fast = h->warp = h->tile = false;
         h->variant = h->tail_variant;
     }
+    const bool tail_block = !s.global && (s.dim % s.block) != 0 && s.b1 == s.nblocks_global;
+    if (!s.global && (!h->fast || tail_block)) smem = std::max(smem, generic_smem);
     if (smem > size_t(smem_max)) {
         delete h;
         return fail(MA_ERR_UNSUPPORTED, "block/window shape needs more shared memory than one SM has");

@@ -584,7 +584,7 @@ __device__ __forceinline__ void g_nnz_partial(const GlobalArgs& p, int64_t c, do
 __global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w, int filled) {
     extern __shared__ uint4 s_th4[];  // the chunk's θ, staged with 16-byte loads
     __shared__ double s_red[kThreads / 32];
-    __shared__ int s_j0[kMaxWindow], s_off[kMaxWindow + 1];
+    __shared__ int s_j0[kMaxWindowGlobal], s_off[kMaxWindowGlobal + 1];
     __shared__ int16_t s_ei[kStage];
     __shared__ double s_ev[kStage];
     __shared__ double s_z1[kStage], s_z2[kStage];  // per owner entry
@@ -665,7 +665,7 @@ __global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w,
 __global__ void g_stats_update_dense(GlobalArgs p, const __grid_constant__ GWeights w, int filled) {
     extern __shared__ double s_z[];  // [kChunk] z1, [kChunk] z2
     __shared__ double s_red[kThreads / 32];
-    __shared__ int s_j0[kMaxWindow], s_off[kMaxWindow + 1];
+    __shared__ int s_j0[kMaxWindowGlobal], s_off[kMaxWindowGlobal + 1];
     double* s_z1 = s_z;
     double* s_z2 = s_z + kChunk;
     const unsigned novf = *p.ovf_n;

@@ -7,7 +7,8 @@
 
 namespace ma {
 
-constexpr int kMaxWindow = 256;  // m supported on device (params carry m weights)
+constexpr int kMaxWindow = 1024;  // m supported on device (params carry m weights; 10-bit rows in dup lists)
+constexpr int kMaxWindowGlobal = 256;  // m of the global Top-K mode (its stats kernel stages m row bounds)
 constexpr int kMaxRanks = 8;     // gradient sources of a fused reduce-scatter step
 constexpr int kMaxBlock = 8192;  // B_d supported on device (fp64 block held on chip)
 constexpr int kCandCap = 128;    // exact-rank stage capacity of the Top-K select
@@ -103,8 +104,8 @@ cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s);  // G2 + row of
 cudaError_t g_launch_emit(const GlobalArgs& a, cudaStream_t s);
 cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s);
 struct GWeights {
-    double w1[kMaxWindow];
-    double w2[kMaxWindow];
+    double w1[kMaxWindowGlobal];
+    double w2[kMaxWindowGlobal];
 };
 cudaError_t g_launch_stats_update(const GlobalArgs& a, const GWeights& w, int filled, cudaStream_t s);
 

@@ -178,6 +178,16 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total) {
     return incl - v;
 }
 
+// Ordered duplicate-list entry: block-relative index (12 bits) | physical
+// window row (10 bits) | position in the row (10 bits): m <= 1023, k_b <= 1023.
+__device__ __forceinline__ int dup_pack(int idx, int r, int pos) {
+    return static_cast<int>((static_cast<uint32_t>(idx) << 20) | (static_cast<uint32_t>(r) << 10) |
+                            static_cast<uint32_t>(pos));
+}
+__device__ __forceinline__ int dup_idx(int x) { return static_cast<int>(static_cast<uint32_t>(x) >> 20); }
+__device__ __forceinline__ int dup_row(int x) { return (x >> 10) & 0x3FF; }
+__device__ __forceinline__ int dup_pos(int x) { return x & 0x3FF; }
+
 // Rank correction among candidates whose high words tie (compress.cpp:43-48:
 // full |a| key first, then the lower index). Out of line: rare.
 __device__ __noinline__ int tie_rank_w(const double* cval, const int16_t* cidx, int ncand, int t) {
@@ -373,7 +383,7 @@ __device__ __noinline__ double dup_stats(const StepArgs* pp, unsigned char* ws, 
     for (int q = lane; q < n; q += 32) {
         int idx;
         if (listed) {
-            idx = dupl[q] >> 16;
+            idx = dup_idx(dupl[q]);
         } else {
             const int r = row_of(q, kb, inv_kb);
             idx = gwi[r * kbs + (q - r * kb)];
@@ -385,9 +395,9 @@ __device__ __noinline__ double dup_stats(const StepArgs* pp, unsigned char* ws, 
         if (listed) {
             for (int q2 = 0; q2 < ndup; ++q2) {  // list order = physical slot order (window.cpp:32-39)
                 const int x = dupl[q2];
-                if ((x >> 16) != idx) continue;
-                const int rr = (x >> 8) & 0xFF;
-                const double v = ld_t<KT::VDT>(gwv, rr * kbs + (x & 0xFF));
+                if (dup_idx(x) != idx) continue;
+                const int rr = dup_row(x);
+                const double v = ld_t<KT::VDT>(gwv, rr * kbs + dup_pos(x));
                 z1 = __dadd_rn(z1, __dmul_rn(p.w1[rr], v));
                 z2 = __dadd_rn(z2, __dmul_rn(p.w2[rr], __dmul_rn(v, v)));
             }
@@ -735,7 +745,7 @@ __global__ void __launch_bounds__(32 * kWarps, 8) microadam_step_warp(const __gr
             }
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
             const int q = ndup + __popc(bal & lanemask_lt());
-            if (dup && q < qcap) dupl[q] = (idx[k] << 16) | (r[k] << 8) | (t - r[k] * kb);
+            if (dup && q < qcap) dupl[q] = dup_pack(idx[k], r[k], t - r[k] * kb);
             ndup += __popc(bal);
         }
 #pragma unroll
@@ -1210,6 +1220,18 @@ __device__ __forceinline__ void unique_update_smem(const StepArgs& p, int64_t ba
     }
 }
 
+// Stage the block's window rows in shared memory when they fit next to the
+// LLayout area without dropping below 8 resident CTAs per SM.
+__host__ __device__ __forceinline__ bool lean_stage_rows(int m, int kbs, int vsz) {
+    return size_t(m) * size_t(kbs) * size_t(2 + vsz) <= 2048;
+}
+__device__ __forceinline__ int16_t* gwi_of(const StepArgs& p, int64_t b, int /*vsz*/) {
+    return p.win_idx + b * p.m * static_cast<int64_t>(p.kb_stride);
+}
+__device__ __forceinline__ unsigned char* gwv_of(const StepArgs& p, int64_t b, int vsz) {
+    return static_cast<unsigned char*>(p.win_val) + b * p.m * static_cast<int64_t>(p.kb_stride) * vsz;
+}
+
 // The block's m window rows -> shared memory by two 1-D bulk copies completing
 // on one mbarrier (lane 0; phase 0 is awaited before the rows are used).
 __device__ __forceinline__ void stage_rows(uint64_t* bar, void* s_idx, const void* g_idx, void* s_val, const void* g_val,
@@ -1271,7 +1293,7 @@ __device__ __noinline__ bool dup_chunks(const StepArgs* pp, unsigned char* ws, i
         for (int c0 = 0; c0 < ndup; c0 += 32) {
             bool has = c0 + lane < ndup;
             const int x = has ? dupl[c0 + lane] : 0;
-            const int idx = x >> 16, r = (x >> 8) & 0xFF, pos = x & 0xFF;
+            const int idx = dup_idx(x), r = dup_row(x), pos = dup_pos(x);
             int id = 0;
             if (has) {
                 id = s_dpref[idx >> 5] + __popc(s_dup[idx >> 5] & ((1u << (idx & 31)) - 1u)) - id0;
@@ -1365,11 +1387,14 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     const LLayout L(BUCKET, KT::CAPL);
     // PH & 2: the block's m window rows (indices, then values) are staged after
     // the warp's LLayout area by one bulk copy issued in the prologue
-    const uint32_t wrow_i = (PH & 2) ? static_cast<uint32_t>(align_up(size_t(p.m) * p.kb_stride * 2, 16)) : 0u;
-    const uint32_t wrow_v = (PH & 2) ? static_cast<uint32_t>(align_up(size_t(p.m) * p.kb_stride * vsz, 16)) : 0u;
+    // (only while that keeps 8 CTAs per SM: lean_stage_rows; else the rows are
+    // read from global memory through the same pointers)
+    const bool stage = (PH & 2) && lean_stage_rows(p.m, p.kb_stride, vsz);
+    const uint32_t wrow_i = stage ? static_cast<uint32_t>(align_up(size_t(p.m) * p.kb_stride * 2, 16)) : 0u;
+    const uint32_t wrow_v = stage ? static_cast<uint32_t>(align_up(size_t(p.m) * p.kb_stride * vsz, 16)) : 0u;
     unsigned char* ws = smem + warp * (L.total + wrow_i + wrow_v);
-    int16_t* s_widx = reinterpret_cast<int16_t*>(ws + L.total);
-    unsigned char* s_wval = ws + L.total + wrow_i;
+    int16_t* s_widx = stage ? reinterpret_cast<int16_t*>(ws + L.total) : gwi_of(p, b, vsz);
+    unsigned char* s_wval = stage ? ws + L.total + wrow_i : gwv_of(p, b, vsz);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(ws + L.misc + 48);
     double2* s_ll = reinterpret_cast<double2*>(ws + L.ll);
     float4* s_llf = reinterpret_cast<float4*>(ws + L.llf);
@@ -1432,7 +1457,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         if constexpr (!KT::RS) prefetch_l2_keep(static_cast<const unsigned char*>(p.grads) + base * gsz, kBlk * gsz);
         prefetch_l2_keep(p.codes + base / 2, kBlk / 2);
         prefetch_l2(p.meta + base / BUCKET, NBK * 16);
-        if constexpr (PH & 2) stage_rows(s_bar, s_widx, gwi, s_wval, gwv, m * kbs * 2, m * kbs * vsz);
+        if ((PH & 2) && stage) stage_rows(s_bar, s_widx, gwi, s_wval, gwv, m * kbs * 2, m * kbs * vsz);
     }
     const uint32_t tstate = __ldg(p.thresh + b);
     const uint32_t T = tstate & 0xFFFFu;
@@ -1740,7 +1765,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     }
     __syncwarp();
     const int64_t row0 = static_cast<int64_t>(slot) * kbs;
-    if constexpr (PH & 2) {
+    if ((PH & 2) && stage) {
         // the staged copy of the ring (issued in the prologue) must land before
         // this step's row overwrites slot `slot` in it
         while (!mbar_try_wait(s_bar, 0)) {
@@ -1755,7 +1780,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                 const int pos = s_wpref[e >> 5] + __popc(s_sel[e >> 5] & ((1u << (e & 31)) - 1u));
                 gwi[row0 + pos] = static_cast<int16_t>(e);
                 st_t<KT::VDT>(gwv, row0 + pos, s_cval[q]);
-                if constexpr ((PH & 2) != 0) {
+                if ((PH & 2) && stage) {
                     s_widx[row0 + pos] = static_cast<int16_t>(e);
                     st_t<KT::VDT>(s_wval, row0 + pos, s_cval[q]);
                 }
@@ -1775,7 +1800,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                 gwi[row0 + pos] = static_cast<int16_t>(e);
                 const double av = recompute_a<KT>(p, base, s_ll, e);
                 st_t<KT::VDT>(gwv, row0 + pos, av);
-                if constexpr ((PH & 2) != 0) {
+                if ((PH & 2) && stage) {
                     s_widx[row0 + pos] = static_cast<int16_t>(e);
                     st_t<KT::VDT>(s_wval, row0 + pos, av);
                 }
@@ -1950,7 +1975,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
     }  // PH & 1
     if constexpr (PH == 2) {
         if (lane == 0) {
-            stage_rows(s_bar, s_widx, gwi, s_wval, gwv, m * kbs * 2, m * kbs * vsz);
+            if (stage) stage_rows(s_bar, s_widx, gwi, s_wval, gwv, m * kbs * 2, m * kbs * vsz);
             prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
         }
 #pragma unroll
@@ -1959,7 +1984,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
             s_dup[lane * 4 + k] = 0;
         }
         __syncwarp();
-        while (!mbar_try_wait(s_bar, 0)) {
+        while (stage && !mbar_try_wait(s_bar, 0)) {
         }
     }
     if constexpr (PH & 2) {
@@ -2051,7 +2076,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, dup);
                 if (bal) {
                     const int qd = ndup + __popc(bal & lanemask_lt());
-                    if (dup && qd < dup_max) dupl[qd] = (idx << 16) | (rr << 8) | pp;
+                    if (dup && qd < dup_max) dupl[qd] = dup_pack(idx, rr, pp);
                     ndup += __popc(bal);
                 }
                 if (act && !dup) unique_update_smem<KT>(p, base, thb, gwv, s_wval, s_th + (t0 - c0) * tsz, e, rr, idx);
@@ -2072,7 +2097,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         // peer sums the terms in lane order (window.cpp:32-39) and updates θ.
         const bool has = lane < ndup;
         const int x = has ? dupl[lane] : 0;
-        const int idx = x >> 16, r = (x >> 8) & 0xFF, pos = x & 0xFF;
+        const int idx = dup_idx(x), r = dup_row(x), pos = dup_pos(x);
         double t1 = 0.0, t2 = 0.0;
         if (has) {
             const double v = ld_t<KT::VDT>(s_wval, r * kbs + pos);
@@ -2114,9 +2139,9 @@ template <class KT, int PH = 3>
 cudaError_t launch_kl(const StepArgs& a, cudaStream_t s) {
     constexpr int vsz = KT::VDT == F64 ? 8 : (KT::VDT == F32 ? 4 : 2);
     // per warp: the LLayout area + (PH & 2) the staged window rows (indices, values)
-    const size_t rows = (PH & 2) ? align_up(size_t(a.m) * a.kb_stride * 2, 16) +
-                                       align_up(size_t(a.m) * a.kb_stride * vsz, 16)
-                                 : 0;
+    const size_t rows = ((PH & 2) && lean_stage_rows(a.m, a.kb_stride, vsz))
+                            ? align_up(size_t(a.m) * a.kb_stride * 2, 16) + align_up(size_t(a.m) * a.kb_stride * vsz, 16)
+                            : 0;
     const size_t smem = size_t(kWarps) * (LLayout(KT::BUCKET, KT::CAPL).total + rows);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     auto k = microadam_step_lean<KT, PH>;
@@ -2161,8 +2186,10 @@ cudaError_t launch_ldt(const StepArgs& a, cudaStream_t s) {
 size_t lean_smem_bytes(const StepArgs& a) {
     const int capl = a.per_block_k > kCap / 2 ? 16 : kLCapL;
     const size_t vsz = a.v_dtype == F64 ? 8 : (a.v_dtype == F32 ? 4 : 2);
-    const size_t rows = align_up(size_t(a.m) * a.kb_stride * 2, 16) + align_up(size_t(a.m) * a.kb_stride * vsz, 16);
-    return size_t(kWarps) * (LLayout(8 * (a.bucket / 8), capl).total + rows);
+    const size_t rows = lean_stage_rows(a.m, a.kb_stride, int(vsz))
+                            ? align_up(size_t(a.m) * a.kb_stride * 2, 16) + align_up(size_t(a.m) * a.kb_stride * vsz, 16)
+                            : 0;
+    return size_t(kWarps) * (LLayout(a.bucket, capl).total + rows);
 }
 
 bool lean_ok(const StepArgs& a) {

@@ -115,11 +115,17 @@ def test_k_exceeding_dim_rejected(ma):  # optim.cpp:23-26
     assert _validate(ma, dim=5, k=7) == ma._capi.MA_ERR_INVALID_ARG
 
 
-@pytest.mark.parametrize("kw", [dict(block=16384), dict(window=300),
+@pytest.mark.parametrize("kw", [dict(block=16384), dict(window=1025), dict(window=300, blockwise=0),
                                 dict(lossless_error=1, blockwise=0),
                                 dict(bucket=100, bits=3), dict(bucket=100, lossless_error=1)])
 def test_unsupported_device_shapes_are_explicit(ma, kw):
     assert _validate(ma, dim=100_000, **kw) == ma._capi.MA_ERR_UNSUPPORTED
+
+
+def test_long_windows(ma):
+    # HyperParams::validate only needs window >= 1 (optim.cpp:13): m up to 1024 on device
+    assert _validate(ma, dim=100_000, window=300) == ma._capi.MA_OK
+    assert _validate(ma, dim=100_000, window=1024) == ma._capi.MA_OK
 
 
 @pytest.mark.parametrize("kw", [dict(bucket=100), dict(block=4095), dict(bucket=100_000),

@@ -49,3 +49,21 @@ def test_straddling_buckets_host_path():
         opt.step(g)
         orc.step(g, hp["lr"])
     assert np.array_equal(opt.params().view(np.uint64), orc.state().params.view(np.uint64))
+
+
+@pytest.mark.parametrize("d,density,m,steps,dt", [
+    (4096 * 4 + 100, 0.002, 300, 320, "bf16"),  # lean kernel (+ generic tail), rows > 255 in the dup lists
+    (4096 * 4, 0.01, 600, 610, "f32"),          # staged rows do not fit: the exact warp kernel alone
+    (4096 * 4, 0.0005, 1024, 1030, "bf16"),     # the longest window on device
+])
+def test_long_windows_vs_composed_oracle(d, density, m, steps, dt):
+    # HyperParams::validate only needs window >= 1 (optim.cpp:13); the rows are
+    # summed in physical slot order (window.cpp:32-39) with weights β^(t - stamp)
+    hp = dict(lr=1e-2, window=m, density=density)
+    run_parity(d, hp, gdt=dt, pdt=dt, vdt="bf16", steps=steps, check_every=97)
+
+
+def test_long_window_fp64_vs_unmodified_reference():
+    hp = dict(lr=1e-2, window=270, density=0.004)
+    run_parity(4096 * 3, hp, gdt="f64", pdt="f64", vdt="f64", steps=280, check_every=70,
+               check_reference=oracle.reference_available())

@@ -63,7 +63,7 @@ def make_engine(kernel, *args, **kw):
 
 def run_parity(d, hp, *, gdt="f32", pdt="f32", vdt="bf16", steps=12, levels=False, seed=42,
                grad_fn=None, check_reference=None, lr=None, report_every=0, kernel="fast",
-               theta0=None):
+               theta0=None, check_every=1):
     torch = _torch()
     oracle.build()
     lr = hp.get("lr", 1e-3) if lr is None else lr
@@ -84,6 +84,10 @@ def run_parity(d, hp, *, gdt="f32", pdt="f32", vdt="bf16", steps=12, levels=Fals
         want_rep = bool(report_every) and s % report_every == 0
         rep = eng.step(params, _dev(g, gdt), lr, report=want_rep)
         orep = orc.step(g, lr)
+        if ref is not None:
+            ref.step(g)
+        if s % check_every and s != steps:
+            continue
         torch.cuda.synchronize()
         eng.synchronize()
         so = orc.state()
@@ -109,7 +113,6 @@ def run_parity(d, hp, *, gdt="f32", pdt="f32", vdt="bf16", steps=12, levels=Fals
                 assert abs(a - b) <= 1e-12 * max(abs(b), 1e-300), (k, a, b)
             assert rep.update_nnz == orep["update_nnz"]
         if ref is not None:
-            ref.step(g)
             sr = ref.state()
             assert np.array_equal(_bits(sr.params), _bits(got)), f"θ vs unmodified reference @ {s}"
             assert np.array_equal(sr.codes, eb.codes)
