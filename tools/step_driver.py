@@ -2,7 +2,7 @@
 """Minimal driver for profiling: N MicroAdam steps on one GPU.
 
     python tools/step_driver.py --dim 110000000 --dtype bf16 --steps 3
-Used under ncu (profiles/README.md); never a bench number.
+Used under ncu (tools/r2_ncu_kern.sh, tools/r2_evidence.sh); never a bench number.
 """
 import argparse
 import os
