@@ -12,7 +12,7 @@ LIB      := $(LIBDIR)/libmicroadam_cuda.so
 NVFLAGS  := -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
             -fmad=false -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
             -Xcompiler -fvisibility=hidden -Xptxas -warn-spills $(EXTRA)
-SRCS     := $(CSRC)/ma_nccl.cpp $(CSRC)/ma_kernels.cu $(CSRC)/ma_fast.cu $(CSRC)/ma_warp.cu $(CSRC)/ma_tile.cu $(CSRC)/ma_global.cu $(CSRC)/ma_capi.cu $(CSRC)/microadam_b200.cpp
+SRCS     := $(CSRC)/ma_nccl.cpp $(CSRC)/ma_bigblock.cu $(CSRC)/ma_kernels.cu $(CSRC)/ma_fast.cu $(CSRC)/ma_warp.cu $(CSRC)/ma_tile.cu $(CSRC)/ma_global.cu $(CSRC)/ma_capi.cu $(CSRC)/microadam_b200.cpp
 HDRS     := include/microadam_cuda.h include/ma_synth.h $(CSRC)/ma_internal.h $(CSRC)/ma_device.cuh $(CSRC)/ma_async.cuh $(CSRC)/microadam_b200.hpp
 
 .PHONY: all lib oracle clean sass
@@ -28,7 +28,7 @@ $(LIBDIR)/%.o: $(CSRC)/%.cpp $(HDRS)
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(NVFLAGS) -Iinclude -x cu -dc -o $@ $<
 
-$(LIB): $(LIBDIR)/ma_nccl.o $(LIBDIR)/ma_kernels.o $(LIBDIR)/ma_fast.o $(LIBDIR)/ma_warp.o $(LIBDIR)/ma_tile.o $(LIBDIR)/ma_global.o $(LIBDIR)/ma_capi.o $(LIBDIR)/microadam_b200.o
+$(LIB): $(LIBDIR)/ma_nccl.o $(LIBDIR)/ma_bigblock.o $(LIBDIR)/ma_kernels.o $(LIBDIR)/ma_fast.o $(LIBDIR)/ma_warp.o $(LIBDIR)/ma_tile.o $(LIBDIR)/ma_global.o $(LIBDIR)/ma_capi.o $(LIBDIR)/microadam_b200.o
 	$(NVCC) $(NVFLAGS) -shared -o $@ $^ -ldl
 
 oracle:

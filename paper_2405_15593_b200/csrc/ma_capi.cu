@@ -53,6 +53,7 @@ struct Shape {
     int64_t kb_stride = 0;
     bool global = false;     // global Top-K over d > kMaxBlock (ma_global.cu)
     bool split = false;      // blockwise with B_q not dividing B_d: per-bucket re-quantization kernel
+    bool big = false;        // blockwise B_d in (8192, 32767]: ma_bigblock.cu (+ split re-quantization)
 };
 
 // HyperParams::validate (optim.cpp:7-21) — same checks, same order.
@@ -121,10 +122,13 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
         if (hp.window > ma::kMaxWindowGlobal) return fail(MA_ERR_UNSUPPORTED, "global mode on device: window <= 256");
         s.global = true;
     } else if (s.block > ma::kMaxBlock) {
-        return fail(MA_ERR_UNSUPPORTED, "block > 8192 not supported on device");
+        if (s.block > ma::kMaxBlockBig) return fail(MA_ERR_UNSUPPORTED, "block > 32767 not supported on device");
+        if (hp.bits != 4 || cfg->lossless_error)
+            return fail(MA_ERR_UNSUPPORTED, "block > 8192: 4-bit quantized EF only on device");
+        s.big = true;  // the big-block kernel; EF re-quantized per bucket (split mode)
     }
     s.nblocks_global = (dim + s.block - 1) / s.block;
-    if (!s.global && s.nblocks_global > 1 && (s.block % hp.bucket != 0 || s.block % 2 != 0)) {
+    if (!s.global && (s.big || (s.nblocks_global > 1 && (s.block % hp.bucket != 0 || s.block % 2 != 0)))) {
         // Buckets straddle Top-K blocks (quantize.cpp:142-162 buckets the whole
         // vector): the step selects per block, then re-quantizes per bucket.
         if (hp.bits != 4 || cfg->lossless_error)
@@ -391,6 +395,7 @@ void base_args(ma_handle* h, ma::StepArgs* a) {
 // Fast path: the persistent kernel takes the range's full blocks and the
 // generic kernel the shard's partial tail block (if it is in the range).
 cudaError_t launch(ma_handle* h, ma::StepArgs& a, int64_t nblocks, cudaStream_t st) {
+    if (h->shape.big) return ma::launch_step_big(a, nblocks, st);
     if (!h->fast) return ma::launch_step(a, h->variant, nblocks, st);
     const Shape& s = h->shape;
     const int64_t nb_shard = s.b1 - s.b0;
@@ -694,7 +699,12 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         h->variant = h->tail_variant;
     }
     const bool tail_block = !s.global && (s.dim % s.block) != 0 && s.b1 == s.nblocks_global;
-    if (!s.global && (!h->fast || tail_block)) smem = std::max(smem, generic_smem);
+    if (s.big) {
+        h->fast = h->warp = h->tile = false;
+        smem = ma::big_block_smem_bytes(int(s.block), int(cfg->hp.window), int(s.kb_stride));
+    } else if (!s.global && (!h->fast || tail_block)) {
+        smem = std::max(smem, generic_smem);
+    }
     if (smem > size_t(smem_max)) {
         delete h;
         return fail(MA_ERR_UNSUPPORTED, "block/window shape needs more shared memory than one SM has");

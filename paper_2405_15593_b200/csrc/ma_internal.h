@@ -10,7 +10,8 @@ namespace ma {
 constexpr int kMaxWindow = 1024;  // m supported on device (params carry m weights; 10-bit rows in dup lists)
 constexpr int kMaxWindowGlobal = 256;  // m of the global Top-K mode (its stats kernel stages m row bounds)
 constexpr int kMaxRanks = 8;     // gradient sources of a fused reduce-scatter step
-constexpr int kMaxBlock = 8192;  // B_d supported on device (fp64 block held on chip)
+constexpr int kMaxBlock = 8192;  // B_d of the register-resident kernels (fp64 block held on chip)
+constexpr int kMaxBlockBig = 32767;  // B_d of the big-block kernel (the reference's BlockLayout limit)
 constexpr int kCandCap = 128;    // exact-rank stage capacity of the Top-K select
 constexpr int kReportFields = 5; // Σg², Σa², Σr², Σe_new², nnz per block
 
@@ -158,6 +159,11 @@ cudaError_t launch_gather_window_theta(const int16_t* win_idx, const void* theta
 // gradients, fp64 for f64): the unfused reduce-scatter of ma_step_reduce.
 cudaError_t launch_reduce_grads(const void* const* srcs, int nsrc, float scale, int gdt, void* dst, int64_t e0,
                                 int64_t e1, cudaStream_t s);
+// Blockwise Top-K blocks in (kMaxBlock, kMaxBlockBig] (ma_bigblock.cu): one CTA
+// per block, a recomputed from global memory, EF re-quantized afterwards by
+// launch_requant_buckets (the handle runs in bucket-split mode).
+size_t big_block_smem_bytes(int block, int m, int kb_stride);
+cudaError_t launch_step_big(const StepArgs& a, int64_t nblocks, cudaStream_t s);
 // Bucket-split mode: per bucket q of the whole vector, a = g + decode(old
 // codes, meta[q]) (codes_old), zero the elements marked in `sel`, exact
 // (lo, hi), 4-bit codes by the guarded quotient into codes_new (zeroed before),

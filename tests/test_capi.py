@@ -115,11 +115,20 @@ def test_k_exceeding_dim_rejected(ma):  # optim.cpp:23-26
     assert _validate(ma, dim=5, k=7) == ma._capi.MA_ERR_INVALID_ARG
 
 
-@pytest.mark.parametrize("kw", [dict(block=16384), dict(window=1025), dict(window=300, blockwise=0),
+@pytest.mark.parametrize("kw", [dict(block=16384, bits=3), dict(window=1025),
+                                dict(window=300, blockwise=0),
                                 dict(lossless_error=1, blockwise=0),
                                 dict(bucket=100, bits=3), dict(bucket=100, lossless_error=1)])
 def test_unsupported_device_shapes_are_explicit(ma, kw):
     assert _validate(ma, dim=100_000, **kw) == ma._capi.MA_ERR_UNSUPPORTED
+
+
+def test_big_blocks(ma):
+    # BlockLayout allows B_d up to 32767 (compress.hpp:23): the big-block kernel
+    assert _validate(ma, dim=100_000, block=16384) == ma._capi.MA_OK
+    assert _validate(ma, dim=100_000, block=32767) == ma._capi.MA_OK
+    # beyond the reference's limit: its BlockLayout throws (std::invalid_argument)
+    assert _validate(ma, dim=100_000, block=40000) == ma._capi.MA_ERR_INVALID_ARG
 
 
 def test_long_windows(ma):

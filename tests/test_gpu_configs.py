@@ -67,3 +67,27 @@ def test_long_window_fp64_vs_unmodified_reference():
     hp = dict(lr=1e-2, window=270, density=0.004)
     run_parity(4096 * 3, hp, gdt="f64", pdt="f64", vdt="f64", steps=280, check_every=70,
                check_reference=oracle.reference_available())
+
+
+@pytest.mark.parametrize("d,block,bucket,density", [
+    (3 * 16384 + 1000, 16384, 64, 0.01),     # B_d > 8192: the big-block kernel
+    (2 * 32767 + 5, 32767, 100, 0.005),      # the reference's largest block (compress.hpp:23)
+    (20_000, 10_000, 4096, 0.02),
+    (9_000, 32767, 64, 0.01),                 # one block of d > 8192 (block = min(B_d, d))
+])
+def test_big_blocks_fp64_vs_unmodified_reference(d, block, bucket, density):
+    hp = dict(lr=1e-2, window=4, block=block, bucket=bucket, density=density)
+    run_parity(d, hp, gdt="f64", pdt="f64", vdt="f64", steps=7,
+               check_reference=oracle.reference_available(), report_every=3)
+
+
+def test_big_blocks_bf16_vs_composed_oracle():
+    hp = dict(lr=1e-2, window=5, block=20_000, bucket=64, density=0.01)
+    run_parity(70_000, hp, gdt="bf16", pdt="bf16", vdt="bf16", steps=9)
+
+
+def test_big_block_tie_heavy():
+    # 16-level gradients: many exact |a| ties at the k_b-th key (lowest indices win)
+    hp = dict(lr=1e-2, window=3, block=12_288, bucket=64, density=0.01)
+    run_parity(3 * 12_288, hp, gdt="f64", pdt="f64", vdt="f64", steps=5, levels=True,
+               check_reference=oracle.reference_available())
