@@ -116,8 +116,6 @@ ma_status resolve_shape(const ma_config* cfg, int64_t dim, int64_t b0, int64_t b
             return fail(MA_ERR_UNSUPPORTED, "global mode on device needs bucket | 4096");
         if (b0 != 0 || (b1 >= 0 && b1 != 1))
             return fail(MA_ERR_UNSUPPORTED, "global mode cannot be block-sharded");
-        if (cfg->lossless_error)
-            return fail(MA_ERR_UNSUPPORTED, "global mode with lossless_error is not on the device path");
         if (hp.bits != 4) return fail(MA_ERR_UNSUPPORTED, "global mode on device implements bits = 4");
         if (hp.window > ma::kMaxWindowGlobal) return fail(MA_ERR_UNSUPPORTED, "global mode on device: window <= 256");
         s.global = true;
@@ -493,6 +491,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.bounds = h->g_bounds;
     g.partials = report ? h->d_partials : nullptr;
     g.flag = h->d_flag;
+    g.dense = h->d_dense;
     g.dim = s.dim;
     g.nbuckets = s.nbuckets;
     g.bucket = s.bucket;

@@ -43,6 +43,7 @@ __device__ __forceinline__ int64_t global_chunks_d(int64_t dim) { return (dim + 
 constexpr int kStage = 1024;  // window entries per chunk staged in shared memory by g_stats_update
 
 __device__ __forceinline__ double g_a(const GlobalArgs& p, int64_t i) {
+    if (p.dense) return __dadd_rn(ld_val(p.grads, p.g_dtype, i), p.dense[i]);  // lossless (optim.cpp:166-168)
     const int64_t q = i >> p.bucket_shift;  // bucket | 4096: a power of two
     const double lo = p.meta[q].x;
     const uint32_t byte = p.codes[i >> 1];
@@ -57,7 +58,7 @@ __device__ __forceinline__ double g_a(const GlobalArgs& p, int64_t i) {
 // the bucket holds the whole group.
 __device__ __forceinline__ int g_a8(const GlobalArgs& p, int64_t i0, double (&a)[8]) {
     const int nv = p.dim - i0 >= 8 ? 8 : static_cast<int>(p.dim - i0);
-    const bool vec = nv == 8 && p.bucket_shift >= 3 &&
+    const bool vec = nv == 8 && p.bucket_shift >= 3 && !p.dense &&
                      (reinterpret_cast<uintptr_t>(p.grads) & 15u) == 0;
     if (!vec) {
 #pragma unroll
@@ -377,6 +378,41 @@ __global__ void g_requant8(GlobalArgs p) {
             for (int b = 0; 2 * b < nv; ++b) p.codes[(i0 >> 1) + b] = static_cast<uint8_t>(word >> (8 * b));
         }
         if ((threadIdx.x & (LPB - 1)) == 0) p.meta[i0 >> p.bucket_shift] = make_double2(lo, hi);
+    }
+    if (p.partials) {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        for (int f = 0; f < 4; ++f) {
+            for (int off = 16; off > 0; off >>= 1) rep[f] += __shfl_xor_sync(0xFFFFFFFFu, rep[f], off);
+            if (lane == 0) s_red[w][f] = rep[f];
+        }
+        __syncthreads();
+        if (threadIdx.x < 4) {
+            double sum = 0.0;
+            for (int w2 = 0; w2 < kThreads / 32; ++w2) sum += s_red[w2][threadIdx.x];
+            p.partials[int64_t(blockIdx.x) * kReportFields + threadIdx.x] = sum;
+        }
+    }
+}
+
+// Lossless error feedback (optim.cpp:172-173): the residual of the selection
+// is the new error, kept dense in fp64 (read before it is overwritten: each
+// thread owns its elements); report sums.
+__global__ void g_residual_dense(GlobalArgs p) {
+    __shared__ double s_red[kThreads / 32][4];
+    const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+    double rep[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = threadIdx.x; j < kChunk; j += kThreads) {
+        const int64_t i = c0 + j;
+        if (i >= p.dim) break;
+        const double g = ld_val(p.grads, p.g_dtype, i);
+        const double a = __dadd_rn(g, p.dense[i]);
+        const bool s = (p.selbits[i / kPer] >> (i % kPer)) & 1u;
+        const double r = s ? 0.0 : a;
+        p.dense[i] = r;
+        rep[0] += g * g;
+        rep[1] += a * a;
+        rep[2] += r * r;
+        rep[3] += r * r;
     }
     if (p.partials) {
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -878,6 +914,10 @@ cudaError_t g_launch_emit(const GlobalArgs& a, cudaStream_t s) {
 
 cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s) {
     const unsigned nch = static_cast<unsigned>(global_chunks(a.dim));
+    if (a.dense) {
+        g_residual_dense<<<nch, kThreads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     switch (a.bucket) {  // the register path for 8 <= B_q <= 256
         case 8: g_requant8<1><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
         case 16: g_requant8<2><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();

@@ -93,6 +93,7 @@ struct GlobalArgs {
     unsigned int* ovf_n;
     double* partials;    // nullable: [chunks][kReportFields]
     unsigned int* flag;
+    double* dense;       // lossless error feedback (optim.cpp:149-152): the fp64 residual, else null
     int64_t dim, nbuckets, bucket, k, row_stride;
     int32_t slot, g_dtype, p_dtype, v_dtype, check_finite, bucket_shift;
     double eps, lr, scale1, scale2;
@@ -103,7 +104,7 @@ cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s);
 cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s);  // G1: six digit passes, no host sync
 cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s);  // G2 + row offsets / ties per chunk
 cudaError_t g_launch_emit(const GlobalArgs& a, cudaStream_t s);
-cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s);
+cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s);  // lossless: the residual itself
 struct GWeights {
     double w1[kMaxWindowGlobal];
     double w2[kMaxWindowGlobal];

@@ -117,7 +117,6 @@ def test_k_exceeding_dim_rejected(ma):  # optim.cpp:23-26
 
 @pytest.mark.parametrize("kw", [dict(block=16384, bits=3), dict(window=1025),
                                 dict(window=300, blockwise=0),
-                                dict(lossless_error=1, blockwise=0),
                                 dict(bucket=100, bits=3), dict(bucket=100, lossless_error=1)])
 def test_unsupported_device_shapes_are_explicit(ma, kw):
     assert _validate(ma, dim=100_000, **kw) == ma._capi.MA_ERR_UNSUPPORTED
@@ -206,6 +205,7 @@ def test_global_mode_shapes(ma):
 def test_lossless_blockwise_is_supported(ma):
     # MicroAdamOptimizer(..., lossless_error = true) (optim.hpp:103-104): dense fp64 EF
     assert _validate(ma, dim=100_000, lossless_error=1) == ma._capi.MA_OK
+    assert _validate(ma, dim=100_000, lossless_error=1, blockwise=0) == ma._capi.MA_OK
 
 
 def test_code_widths(ma):

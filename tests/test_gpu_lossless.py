@@ -20,13 +20,15 @@ def _bits(x):
     return np.asarray(x, np.float64).view(np.uint64)
 
 
-@pytest.mark.parametrize("d,hp", [(30_011, dict(lr=1e-2, window=4)),
-                                  (4096 * 3, dict(lr=1e-2, window=3, block=1024, density=0.02))])
-def test_lossless_matches_reference_and_conserves(d, hp):
+@pytest.mark.parametrize("d,hp,blockwise", [(30_011, dict(lr=1e-2, window=4), True),
+                                            (4096 * 3, dict(lr=1e-2, window=3, block=1024, density=0.02), True),
+                                            (30_011, dict(lr=1e-2, window=4), False),   # global Top-K (ma_global.cu)
+                                            (50_000, dict(lr=1e-2, window=3, k=333), False)])
+def test_lossless_matches_reference_and_conserves(d, hp, blockwise):
     from paper_2405_15593_b200 import MicroAdamOptimizer
     th0 = oracle.synth(1, 0, 0, d)
-    opt = MicroAdamOptimizer(th0, hp, blockwise=True, lossless_error=True)
-    ref = oracle.Reference(th0, hp, lossless=True)
+    opt = MicroAdamOptimizer(th0, hp, blockwise=blockwise, lossless_error=True)
+    ref = oracle.Reference(th0, hp, blockwise=blockwise, lossless=True)
     assert opt.lossless()
     e_prev = np.zeros(d)
     for s in range(1, 8):
