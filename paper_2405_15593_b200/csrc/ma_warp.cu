@@ -1908,27 +1908,24 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
 #pragma unroll
                     for (int k = 0; k < Raw16<KT::GDT>::N; ++k) slot[k] = raw.v[k];
                     const double2 q = s_ll[e0 / BUCKET];
-                    do {
+                    const uint64_t cw64 = (static_cast<uint64_t>(cw.y) << 32) | cw.x;
+                    do {  // branch-free body: every flagged element takes the same path
                         const int i = __ffs(fl) - 1;
                         fl &= fl - 1;
                         const bool s = (sel16 >> i) & 1u;
-                        const uint32_t c = ((i < 8 ? cw.x : cw.y) >> (4 * (i & 7))) & 15u;
+                        const uint32_t c = static_cast<uint32_t>(cw64 >> (4 * i)) & 15u;
                         const float g = KT::GDT == BF16
                                             ? __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(slot)[i]) << 16)
                                             : reinterpret_cast<const float*>(slot)[i];
                         const float r32 = s ? 0.0f : __fadd_rn(g, __fmaf_rn(static_cast<float>(c), f.y, f.x));
                         const uint32_t N = (__float_as_uint(__fmaf_rn(r32, k2, c2)) >> 15) & 0xFFu;
-                        if (N == 0u || N > 31u) {
-                            bad = true;
-                        } else if (N == 1u || N == 31u) {
-                            const double rx = s ? 0.0
-                                                : __dadd_rn(static_cast<double>(g),
-                                                            __dadd_rn(__dmul_rn(static_cast<double>(c), q.y), q.x));
-                            if (N == 1u) lmin = rx < lmin ? rx : lmin;
-                            else lmax = rx > lmax ? rx : lmax;
-                        } else if ((N & 1u) == 0u) {
-                            bnd |= 1u << i;
-                        }
+                        const double rx = s ? 0.0
+                                            : __dadd_rn(static_cast<double>(g),
+                                                        __dadd_rn(__dmul_rn(static_cast<double>(c), q.y), q.x));
+                        bad |= N == 0u || N > 31u;
+                        lmin = (N == 1u && rx < lmin) ? rx : lmin;
+                        lmax = (N == 31u && rx > lmax) ? rx : lmax;
+                        bnd |= static_cast<uint32_t>((N & 1u) == 0u && N - 1u < 31u) << i;
                     } while (fl);
                 }
             }
