@@ -313,15 +313,19 @@ def run_ours(args):
     vdt = "bf16"
     tdt = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[dt]
     hp = ma.HyperParams(density=args.density, window=args.window, lr=1e-3)
-    gather = world > 1 and args.mode == "allgather"
+    # BENCH_FORCE_COMM=1: run the N>1 collective code path with a 1-rank NCCL
+    # communicator (a smoke test of the multi-GPU layout on a one-GPU box)
+    force_comm = os.environ.get("BENCH_FORCE_COMM") == "1"
+    gather = (world > 1 or force_comm) and args.mode == "allgather"
     sparse = args.mode == "sparse"
     levels = 2 if args.grad_stream == "heavy" else 0
     comm = None
-    if world > 1 and args.mode in ("allgather", "sparse"):
+    if (world > 1 or force_comm) and args.mode in ("allgather", "sparse"):
         # the library's own NCCL communicator (ma_comm_init); torch.distributed only
         # carries the 128-byte unique id and the timing reductions
         uid = [ma.Comm.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
         comm = ma.Comm(uid[0], world, rank, local)
     if sparse:  # strong scaling, window-row exchange: a whole-vector handle per rank
         if d % hp.block:
