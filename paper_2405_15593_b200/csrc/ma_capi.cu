@@ -205,6 +205,9 @@ struct ma_handle {
     unsigned long long* g_selstate = nullptr;
     uint64_t* g_cand = nullptr;
     int64_t* g_cand_idx = nullptr;
+    uint64_t* g_seg_key = nullptr;
+    int64_t* g_seg_idx = nullptr;
+    unsigned* g_seg_n = nullptr;
     int32_t* g_ovf = nullptr;
     unsigned cand_cap = 0;
     int32_t* g_bounds = nullptr;
@@ -282,6 +285,9 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_selstate);
     cudaFree(h->g_cand);
     cudaFree(h->g_cand_idx);
+    cudaFree(h->g_seg_key);
+    cudaFree(h->g_seg_idx);
+    cudaFree(h->g_seg_n);
     cudaFree(h->g_ovf);
     cudaFree(h->g_bounds);
     cudaFree(h->d_dense);
@@ -484,6 +490,9 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.sel_state = h->g_selstate;
     g.cand = h->g_cand;
     g.cand_idx = h->g_cand_idx;
+    g.seg_key = h->g_seg_key;
+    g.seg_idx = h->g_seg_idx;
+    g.seg_n = h->g_seg_n;
     g.cand_n = reinterpret_cast<unsigned int*>(h->g_selstate + 3);
     g.cand_cap = h->cand_cap;
     g.ovf_list = h->g_ovf;
@@ -514,7 +523,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     // one-CTA scan — the step never waits for the host.
     MA_CUDA(ma::g_launch_select(g, st));
     MA_CUDA(ma::g_launch_count(g, st));
-    h->launches += 14;
+    h->launches += 28;  // levels, select (init, bracket x4, 6 x (hist, hist_cand, pick), next), count x3
     MA_CUDA(ma::g_launch_emit(g, st));
     MA_CUDA(ma::g_launch_requant(g, st));
     ma::GWeights w;
@@ -523,7 +532,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
         w.w2[r] = a.w2[r];
     }
     MA_CUDA(ma::g_launch_stats_update(g, w, int(h->filled), st));
-    h->launches += 5;
+    h->launches += ma::global_fused_emit(g) ? 4 : 5;
     ma_status ms = mark_done(h, st);
     if (ms != MA_OK) return ms;
     if (report) {
@@ -727,13 +736,18 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         alloc(reinterpret_cast<void**>(&h->g_hist), 2048 * sizeof(uint32_t));
         alloc(reinterpret_cast<void**>(&h->g_cnt), size_t(nch) * sizeof(int2));
         alloc(reinterpret_cast<void**>(&h->g_selinfo), size_t(nch) * sizeof(int2));
-        alloc(reinterpret_cast<void**>(&h->g_selstate), 8 * sizeof(unsigned long long));
+        alloc(reinterpret_cast<void**>(&h->g_selstate), 16 * sizeof(unsigned long long));
         alloc(reinterpret_cast<void**>(&h->g_ovf), size_t(nch) * sizeof(int32_t));
         // MA_GLOBAL_CAND_CAP (tests): a small capacity forces the overflow path
         const char* cc = std::getenv("MA_GLOBAL_CAND_CAP");
-        h->cand_cap = cc ? static_cast<unsigned>(std::strtoul(cc, nullptr, 10)) : kGlobalCandCap;
+        // default: d / 128 keys (the carried bracket's collection), 1M..32M
+        const int64_t cap_d = std::min<int64_t>(int64_t(32) << 20, std::max<int64_t>(kGlobalCandCap, s.dim / 128));
+        h->cand_cap = cc ? static_cast<unsigned>(std::strtoul(cc, nullptr, 10)) : static_cast<unsigned>(cap_d);
         alloc(reinterpret_cast<void**>(&h->g_cand), size_t(h->cand_cap) * sizeof(uint64_t));
         alloc(reinterpret_cast<void**>(&h->g_cand_idx), size_t(h->cand_cap) * sizeof(int64_t));
+        alloc(reinterpret_cast<void**>(&h->g_seg_key), size_t(h->cand_cap) * sizeof(uint64_t));
+        alloc(reinterpret_cast<void**>(&h->g_seg_idx), size_t(h->cand_cap) * sizeof(int64_t));
+        alloc(reinterpret_cast<void**>(&h->g_seg_n), size_t(ma::kBracketCtas) * sizeof(unsigned));
         alloc(reinterpret_cast<void**>(&h->g_bounds), size_t(cfg->hp.window) * size_t(nch + 1) * sizeof(int32_t));
     }
     alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));

@@ -121,6 +121,7 @@ __global__ void g_hist(GlobalArgs p, int shift, int nbins, int collect, int from
     uint32_t* h = PRIV ? s_hw + (threadIdx.x >> 5) * 2048 : s_h1;
     const uint64_t prefix = p.sel_state[0], pmask = p.sel_state[1];
     if (from_cand && *p.cand_n <= p.cand_cap) return;  // g_hist_cand covers this digit
+    if (p.sel_state[8]) return;                          // the bracket holds K*: g_hist_cand
     for (int i = threadIdx.x; i < (PRIV ? 2048 * (kThreads / 32) : nbins); i += blockDim.x) (PRIV ? s_hw : s_h1)[i] = 0;
     __syncthreads();
     bool bad = false;
@@ -298,32 +299,95 @@ __global__ void g_emit(GlobalArgs p) {
 // t of a chunk holds the 8-groups t and t + 256, a bucket spans B_q / 8
 // consecutive threads (shuffle min/max), codes packed 8 to a word. Same
 // arithmetic and IEEE-quotient guard as g_requant.
-template <int LPB>
+//
+// EMIT: G3 fused in (one pass over d fewer): the selection of the chunk is
+// decided here from the keys (> K*, or == K* among the first ties of the
+// chunk's quota, index order: the 8-groups of h = 0 then h = 1, thread order
+// within) and written to the window row at the chunk's row offset, exactly as
+// g_emit writes it.
+template <int LPB, bool EMIT>
 __global__ void g_requant8(GlobalArgs p) {
     __shared__ double s_red[kThreads / 32][4];
+    __shared__ int s_tmp[33];
     const int64_t c0 = int64_t(blockIdx.x) * kChunk;
     double rep[4] = {0.0, 0.0, 0.0, 0.0};
+    int2 cs = make_int2(0, 0);
+    uint64_t kstar = 0;
+    if constexpr (EMIT) {
+        cs = p.sel_info[blockIdx.x];  // (row offset, ties to take in this chunk)
+        kstar = p.sel_state[0];
+    }
+    int64_t* ri = p.win_idx + int64_t(p.slot) * p.row_stride;
 #pragma unroll 1
     for (int h = 0; h < kChunk / (8 * kThreads); ++h) {
         const int64_t i0 = c0 + 8 * (int64_t(threadIdx.x) + int64_t(h) * kThreads);
         double a[8];
         const int nv = i0 < p.dim ? g_a8(p, i0, a) : 0;
-        const uint32_t sw = nv ? (p.selbits[i0 / kPer] >> (i0 % kPer)) & 0xFFu : 0u;
-        double lo = CUDART_INF, hi = -CUDART_INF;
+        uint32_t sw;
+        if constexpr (EMIT) {
+            // high words first: keys whose high word is below K*'s are below it
+            const uint32_t ks_hi = static_cast<uint32_t>(kstar >> 32);
+            uint32_t maybe = 0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const double r = ((sw >> e) & 1u) ? 0.0 : a[e];
-            if (p.partials && e < nv) {
+            for (int e = 0; e < 8; ++e)
+                maybe |= static_cast<uint32_t>((static_cast<uint32_t>(__double2hiint(a[e])) & 0x7FFFFFFFu) >= ks_hi) << e;
+            if (nv < 8) maybe &= (1u << nv) - 1u;
+            uint32_t gtm = 0, eqm = 0;
+            if (maybe) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint64_t k = key_of(a[e]);
+                    gtm |= static_cast<uint32_t>(k > kstar) << e;
+                    eqm |= static_cast<uint32_t>(k == kstar) << e;
+                }
+                gtm &= maybe;
+                eqm &= maybe;
+            }
+            int te;
+            int tie_before = cta_excl_scan(__popc(eqm), s_tmp, te);
+            sw = gtm;
+            for (uint32_t m = eqm; m; m &= m - 1) {
+                if (tie_before < cs.y) sw |= m & (0u - m);
+                ++tie_before;
+            }
+            int tot;
+            int pos = cs.x + cta_excl_scan(__popc(sw), s_tmp, tot);
+            for (uint32_t m = sw; m; m &= m - 1) {
+                const int e = __ffs(m) - 1;
+                ri[pos] = i0 + e;
+                st_val(p.win_val, p.v_dtype, int64_t(p.slot) * p.row_stride + pos, a[e]);
+                ++pos;
+            }
+            cs.x += tot;
+            cs.y -= te;
+        } else {
+            sw = nv ? (p.selbits[i0 / kPer] >> (i0 % kPer)) & 0xFFu : 0u;
+        }
+        double lo = CUDART_INF, hi = -CUDART_INF;
+        if (p.partials) {
+            for (int e = 0; e < nv; ++e) {
+                const double r = ((sw >> e) & 1u) ? 0.0 : a[e];
                 const double g = ld_val(p.grads, p.g_dtype, i0 + e);
                 rep[0] += g * g;
                 rep[1] += a[e] * a[e];
                 rep[2] += r * r;
             }
-            a[e] = r;
-            if (e < nv) {
-                lo = r < lo ? r : lo;
-                hi = r > hi ? r : hi;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a[e] = ((sw >> e) & 1u) ? 0.0 : a[e];
+        if (nv == 8) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                lo = a[e] < lo ? a[e] : lo;
+                hi = a[e] > hi ? a[e] : hi;
             }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (e < nv) {
+                    lo = a[e] < lo ? a[e] : lo;
+                    hi = a[e] > hi ? a[e] : hi;
+                }
         }
 #pragma unroll
         for (int off = 1; off < LPB; off <<= 1) {
@@ -735,16 +799,21 @@ __global__ void g_stats_update_dense(GlobalArgs p, const __grid_constant__ GWeig
 }
 
 // One digit's histogram over the collected candidate keys.
-__global__ void g_hist_cand(GlobalArgs p, int shift, int nbins) {
+__global__ void g_hist_cand(GlobalArgs p, int shift, int nbins, int early) {
     __shared__ uint32_t h[2048];
     const unsigned n = *p.cand_n;
-    if (n > p.cand_cap) return;  // overflowed: the full pass runs instead
+    if (n > p.cand_cap) return;           // overflowed: the full pass runs instead
+    if (early && !p.sel_state[8]) return;  // leading digits: only over a bracket's keys
     const uint64_t prefix = p.sel_state[0], pmask = p.sel_state[1];
     for (int i = threadIdx.x; i < nbins; i += blockDim.x) h[i] = 0;
     __syncthreads();
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint64_t k = p.cand[i];
-        if ((k & pmask) == prefix) atomicAdd(&h[(k >> shift) & uint64_t(nbins - 1)], 1u);
+    const unsigned n32 = (n + 31u) & ~31u;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += gridDim.x * blockDim.x) {
+        const uint64_t k = i < n ? p.cand[i] : 0;
+        const int bin = i < n && (k & pmask) == prefix ? static_cast<int>((k >> shift) & uint64_t(nbins - 1)) : -1;
+        // one atomic per distinct bin per warp (a bracket's keys crowd a few bins)
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+        if (bin >= 0 && (__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&h[bin], __popc(peers));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < nbins; i += blockDim.x)
@@ -766,6 +835,194 @@ __global__ void g_count_cand(GlobalArgs p) {
     }
 }
 
+// Carried bracket (one pass over d instead of three): K* moves little from
+// step to step, so the keys in [Kc - W, Kc + W] around the previous step's K*
+// are collected with their indices and the keys above the bracket only
+// counted (per chunk, and in total). When above < k <= above + collected and
+// the buffer held them all, the k-th largest key lies in the bracket and the
+// six digit picks run over the collected keys alone (g_hist_cand): the same
+// exact K* and tie count as the full passes. Otherwise the step falls back to
+// the full digit passes (g_bracket_check resets the state). The bracket only
+// decides which kernels do the work, never the result.
+// sel_state: [5] Kc, [6] W (0: no bracket yet), [7] keys above, [8] bracket ok
+__global__ void __launch_bounds__(256) g_bracket(GlobalArgs p) {
+    __shared__ unsigned long long s_above;
+    __shared__ unsigned s_cn;  // keys collected into this CTA's segment
+    const uint64_t kc = p.sel_state[5], w = p.sel_state[6];
+    if (w == 0) return;
+    // the bracket widened to whole 2^32 steps of the key: the tests below read
+    // only the high word of |a| (keys >= lo32 << 32 and <= hi32 << 32 | ~0u)
+    const uint32_t lo32 = static_cast<uint32_t>((kc > w ? kc - w : 0) >> 32);
+    const uint32_t hi32 = static_cast<uint32_t>((kc + w) >> 32), span = hi32 - lo32;
+    // keys go to this CTA's segment of seg_key / seg_idx, slots taken with a
+    // shared-memory counter (a global one serialises every warp in L2)
+    const unsigned seg_cap = p.cand_cap / gridDim.x;
+    uint64_t* sk = p.seg_key + size_t(blockIdx.x) * seg_cap;
+    int64_t* si = p.seg_idx + size_t(blockIdx.x) * seg_cap;
+    if (threadIdx.x == 0) {
+        s_above = 0;
+        s_cn = 0;
+    }
+    __syncthreads();
+    uint32_t mx = 0;  // largest high word: inf / NaN (check_finite in topk_global)
+    unsigned above_t = 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t ngroups = (p.dim + 7) / 8;
+    for (int64_t gi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; gi < ngroups;
+         gi += int64_t(gridDim.x) * blockDim.x) {
+        double a[8];
+        const int nv = g_a8(p, gi * 8, a);
+        const unsigned act = __activemask();
+        uint32_t inm = 0;
+        int above = 0;
+        if (nv == 8) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t h = static_cast<uint32_t>(__double2hiint(a[e])) & 0x7FFFFFFFu;
+                mx = max(mx, h);
+                above += h > hi32;
+                inm |= static_cast<uint32_t>(h - lo32 <= span) << e;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t h = static_cast<uint32_t>(__double2hiint(a[e])) & 0x7FFFFFFFu;
+                if (e < nv) {
+                    mx = max(mx, h);
+                    above += h > hi32;
+                    inm |= static_cast<uint32_t>(h - lo32 <= span) << e;
+                }
+            }
+        }
+        // keys above the bracket are above K*: count them per chunk (a warp's
+        // 32 groups lie in one 4096-chunk)
+        const int wsum = __reduce_add_sync(act, above);
+        if (wsum && lane == __ffs(act) - 1) atomicAdd(&p.cnt[(gi * 8) / kChunk].x, wsum);
+        above_t += above;
+        if (!__any_sync(act, inm != 0)) continue;
+        const int n = __popc(inm);
+        int incl = n;  // warp-aggregated slot reservation
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(act, incl, off);
+            if (lane >= off && ((act >> (lane - off)) & 1u)) incl += t;
+        }
+        const int last = 31 - __clz(act);
+        const int tot = __shfl_sync(act, incl, last);
+        unsigned base = 0;
+        if (lane == last) base = atomicAdd(&s_cn, static_cast<unsigned>(tot));
+        base = __shfl_sync(act, base, last) + static_cast<unsigned>(incl - n);
+        while (inm) {
+            const int e = __ffs(inm) - 1;
+            inm &= inm - 1;
+            if (base < seg_cap) {
+                sk[base] = key_of(a[e]);
+                si[base] = gi * 8 + e;
+            }
+            ++base;
+        }
+    }
+    if (mx >= 0x7FF00000u && p.check_finite) atomicOr(p.flag, 1u);
+    above_t = __reduce_add_sync(0xFFFFFFFFu, above_t);
+    if (lane == 0 && above_t) atomicAdd(&s_above, static_cast<unsigned long long>(above_t));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_above) atomicAdd(&p.sel_state[7], s_above);
+        p.seg_n[blockIdx.x] = s_cn;
+    }
+}
+
+// Does the bracket hold the k-th largest key? Yes: the digit picks start over
+// the collected keys with k - above entries to place (g_bracket_compact packs
+// the segments into cand first). No: full passes, from a clean state
+// (g_cnt_reset clears the per-chunk counts the bracket made).
+// sel_state[10]: the bracket's width exponent (adapted here and in g_bracket_next)
+__global__ void g_bracket_check(GlobalArgs p) {
+    __shared__ unsigned long long s_n;
+    __shared__ int s_ovf;
+    if (threadIdx.x == 0) {
+        s_n = 0;
+        s_ovf = 0;
+    }
+    __syncthreads();
+    const unsigned long long w = p.sel_state[6], above = p.sel_state[7];
+    const unsigned seg_cap = p.cand_cap / kBracketCtas;
+    unsigned long long n_t = 0;
+    int ovf_t = 0;
+    if (w != 0)
+        for (int b = threadIdx.x; b < kBracketCtas; b += blockDim.x) {
+            const unsigned c = p.seg_n[b];
+            n_t += c;
+            ovf_t |= c > seg_cap;
+        }
+    atomicAdd(&s_n, n_t);
+    if (ovf_t) s_ovf = 1;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const unsigned long long n = s_n;
+    const bool ok = w != 0 && !s_ovf && above < static_cast<unsigned long long>(p.k) &&
+                    above + n >= static_cast<unsigned long long>(p.k);
+    p.sel_state[8] = ok;
+    if (ok) {
+        p.sel_state[2] = static_cast<unsigned long long>(p.k) - above;
+        *p.cand_n = static_cast<unsigned>(n);
+    } else {
+        *p.cand_n = 0;
+        p.sel_state[2] = static_cast<unsigned long long>(p.k);
+        if (w != 0) {  // narrower if a segment overflowed, else wider
+            long long e = static_cast<long long>(p.sel_state[10]) + (s_ovf ? -1 : 1);
+            p.sel_state[10] = static_cast<unsigned long long>(e < 0 ? 0 : (e > 12 ? 12 : e));
+        }
+    }
+}
+
+// Segments -> cand[0, n) (order is irrelevant to the digit picks and counts).
+__global__ void g_bracket_compact(GlobalArgs p) {
+    __shared__ unsigned s_off;
+    if (!p.sel_state[8]) return;
+    const unsigned b = blockIdx.x, seg_cap = p.cand_cap / kBracketCtas;
+    unsigned off_t = 0;
+    for (unsigned j = threadIdx.x; j < b; j += blockDim.x) off_t += p.seg_n[j];
+    off_t = __reduce_add_sync(0xFFFFFFFFu, off_t);
+    if (threadIdx.x == 0) s_off = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_off, off_t);
+    __syncthreads();
+    const unsigned n = p.seg_n[b], off = s_off;
+    for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
+        p.cand[off + i] = p.seg_key[size_t(b) * seg_cap + i];
+        p.cand_idx[off + i] = p.seg_idx[size_t(b) * seg_cap + i];
+    }
+}
+
+__global__ void g_cnt_reset(GlobalArgs p, int64_t nch) {
+    if (p.sel_state[8] || p.sel_state[6] == 0) return;
+    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < nch; c += int64_t(gridDim.x) * blockDim.x)
+        p.cnt[c] = make_int2(0, 0);
+}
+
+// The next step's bracket. K* drifts steadily while the error feedback builds
+// up (the keys grow as unselected coordinates accumulate), so the centre is
+// this step's K* plus the last change (linear extrapolation in key space) and
+// the half-width is that change (at least 2^40, ~2^-12 of a binade) times
+// 2^(e-1), e adapted: +1 after a miss, -1 after an overflow or a crowded
+// buffer. sel_state[9]: this step's K* for the next extrapolation.
+__global__ void g_bracket_next(GlobalArgs p) {
+    const unsigned long long kstar = p.sel_state[0], prev = p.sel_state[9];
+    const bool first = p.sel_state[6] == 0;
+    long long e = first ? 2 : static_cast<long long>(p.sel_state[10]);
+    if (!first && p.sel_state[8] && *p.cand_n > p.cand_cap / 4 && e > 0) --e;
+    const long long delta = first ? 0 : static_cast<long long>(kstar) - static_cast<long long>(prev);
+    const unsigned long long ad = static_cast<unsigned long long>(delta < 0 ? -delta : delta);
+    const unsigned long long base = ad > (1ull << 40) ? ad : (1ull << 40);
+    unsigned long long w = e >= 1 ? base << (e - 1) : base >> 1;
+    if (w > (1ull << 58)) w = 1ull << 58;
+    const long long c = static_cast<long long>(kstar) + delta;
+    p.sel_state[5] = static_cast<unsigned long long>(c < 0 ? 0 : c);
+    p.sel_state[6] = w;
+    p.sel_state[9] = kstar;
+    p.sel_state[10] = static_cast<unsigned long long>(e);
+}
+
 // Radix select state: no key prefix yet, k entries still to place.
 __global__ void g_sel_init(GlobalArgs p, int64_t nch) {
     for (int i = threadIdx.x; i < 2048; i += blockDim.x) p.hist[i] = 0;
@@ -775,6 +1032,8 @@ __global__ void g_sel_init(GlobalArgs p, int64_t nch) {
         p.sel_state[1] = 0;
         p.sel_state[2] = static_cast<unsigned long long>(p.k);
         *p.cand_n = 0;
+        p.sel_state[7] = 0;
+        p.sel_state[8] = 0;
     }
 }
 
@@ -845,6 +1104,23 @@ __global__ void g_alloc(GlobalArgs p, int64_t nch) {
     }
 }
 
+// G3 fused into the register re-quantization (8 <= B_q <= 256, 4-bit EF)
+bool g_fused_emit(const GlobalArgs& a) {
+    static const bool on = [] {  // A/B: MA_GLOBAL_FUSED_EMIT=0 keeps g_emit separate
+        const char* e = std::getenv("MA_GLOBAL_FUSED_EMIT");
+        return !(e && e[0] == '0');
+    }();
+    return on && !a.dense && a.bucket >= 8 && a.bucket <= 256 && (a.bucket & (a.bucket - 1)) == 0;
+}
+
+bool g_use_bracket() {
+    static const bool on = [] {  // A/B and tests: MA_GLOBAL_BRACKET=0 runs the full digit passes
+        const char* e = std::getenv("MA_GLOBAL_BRACKET");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 unsigned grid_for(int64_t n, int per) {
     const int64_t want = (n + per - 1) / per;
     return static_cast<unsigned>(want < 148 * 16 ? (want > 0 ? want : 1) : 148 * 16);
@@ -853,6 +1129,7 @@ unsigned grid_for(int64_t n, int per) {
 }  // namespace
 
 int64_t global_chunks(int64_t dim) { return (dim + kChunk - 1) / kChunk; }
+bool global_fused_emit(const GlobalArgs& a) { return g_fused_emit(a); }
 
 size_t global_requant_smem(int64_t bucket) {
     // residuals + per-bucket lo, level, 1/level
@@ -883,9 +1160,18 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
     const bool g_hist_priv =
         !g_hist_match &&
         cudaFuncSetAttribute(g_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPrivSmem)) == cudaSuccess;
-    g_sel_init<<<1, 1024, 0, s>>>(a, global_chunks(a.dim));
+    const int64_t nch = global_chunks(a.dim);
+    g_sel_init<<<1, 1024, 0, s>>>(a, nch);
+    if (g_use_bracket()) {
+        g_bracket<<<kBracketCtas, 256, 0, s>>>(a);
+        g_bracket_check<<<1, 256, 0, s>>>(a);
+        g_bracket_compact<<<kBracketCtas, 256, 0, s>>>(a);
+        g_cnt_reset<<<static_cast<unsigned>(nch < 148 * 64 ? (nch + 255) / 256 + 1 : 148 * 4), 256, 0, s>>>(a, nch);
+    }
     // digit 3 collects the keys sharing the 22-bit prefix; digits 4-6 read
-    // them (a few thousand keys) instead of re-decoding d elements
+    // them (a few thousand keys) instead of re-decoding d elements. With a
+    // bracket holding K*, every digit reads the bracket's keys (the full
+    // passes return at once).
     for (int pass = 0; pass < 6; ++pass) {
         const int nbins = pass == 5 ? 256 : 2048;
         if (pass < g_priv_passes && g_hist_priv) {
@@ -893,9 +1179,10 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
         } else {
             g_hist<false><<<grid_for(a.dim, 256 * 16), 256, 0, s>>>(a, kShift[pass], nbins, pass == 2, pass > 2);
         }
-        if (pass > 2) g_hist_cand<<<64, 256, 0, s>>>(a, kShift[pass], nbins);
+        g_hist_cand<<<148 * 2, 256, 0, s>>>(a, kShift[pass], nbins, pass <= 2);
         g_pick<<<1, 32, 0, s>>>(a, kShift[pass], nbins);
     }
+    if (g_use_bracket()) g_bracket_next<<<1, 1, 0, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -908,6 +1195,7 @@ cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s) {
 }
 
 cudaError_t g_launch_emit(const GlobalArgs& a, cudaStream_t s) {
+    if (g_fused_emit(a)) return cudaSuccess;  // g_requant8<L, true> emits
     g_emit<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
@@ -918,15 +1206,21 @@ cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s) {
         g_residual_dense<<<nch, kThreads, 0, s>>>(a);
         return cudaGetLastError();
     }
+    const bool emit = g_fused_emit(a);  // g_launch_emit left G3 to this kernel
+#define MA_RQ8(L)                                                                   \
+    if (emit) g_requant8<L, true><<<nch, kThreads, 0, s>>>(a);                     \
+    else g_requant8<L, false><<<nch, kThreads, 0, s>>>(a);                         \
+    return cudaGetLastError();
     switch (a.bucket) {  // the register path for 8 <= B_q <= 256
-        case 8: g_requant8<1><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
-        case 16: g_requant8<2><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
-        case 32: g_requant8<4><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
-        case 64: g_requant8<8><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
-        case 128: g_requant8<16><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
-        case 256: g_requant8<32><<<nch, kThreads, 0, s>>>(a); return cudaGetLastError();
+        case 8: MA_RQ8(1)
+        case 16: MA_RQ8(2)
+        case 32: MA_RQ8(4)
+        case 64: MA_RQ8(8)
+        case 128: MA_RQ8(16)
+        case 256: MA_RQ8(32)
         default: break;
     }
+#undef MA_RQ8
     const size_t smem = global_requant_smem(a.bucket);
     cudaError_t e = cudaFuncSetAttribute(g_requant, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;

@@ -90,6 +90,9 @@ struct GlobalArgs {
     unsigned int cand_cap;
     int32_t* bounds;     // [m][chunks + 1] first entry of each 4096-chunk per row
     int32_t* ovf_list;   // [chunks] chunks with more window entries than the staged path holds
+    uint64_t* seg_key;    // carried bracket: per-CTA segments of collected keys (cand_cap entries)
+    int64_t* seg_idx;     // their indices
+    unsigned int* seg_n;  // [kBracketCtas] keys collected per segment
     unsigned int* ovf_n;
     double* partials;    // nullable: [chunks][kReportFields]
     unsigned int* flag;
@@ -98,7 +101,9 @@ struct GlobalArgs {
     int32_t slot, g_dtype, p_dtype, v_dtype, check_finite, bucket_shift;
     double eps, lr, scale1, scale2;
 };
+constexpr int kBracketCtas = 148 * 8;  // g_bracket grid (one collection segment per CTA)
 int64_t global_chunks(int64_t dim);
+bool global_fused_emit(const GlobalArgs& a);  // G3 runs inside the re-quantization kernel
 size_t global_requant_smem(int64_t bucket);
 cudaError_t g_launch_levels(const GlobalArgs& a, cudaStream_t s);
 cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s);  // G1: six digit passes, no host sync

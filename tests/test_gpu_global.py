@@ -144,3 +144,30 @@ def test_global_dense_window_chunks(dt, density):
         torch.cuda.synchronize()
         assert np.array_equal(_bits(_host(p)), _bits(orc.state().params)), f"θ @ {s}"
     assert np.array_equal(eng.error_buffer().codes, orc.state().codes)
+
+
+@pytest.mark.parametrize("dt,levels", [("bf16", False), ("f32", True)])
+def test_global_carried_bracket_scale_jumps(dt, levels):
+    # The select carries a bracket around the previous step's K* (g_bracket):
+    # gradient scale jumps of 2^±12 move K* far outside it (fallback to the
+    # full digit passes, then a re-centred bracket), steady steps keep K*
+    # inside; 16-level gradients put many ties at K* inside the bracket.
+    d = 32_003  # the composed oracle takes the whole vector as one block (<= 32767)
+    hp = dict(lr=1e-2, window=4, density=0.01)
+    scales = [1.0, 1.0, 1.0, 2.0 ** 12, 2.0 ** 12, 2.0 ** 12, 2.0 ** -12, 1.0, 1.0, 1.0, 1.0]
+    torch = _torch()
+    th0 = _host(_dev(oracle.synth(1, 0, 0, d, dt), dt))
+    orc = oracle.Oracle(th0, dict(hp, block=d), param_dtype=dt, value_dtype="bf16")
+    eng = _global_engine(d, hp, dt, "bf16")
+    p = _dev(th0, dt)
+    for s, sc in enumerate(scales, start=1):
+        g = _host(_dev(oracle.synth(42, s, 0, d, dt, levels=levels) * sc, dt))
+        orc.step(g, hp["lr"])
+        eng.step(p, _dev(g, dt), hp["lr"])
+        torch.cuda.synchronize()
+        so = orc.state()
+        w = eng.window()
+        slot = (eng.counters()[1] + hp["window"] - 1) % hp["window"]
+        assert np.array_equal(w.indices[slot], so.win_idx[slot]), f"selection @ {s}"
+        assert np.array_equal(eng.error_buffer().codes, so.codes), f"codes @ {s}"
+        assert np.array_equal(_bits(_host(p)), _bits(so.params)), f"θ @ {s}"
