@@ -208,6 +208,7 @@ struct ma_handle {
     uint64_t* g_seg_key = nullptr;
     int64_t* g_seg_idx = nullptr;
     unsigned* g_seg_n = nullptr;
+    bool g_bounds_valid = false;  // per-row chunk bounds of the global window (emit keeps the new row's)
     int32_t* g_ovf = nullptr;
     unsigned cand_cap = 0;
     int32_t* g_bounds = nullptr;
@@ -531,8 +532,9 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
         w.w1[r] = a.w1[r];
         w.w2[r] = a.w2[r];
     }
-    MA_CUDA(ma::g_launch_stats_update(g, w, int(h->filled), st));
-    h->launches += ma::global_fused_emit(g) ? 4 : 5;
+    MA_CUDA(ma::g_launch_stats_update(g, w, int(h->filled), !h->g_bounds_valid, st));
+    h->launches += (ma::global_fused_emit(g) ? 3 : 4) + (h->g_bounds_valid ? 0 : 1);
+    h->g_bounds_valid = true;
     ma_status ms = mark_done(h, st);
     if (ms != MA_OK) return ms;
     if (report) {
@@ -1257,6 +1259,7 @@ ma_status ma_write_state(ma_handle* h, const uint8_t* codes, const double* lo, c
             }
         { ma_status cs = commit_ef(); if (cs != MA_OK) return cs; }
         MA_CUDA(cudaMemcpy(h->d_win_idx, gi.data(), gi.size() * 8, cudaMemcpyHostToDevice));
+        h->g_bounds_valid = false;  // every row changed: the next step recomputes all chunk bounds
         MA_CUDA(cudaMemcpy(h->d_win_val, gv.data(), gv.size(), cudaMemcpyHostToDevice));
         h->step = step;
         h->head = head;

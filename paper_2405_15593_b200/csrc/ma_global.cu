@@ -259,6 +259,12 @@ __global__ void g_emit(GlobalArgs p) {
     const int64_t c0 = int64_t(blockIdx.x) * kChunk;
     const int64_t e0 = c0 + int64_t(threadIdx.x) * kPer;
     const int2 cs = p.sel_info[blockIdx.x];  // (row offset, ties to take in this chunk)
+    if (threadIdx.x == 0) {  // the new row's chunk bounds (what g_bounds would find)
+        const int64_t nch = global_chunks_d(p.dim);
+        int32_t* bd = p.bounds + int64_t(p.slot) * (nch + 1);
+        bd[blockIdx.x] = cs.x;
+        if (blockIdx.x == nch - 1) bd[nch] = static_cast<int32_t>(p.k);
+    }
     uint32_t gtm = 0, eqm = 0;
     const uint64_t kstar = p.sel_state[0];
     double av[kPer];
@@ -306,7 +312,7 @@ __global__ void g_emit(GlobalArgs p) {
 // within) and written to the window row at the chunk's row offset, exactly as
 // g_emit writes it.
 template <int LPB, bool EMIT>
-__global__ void g_requant8(GlobalArgs p) {
+__global__ void __launch_bounds__(kThreads, 4) g_requant8(GlobalArgs p) {
     __shared__ double s_red[kThreads / 32][4];
     __shared__ int s_tmp[33];
     const int64_t c0 = int64_t(blockIdx.x) * kChunk;
@@ -318,6 +324,12 @@ __global__ void g_requant8(GlobalArgs p) {
         kstar = p.sel_state[0];
     }
     int64_t* ri = p.win_idx + int64_t(p.slot) * p.row_stride;
+    if (EMIT && threadIdx.x == 0) {  // the new row's chunk bounds (what g_bounds would find)
+        const int64_t nch = global_chunks_d(p.dim);
+        int32_t* bd = p.bounds + int64_t(p.slot) * (nch + 1);
+        bd[blockIdx.x] = cs.x;
+        if (blockIdx.x == nch - 1) bd[nch] = static_cast<int32_t>(p.k);
+    }
 #pragma unroll 1
     for (int h = 0; h < kChunk / (8 * kThreads); ++h) {
         const int64_t i0 = c0 + 8 * (int64_t(threadIdx.x) + int64_t(h) * kThreads);
@@ -760,6 +772,133 @@ __global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w,
     g_nnz_partial(p, c, nnz, s_red);
 }
 
+// ADAM_STATS + update for one 4096-chunk, sparse form: coordinates held by one
+// window entry (most of them) are updated from that entry alone — z = 0 + w·v,
+// z = 0 + w·v² (window.cpp:37-41 with one term) — and the few held by several
+// entries are summed in physical slot order by their owner (the entry in the
+// earliest row) over the chunk's duplicate list sorted into entry order.
+// Chunks with more than kDupList duplicate entries (dense windows) or more
+// than kStage entries go to the overflow list (g_stats_update_dense) before
+// anything is written.
+constexpr int kDupList = 64;
+__global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, const __grid_constant__ GWeights w,
+                                                           int filled) {
+    extern __shared__ uint4 s_th4[];  // the chunk's θ, staged with 16-byte loads
+    __shared__ double s_red[kThreads / 32];
+    __shared__ int s_j0[kMaxWindowGlobal], s_off[kMaxWindowGlobal + 1];
+    __shared__ int16_t s_ei[kStage];
+    __shared__ uint8_t s_er[kStage];
+    __shared__ double s_ev[kStage];
+    __shared__ uint32_t s_seen[kChunk / 32], s_dup[kChunk / 32];
+    __shared__ int16_t s_dl[kDupList], s_ds[kDupList];
+    __shared__ int s_nd;
+    const int64_t c = blockIdx.x, c0 = c * kChunk;
+    const int psz = p.p_dtype == F64 ? 8 : (p.p_dtype == F32 ? 4 : 2);
+    const int n = static_cast<int>(p.dim - c0 < kChunk ? p.dim - c0 : kChunk);
+    const bool vec = n == kChunk && (reinterpret_cast<uintptr_t>(p.params) & 15u) == 0;
+    const int nv16 = kChunk * psz / 16;
+    if (vec) {
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(p.params) + c0 * psz);
+        for (int t = threadIdx.x; t < nv16; t += kThreads) s_th4[t] = src[t];
+    }
+    for (int t = threadIdx.x; t < kChunk / 32; t += kThreads) {
+        s_seen[t] = 0;
+        s_dup[t] = 0;
+    }
+    if (threadIdx.x == 0) s_nd = 0;
+    const int total = chunk_rows(p, c, filled, s_j0, s_off);  // (synchronises)
+    if (total > kStage) {
+        if (threadIdx.x == 0) p.ovf_list[atomicAdd(p.ovf_n, 1u)] = static_cast<int>(c);
+        return;
+    }
+    for (int e = threadIdx.x; e < total; e += kThreads) {
+        int r = 0;
+        while (s_off[r + 1] <= e) ++r;
+        const int64_t q = int64_t(r) * p.row_stride + s_j0[r] + (e - s_off[r]);
+        const int i = static_cast<int>(p.win_idx[q] - c0);
+        s_ei[e] = static_cast<int16_t>(i);
+        s_er[e] = static_cast<uint8_t>(r);
+        s_ev[e] = ld_val(p.win_val, p.v_dtype, q);
+        const uint32_t bit = 1u << (i & 31);
+        if (atomicOr(&s_seen[i >> 5], bit) & bit) atomicOr(&s_dup[i >> 5], bit);
+    }
+    __syncthreads();
+    int nd_t = 0;
+    for (int e = threadIdx.x; e < total; e += kThreads) nd_t += (s_dup[s_ei[e] >> 5] >> (s_ei[e] & 31)) & 1u;
+    nd_t = __reduce_add_sync(0xFFFFFFFFu, nd_t);
+    if ((threadIdx.x & 31) == 0 && nd_t) atomicAdd(&s_nd, nd_t);
+    __syncthreads();
+    const int nd = s_nd;
+    if (nd > kDupList) {
+        if (threadIdx.x == 0) p.ovf_list[atomicAdd(p.ovf_n, 1u)] = static_cast<int>(c);
+        return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_nd = 0;
+    __syncthreads();
+    double nnz = 0.0;
+    void* th = s_th4;
+    for (int e = threadIdx.x; e < total; e += kThreads) {
+        const int i = s_ei[e];
+        if ((s_dup[i >> 5] >> (i & 31)) & 1u) {
+            s_dl[atomicAdd(&s_nd, 1)] = static_cast<int16_t>(e);
+            continue;
+        }
+        const int r = s_er[e];
+        const double v = s_ev[e];
+        const double z1 = __dadd_rn(0.0, __dmul_rn(w.w1[r], v));
+        const double z2 = __dadd_rn(0.0, __dmul_rn(w.w2[r], __dmul_rn(v, v)));
+        if (z1 == 0.0 && z2 == 0.0) continue;
+        if (vec) {
+            const double u = __ddiv_rn(__dmul_rn(z1, p.scale1), __dadd_rn(p.eps, __dsqrt_rn(__dmul_rn(z2, p.scale2))));
+            if (u != 0.0) nnz += 1.0;
+            st_val(th, p.p_dtype, i, __dsub_rn(ld_val(th, p.p_dtype, i), __dmul_rn(p.lr, u)));
+        } else {
+            g_apply(p, c0 + i, z1, z2, nnz);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nd) {  // duplicate list into entry (= slot) order
+        const int e = s_dl[threadIdx.x];
+        int rank = 0;
+        for (int j = 0; j < nd; ++j) rank += s_dl[j] < e;
+        s_ds[rank] = static_cast<int16_t>(e);
+    }
+    __syncthreads();
+    if (threadIdx.x < nd) {
+        const int e = s_ds[threadIdx.x], i = s_ei[e];
+        bool owner = true;
+        for (int j = 0; j < static_cast<int>(threadIdx.x); ++j) owner &= s_ei[s_ds[j]] != i;
+        if (owner) {
+            double z1 = 0.0, z2 = 0.0;
+            for (int j = threadIdx.x; j < nd; ++j) {
+                const int ej = s_ds[j];
+                if (s_ei[ej] != i) continue;
+                const int r = s_er[ej];
+                const double v = s_ev[ej];
+                z1 = __dadd_rn(z1, __dmul_rn(w.w1[r], v));
+                z2 = __dadd_rn(z2, __dmul_rn(w.w2[r], __dmul_rn(v, v)));
+            }
+            if (z1 != 0.0 || z2 != 0.0) {
+                if (vec) {
+                    const double u =
+                        __ddiv_rn(__dmul_rn(z1, p.scale1), __dadd_rn(p.eps, __dsqrt_rn(__dmul_rn(z2, p.scale2))));
+                    if (u != 0.0) nnz += 1.0;
+                    st_val(th, p.p_dtype, i, __dsub_rn(ld_val(th, p.p_dtype, i), __dmul_rn(p.lr, u)));
+                } else {
+                    g_apply(p, c0 + i, z1, z2, nnz);
+                }
+            }
+        }
+    }
+    if (vec) {
+        __syncthreads();
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<unsigned char*>(p.params) + c0 * psz);
+        for (int t = threadIdx.x; t < nv16; t += kThreads) dst[t] = s_th4[t];
+    }
+    g_nnz_partial(p, c, nnz, s_red);
+}
+
 // Chunks with more window entries than kStage: dense accumulators in shared
 // memory, rows in slot order (persistent CTAs over the overflow list).
 __global__ void g_stats_update_dense(GlobalArgs p, const __grid_constant__ GWeights w, int filled) {
@@ -845,7 +984,7 @@ __global__ void g_count_cand(GlobalArgs p) {
 // the full digit passes (g_bracket_check resets the state). The bracket only
 // decides which kernels do the work, never the result.
 // sel_state: [5] Kc, [6] W (0: no bracket yet), [7] keys above, [8] bracket ok
-__global__ void __launch_bounds__(256) g_bracket(GlobalArgs p) {
+__global__ void __launch_bounds__(256, 6) g_bracket(GlobalArgs p) {
     __shared__ unsigned long long s_above;
     __shared__ unsigned s_cn;  // keys collected into this CTA's segment
     const uint64_t kc = p.sel_state[5], w = p.sel_state[6];
@@ -1228,14 +1367,27 @@ cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t g_launch_stats_update(const GlobalArgs& a, const GWeights& w, int filled, cudaStream_t s) {
-    g_bounds<<<grid_for(int64_t(filled) * a.k, 256 * 4), 256, 0, s>>>(a, filled);
+cudaError_t g_launch_stats_update(const GlobalArgs& a, const GWeights& w, int filled, bool all_bounds,
+                                  cudaStream_t s) {
+    // the emitters write the new row's chunk bounds; every row's only after a
+    // state load (or before the first step)
+    if (all_bounds) g_bounds<<<grid_for(int64_t(filled) * a.k, 256 * 4), 256, 0, s>>>(a, filled);
     cudaError_t e = cudaMemsetAsync(a.ovf_n, 0, sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     const size_t th_smem = size_t(kChunk) * (a.p_dtype == F64 ? 8 : (a.p_dtype == F32 ? 4 : 2));
-    e = cudaFuncSetAttribute(g_stats_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(th_smem));
-    if (e != cudaSuccess) return e;
-    g_stats_update<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, th_smem, s>>>(a, w, filled);
+    static const bool sparse = [] {  // A/B: MA_GLOBAL_STATS_SPARSE=0 runs the owner / row-loop kernel
+        const char* v = std::getenv("MA_GLOBAL_STATS_SPARSE");
+        return !(v && v[0] == '0');
+    }();
+    if (sparse) {
+        e = cudaFuncSetAttribute(g_stats_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, int(th_smem));
+        if (e != cudaSuccess) return e;
+        g_stats_sparse<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, th_smem, s>>>(a, w, filled);
+    } else {
+        e = cudaFuncSetAttribute(g_stats_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(th_smem));
+        if (e != cudaSuccess) return e;
+        g_stats_update<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, th_smem, s>>>(a, w, filled);
+    }
     const size_t smem = size_t(kChunk) * 2 * sizeof(double);
     e = cudaFuncSetAttribute(g_stats_update_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;

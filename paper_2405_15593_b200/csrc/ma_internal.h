@@ -114,7 +114,8 @@ struct GWeights {
     double w1[kMaxWindowGlobal];
     double w2[kMaxWindowGlobal];
 };
-cudaError_t g_launch_stats_update(const GlobalArgs& a, const GWeights& w, int filled, cudaStream_t s);
+cudaError_t g_launch_stats_update(const GlobalArgs& a, const GWeights& w, int filled, bool all_bounds,
+                                  cudaStream_t s);
 
 struct Variant {
     int nt;   // threads per CTA
