@@ -208,6 +208,7 @@ struct ma_handle {
     uint64_t* g_seg_key = nullptr;
     int64_t* g_seg_idx = nullptr;
     unsigned* g_seg_n = nullptr;
+    int32_t* g_tiles = nullptr;
     bool g_bounds_valid = false;  // per-row chunk bounds of the global window (emit keeps the new row's)
     int32_t* g_ovf = nullptr;
     unsigned cand_cap = 0;
@@ -289,6 +290,7 @@ void free_handle(ma_handle* h) {
     cudaFree(h->g_seg_key);
     cudaFree(h->g_seg_idx);
     cudaFree(h->g_seg_n);
+    cudaFree(h->g_tiles);
     cudaFree(h->g_ovf);
     cudaFree(h->g_bounds);
     cudaFree(h->d_dense);
@@ -494,6 +496,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     g.seg_key = h->g_seg_key;
     g.seg_idx = h->g_seg_idx;
     g.seg_n = h->g_seg_n;
+    g.tiles = h->g_tiles;
     g.cand_n = reinterpret_cast<unsigned int*>(h->g_selstate + 3);
     g.cand_cap = h->cand_cap;
     g.ovf_list = h->g_ovf;
@@ -524,7 +527,7 @@ ma_status run_step_global(ma_handle* h, void* d_params, const void* d_grads, dou
     // one-CTA scan — the step never waits for the host.
     MA_CUDA(ma::g_launch_select(g, st));
     MA_CUDA(ma::g_launch_count(g, st));
-    h->launches += 28;  // levels, select (init, bracket x4, 6 x (hist, hist_cand, pick), next), count x3
+    h->launches += 31;  // levels, select (init, bracket 2 x 3 + compact, 6 x (hist, hist_cand, pick), next), count x3
     MA_CUDA(ma::g_launch_emit(g, st));
     MA_CUDA(ma::g_launch_requant(g, st));
     ma::GWeights w;
@@ -742,14 +745,15 @@ ma_status ma_create_shard(const ma_config* cfg, int64_t dim, int64_t block_begin
         alloc(reinterpret_cast<void**>(&h->g_ovf), size_t(nch) * sizeof(int32_t));
         // MA_GLOBAL_CAND_CAP (tests): a small capacity forces the overflow path
         const char* cc = std::getenv("MA_GLOBAL_CAND_CAP");
-        // default: d / 128 keys (the carried bracket's collection), 1M..32M
-        const int64_t cap_d = std::min<int64_t>(int64_t(32) << 20, std::max<int64_t>(kGlobalCandCap, s.dim / 128));
+        // default: d / 128 keys (the carried bracket's collection), 1M..64M
+        const int64_t cap_d = std::min<int64_t>(int64_t(64) << 20, std::max<int64_t>(kGlobalCandCap, s.dim / 128));
         h->cand_cap = cc ? static_cast<unsigned>(std::strtoul(cc, nullptr, 10)) : static_cast<unsigned>(cap_d);
         alloc(reinterpret_cast<void**>(&h->g_cand), size_t(h->cand_cap) * sizeof(uint64_t));
         alloc(reinterpret_cast<void**>(&h->g_cand_idx), size_t(h->cand_cap) * sizeof(int64_t));
         alloc(reinterpret_cast<void**>(&h->g_seg_key), size_t(h->cand_cap) * sizeof(uint64_t));
         alloc(reinterpret_cast<void**>(&h->g_seg_idx), size_t(h->cand_cap) * sizeof(int64_t));
         alloc(reinterpret_cast<void**>(&h->g_seg_n), size_t(ma::kBracketCtas) * sizeof(unsigned));
+        alloc(reinterpret_cast<void**>(&h->g_tiles), size_t(nch / 1024 + 1) * 4 * sizeof(int32_t));
         alloc(reinterpret_cast<void**>(&h->g_bounds), size_t(cfg->hp.window) * size_t(nch + 1) * sizeof(int32_t));
     }
     alloc(&h->d_win_val, went * dtype_size(cfg->value_dtype));

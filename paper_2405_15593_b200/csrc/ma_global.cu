@@ -355,15 +355,22 @@ __global__ void __launch_bounds__(kThreads, 4) g_requant8(GlobalArgs p) {
                 gtm &= maybe;
                 eqm &= maybe;
             }
-            int te;
-            int tie_before = cta_excl_scan(__popc(eqm), s_tmp, te);
+            // one scan of (above, ties) packed in 16-bit halves (<= 2048 each);
+            // a second only in the chunk holding ties at K*
+            int both;
+            const int pre = cta_excl_scan(__popc(gtm) | (__popc(eqm) << 16), s_tmp, both);
+            const int te = both >> 16;
             sw = gtm;
-            for (uint32_t m = eqm; m; m &= m - 1) {
-                if (tie_before < cs.y) sw |= m & (0u - m);
-                ++tie_before;
+            int tot = both & 0xFFFF;
+            int pos = cs.x + (pre & 0xFFFF);
+            if (te) {
+                int tie_before = pre >> 16;
+                for (uint32_t m = eqm; m; m &= m - 1) {
+                    if (tie_before < cs.y) sw |= m & (0u - m);
+                    ++tie_before;
+                }
+                pos = cs.x + cta_excl_scan(__popc(sw), s_tmp, tot);
             }
-            int tot;
-            int pos = cs.x + cta_excl_scan(__popc(sw), s_tmp, tot);
             for (uint32_t m = sw; m; m &= m - 1) {
                 const int e = __ffs(m) - 1;
                 ri[pos] = i0 + e;
@@ -984,15 +991,14 @@ __global__ void g_count_cand(GlobalArgs p) {
 // the full digit passes (g_bracket_check resets the state). The bracket only
 // decides which kernels do the work, never the result.
 // sel_state: [5] Kc, [6] W (0: no bracket yet), [7] keys above, [8] bracket ok
-__global__ void __launch_bounds__(256, 6) g_bracket(GlobalArgs p) {
+__global__ void __launch_bounds__(256, 6) g_bracket(GlobalArgs p, int pass) {
     __shared__ unsigned long long s_above;
     __shared__ unsigned s_cn;  // keys collected into this CTA's segment
-    const uint64_t kc = p.sel_state[5], w = p.sel_state[6];
-    if (w == 0) return;
-    // the bracket widened to whole 2^32 steps of the key: the tests below read
+    if (pass == 0 ? p.sel_state[6] == 0 : p.sel_state[11] == 0) return;  // no bracket yet / no retry
+    // [lo, hi] widened to whole 2^32 steps of the key: the tests below read
     // only the high word of |a| (keys >= lo32 << 32 and <= hi32 << 32 | ~0u)
-    const uint32_t lo32 = static_cast<uint32_t>((kc > w ? kc - w : 0) >> 32);
-    const uint32_t hi32 = static_cast<uint32_t>((kc + w) >> 32), span = hi32 - lo32;
+    const uint32_t lo32 = static_cast<uint32_t>(p.sel_state[12] >> 32);
+    const uint32_t hi32 = static_cast<uint32_t>(p.sel_state[13] >> 32), span = hi32 - lo32;
     // keys go to this CTA's segment of seg_key / seg_idx, slots taken with a
     // shared-memory counter (a global one serialises every warp in L2)
     const unsigned seg_cap = p.cand_cap / gridDim.x;
@@ -1067,27 +1073,32 @@ __global__ void __launch_bounds__(256, 6) g_bracket(GlobalArgs p) {
     if (threadIdx.x == 0) {
         if (s_above) atomicAdd(&p.sel_state[7], s_above);
         p.seg_n[blockIdx.x] = s_cn;
+        if (blockIdx.x == 0) p.sel_state[14] = 1;  // the per-chunk counts now hold this pass's
     }
 }
 
 // Does the bracket hold the k-th largest key? Yes: the digit picks start over
 // the collected keys with k - above entries to place (g_bracket_compact packs
-// the segments into cand first). No: full passes, from a clean state
-// (g_cnt_reset clears the per-chunk counts the bracket made).
-// sel_state[10]: the bracket's width exponent (adapted here and in g_bracket_next)
-__global__ void g_bracket_check(GlobalArgs p) {
+// the segments into cand first). No, on the first pass without overflow: one
+// retry with a bracket 4x as wide on the side K* lies (the counts say which).
+// Otherwise: full digit passes from a clean state (g_cnt_reset clears the
+// per-chunk counts a bracket pass made).
+// sel_state: [8] ok, [10] width exponent, [11] retry pending, [12]/[13] the
+// bracket [lo, hi], [14] per-chunk counts dirty, [15] reset them
+__global__ void g_bracket_check(GlobalArgs p, int pass) {
     __shared__ unsigned long long s_n;
     __shared__ int s_ovf;
+    if (pass == 1 && p.sel_state[11] == 0) return;  // no retry pending: state stands
     if (threadIdx.x == 0) {
         s_n = 0;
         s_ovf = 0;
     }
     __syncthreads();
-    const unsigned long long w = p.sel_state[6], above = p.sel_state[7];
+    const unsigned long long attempted = pass == 0 ? p.sel_state[6] : 1ull, above = p.sel_state[7];
     const unsigned seg_cap = p.cand_cap / kBracketCtas;
     unsigned long long n_t = 0;
     int ovf_t = 0;
-    if (w != 0)
+    if (attempted)
         for (int b = threadIdx.x; b < kBracketCtas; b += blockDim.x) {
             const unsigned c = p.seg_n[b];
             n_t += c;
@@ -1097,21 +1108,41 @@ __global__ void g_bracket_check(GlobalArgs p) {
     if (ovf_t) s_ovf = 1;
     __syncthreads();
     if (threadIdx.x != 0) return;
-    const unsigned long long n = s_n;
-    const bool ok = w != 0 && !s_ovf && above < static_cast<unsigned long long>(p.k) &&
-                    above + n >= static_cast<unsigned long long>(p.k);
+    const unsigned long long n = s_n, k = static_cast<unsigned long long>(p.k);
+    const bool ok = attempted && !s_ovf && above < k && above + n >= k;
     p.sel_state[8] = ok;
+    p.sel_state[11] = 0;
+    p.sel_state[15] = !ok && p.sel_state[14];
+    p.sel_state[14] = 0;
     if (ok) {
-        p.sel_state[2] = static_cast<unsigned long long>(p.k) - above;
+        p.sel_state[2] = k - above;
         *p.cand_n = static_cast<unsigned>(n);
-    } else {
-        *p.cand_n = 0;
-        p.sel_state[2] = static_cast<unsigned long long>(p.k);
-        if (w != 0) {  // narrower if a segment overflowed, else wider
-            long long e = static_cast<long long>(p.sel_state[10]) + (s_ovf ? -1 : 1);
-            p.sel_state[10] = static_cast<unsigned long long>(e < 0 ? 0 : (e > 12 ? 12 : e));
-        }
+        return;
     }
+    *p.cand_n = 0;
+    p.sel_state[2] = k;
+    p.sel_state[7] = 0;
+    if (!attempted) return;
+    long long e = static_cast<long long>(p.sel_state[10]) + (s_ovf ? -1 : 1);  // for the next step
+    p.sel_state[10] = static_cast<unsigned long long>(e < 0 ? 0 : (e > 12 ? 12 : e));
+    if (pass == 0 && !s_ovf) {
+        const unsigned long long lo = (p.sel_state[12] >> 32) << 32, hi = p.sel_state[13] | 0xFFFFFFFFull;
+        const unsigned long long wide = 4 * (hi - lo + 1);
+        if (above >= k) {  // K* above the bracket
+            p.sel_state[12] = hi + 1;
+            p.sel_state[13] = hi + wide > hi ? hi + wide : ~0ull;
+        } else {  // K* below it
+            p.sel_state[13] = lo > 0 ? lo - 1 : 0;
+            p.sel_state[12] = lo > wide ? lo - wide : 0;
+        }
+        p.sel_state[11] = lo > 0 || above >= k;  // nothing below a bracket starting at 0
+    }
+}
+
+__global__ void g_cnt_reset(GlobalArgs p, int64_t nch) {
+    if (!p.sel_state[15]) return;
+    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < nch; c += int64_t(gridDim.x) * blockDim.x)
+        p.cnt[c] = make_int2(0, 0);
 }
 
 // Segments -> cand[0, n) (order is irrelevant to the digit picks and counts).
@@ -1133,31 +1164,27 @@ __global__ void g_bracket_compact(GlobalArgs p) {
     }
 }
 
-__global__ void g_cnt_reset(GlobalArgs p, int64_t nch) {
-    if (p.sel_state[8] || p.sel_state[6] == 0) return;
-    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < nch; c += int64_t(gridDim.x) * blockDim.x)
-        p.cnt[c] = make_int2(0, 0);
-}
-
-// The next step's bracket. K* drifts steadily while the error feedback builds
-// up (the keys grow as unselected coordinates accumulate), so the centre is
-// this step's K* plus the last change (linear extrapolation in key space) and
-// the half-width is that change (at least 2^40, ~2^-12 of a binade) times
-// 2^(e-1), e adapted: +1 after a miss, -1 after an overflow or a crowded
-// buffer. sel_state[9]: this step's K* for the next extrapolation.
+// The next step's bracket. K* drifts while the error feedback builds up (the
+// keys grow as unselected coordinates accumulate) and jitters with the
+// gradients, so the bracket spans both "no change" and "the same change
+// again": centre K* + delta / 2, half-width |delta| (at least 2^40, ~2^-12 of
+// a binade) times 2^(e-1), e adapted: +1 after a miss, -1 after an overflow or
+// a crowded buffer. sel_state[9]: this step's K* for the next delta.
 __global__ void g_bracket_next(GlobalArgs p) {
     const unsigned long long kstar = p.sel_state[0], prev = p.sel_state[9];
     const bool first = p.sel_state[6] == 0;
     long long e = first ? 2 : static_cast<long long>(p.sel_state[10]);
-    if (!first && p.sel_state[8] && *p.cand_n > p.cand_cap / 4 && e > 0) --e;
+    if (!first && p.sel_state[8] && *p.cand_n > p.cand_cap / 8 && e > 0) --e;
     const long long delta = first ? 0 : static_cast<long long>(kstar) - static_cast<long long>(prev);
     const unsigned long long ad = static_cast<unsigned long long>(delta < 0 ? -delta : delta);
     const unsigned long long base = ad > (1ull << 40) ? ad : (1ull << 40);
     unsigned long long w = e >= 1 ? base << (e - 1) : base >> 1;
     if (w > (1ull << 58)) w = 1ull << 58;
-    const long long c = static_cast<long long>(kstar) + delta;
-    p.sel_state[5] = static_cast<unsigned long long>(c < 0 ? 0 : c);
+    const long long c = static_cast<long long>(kstar) + delta / 2;
+    const unsigned long long cc = static_cast<unsigned long long>(c < 0 ? 0 : c);
     p.sel_state[6] = w;
+    p.sel_state[12] = cc > w ? cc - w : 0;
+    p.sel_state[13] = cc + w;
     p.sel_state[9] = kstar;
     p.sel_state[10] = static_cast<unsigned long long>(e);
 }
@@ -1173,6 +1200,9 @@ __global__ void g_sel_init(GlobalArgs p, int64_t nch) {
         *p.cand_n = 0;
         p.sel_state[7] = 0;
         p.sel_state[8] = 0;
+        p.sel_state[11] = 0;
+        p.sel_state[14] = 0;
+        p.sel_state[15] = 0;
     }
 }
 
@@ -1260,6 +1290,69 @@ bool g_use_bracket() {
     return on;
 }
 
+// g_alloc in three launches for many chunks: per-tile sums of the (> K*, == K*)
+// counts, one CTA scans the tiles (the ties a tile takes follow from the ties
+// before it: clamp(T - eq_before, 0, tile_eq)), then every tile scans its
+// chunks from its carries — the same offsets / ties as the one-CTA scan.
+__global__ void g_alloc_tiles(GlobalArgs p, int64_t nch) {
+    __shared__ int s_tmp[33];
+    const int64_t c = int64_t(blockIdx.x) * kAllocThreads + threadIdx.x;
+    const int2 cnt = c < nch ? p.cnt[c] : make_int2(0, 0);
+    int tg, te;
+    cta_excl_scan<kAllocThreads>(cnt.x, s_tmp, tg);
+    cta_excl_scan<kAllocThreads>(cnt.y, s_tmp, te);
+    if (threadIdx.x == 0) {
+        p.tiles[4 * blockIdx.x + 0] = tg;
+        p.tiles[4 * blockIdx.x + 1] = te;
+    }
+}
+
+__global__ void g_alloc_scan(GlobalArgs p, int64_t ntiles) {
+    __shared__ int s_tmp[33];
+    __shared__ long long s_carry[2];
+    if (threadIdx.x == 0) {
+        s_carry[0] = 0;
+        s_carry[1] = 0;
+    }
+    __syncthreads();
+    const long long ties = static_cast<long long>(p.sel_state[2]);
+    for (int64_t t0 = 0; t0 < ntiles; t0 += kAllocThreads) {
+        const int64_t t = t0 + threadIdx.x;
+        const int tg = t < ntiles ? p.tiles[4 * t + 0] : 0, te = t < ntiles ? p.tiles[4 * t + 1] : 0;
+        int tot_eq;
+        const long long eq_before = s_carry[1] + cta_excl_scan<kAllocThreads>(te, s_tmp, tot_eq);
+        long long take = ties - eq_before;
+        take = take < 0 ? 0 : (take > te ? te : take);
+        int tot_n;
+        const long long off = s_carry[0] + cta_excl_scan<kAllocThreads>(tg + static_cast<int>(take), s_tmp, tot_n);
+        if (t < ntiles) {
+            p.tiles[4 * t + 2] = static_cast<int>(off);
+            p.tiles[4 * t + 3] = static_cast<int>(eq_before);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_carry[0] += tot_n;
+            s_carry[1] += tot_eq;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void g_alloc_final(GlobalArgs p, int64_t nch) {
+    __shared__ int s_tmp[33];
+    const long long ties = static_cast<long long>(p.sel_state[2]);
+    const int64_t c = int64_t(blockIdx.x) * kAllocThreads + threadIdx.x;
+    const int2 cnt = c < nch ? p.cnt[c] : make_int2(0, 0);
+    const long long off0 = p.tiles[4 * blockIdx.x + 2], eqb0 = p.tiles[4 * blockIdx.x + 3];
+    int tot_eq;
+    const long long eq_before = eqb0 + cta_excl_scan<kAllocThreads>(cnt.y, s_tmp, tot_eq);
+    long long take = ties - eq_before;
+    take = take < 0 ? 0 : (take > cnt.y ? cnt.y : take);
+    int tot_n;
+    const long long off = off0 + cta_excl_scan<kAllocThreads>(cnt.x + static_cast<int>(take), s_tmp, tot_n);
+    if (c < nch) p.sel_info[c] = make_int2(static_cast<int>(off), static_cast<int>(take));
+}
+
 unsigned grid_for(int64_t n, int per) {
     const int64_t want = (n + per - 1) / per;
     return static_cast<unsigned>(want < 148 * 16 ? (want > 0 ? want : 1) : 148 * 16);
@@ -1302,10 +1395,13 @@ cudaError_t g_launch_select(const GlobalArgs& a, cudaStream_t s) {
     const int64_t nch = global_chunks(a.dim);
     g_sel_init<<<1, 1024, 0, s>>>(a, nch);
     if (g_use_bracket()) {
-        g_bracket<<<kBracketCtas, 256, 0, s>>>(a);
-        g_bracket_check<<<1, 256, 0, s>>>(a);
+        const unsigned rg = static_cast<unsigned>(nch < 148 * 64 ? (nch + 255) / 256 + 1 : 148 * 4);
+        for (int pass = 0; pass < 2; ++pass) {  // the bracket, then one retry beside it on a miss
+            g_bracket<<<kBracketCtas, 256, 0, s>>>(a, pass);
+            g_bracket_check<<<1, 256, 0, s>>>(a, pass);
+            g_cnt_reset<<<rg, 256, 0, s>>>(a, nch);
+        }
         g_bracket_compact<<<kBracketCtas, 256, 0, s>>>(a);
-        g_cnt_reset<<<static_cast<unsigned>(nch < 148 * 64 ? (nch + 255) / 256 + 1 : 148 * 4), 256, 0, s>>>(a, nch);
     }
     // digit 3 collects the keys sharing the 22-bit prefix; digits 4-6 read
     // them (a few thousand keys) instead of re-decoding d elements. With a
@@ -1329,7 +1425,15 @@ cudaError_t g_launch_count(const GlobalArgs& a, cudaStream_t s) {
     const int64_t nch = global_chunks(a.dim);
     g_count<<<static_cast<unsigned>(nch < 148 * 8 ? nch : 148 * 8), kThreads, 0, s>>>(a, nch);
     g_count_cand<<<256, 256, 0, s>>>(a);
-    g_alloc<<<1, kAllocThreads, 0, s>>>(a, nch);
+    const int64_t ntiles = (nch + kAllocThreads - 1) / kAllocThreads;
+    const char* tiled_env = std::getenv("MA_GLOBAL_ALLOC_TILED");  // tests: 1 = always the tiled scan
+    if (ntiles <= 4 && !(tiled_env && tiled_env[0] == '1')) {
+        g_alloc<<<1, kAllocThreads, 0, s>>>(a, nch);
+    } else {
+        g_alloc_tiles<<<static_cast<unsigned>(ntiles), kAllocThreads, 0, s>>>(a, nch);
+        g_alloc_scan<<<1, kAllocThreads, 0, s>>>(a, ntiles);
+        g_alloc_final<<<static_cast<unsigned>(ntiles), kAllocThreads, 0, s>>>(a, nch);
+    }
     return cudaGetLastError();
 }
 

@@ -93,6 +93,7 @@ struct GlobalArgs {
     uint64_t* seg_key;    // carried bracket: per-CTA segments of collected keys (cand_cap entries)
     int64_t* seg_idx;     // their indices
     unsigned int* seg_n;  // [kBracketCtas] keys collected per segment
+    int32_t* tiles;       // [chunks / 1024 + 1][4] g_alloc tile sums / carries
     unsigned int* ovf_n;
     double* partials;    // nullable: [chunks][kReportFields]
     unsigned int* flag;

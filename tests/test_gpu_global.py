@@ -171,3 +171,26 @@ def test_global_carried_bracket_scale_jumps(dt, levels):
         assert np.array_equal(w.indices[slot], so.win_idx[slot]), f"selection @ {s}"
         assert np.array_equal(eng.error_buffer().codes, so.codes), f"codes @ {s}"
         assert np.array_equal(_bits(_host(p)), _bits(so.params)), f"θ @ {s}"
+
+
+def test_global_tiled_allocation_scan(monkeypatch):
+    # the three-launch chunk allocation (g_alloc_tiles / g_alloc_scan /
+    # g_alloc_final) that large vectors use, forced at a size the composed
+    # oracle checks; 16-level gradients put ties at K* across chunks
+    monkeypatch.setenv("MA_GLOBAL_ALLOC_TILED", "1")
+    d = 31_000
+    hp = dict(lr=1e-2, window=3, density=0.05)
+    torch = _torch()
+    th0 = _host(_dev(oracle.synth(1, 0, 0, d, "bf16"), "bf16"))
+    orc = oracle.Oracle(th0, dict(hp, block=d), param_dtype="bf16", value_dtype="bf16")
+    eng = _global_engine(d, hp, "bf16", "bf16")
+    p = _dev(th0, "bf16")
+    for s in range(1, 7):
+        g = _host(_dev(oracle.synth(9, s, 0, d, "bf16", levels=s % 2 == 0), "bf16"))
+        orc.step(g, hp["lr"])
+        eng.step(p, _dev(g, "bf16"), hp["lr"])
+        torch.cuda.synchronize()
+        so = orc.state()
+        slot = (eng.counters()[1] + hp["window"] - 1) % hp["window"]
+        assert np.array_equal(eng.window().indices[slot], so.win_idx[slot]), f"selection @ {s}"
+        assert np.array_equal(_bits(_host(p)), _bits(so.params)), f"θ @ {s}"
