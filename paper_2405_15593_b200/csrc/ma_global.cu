@@ -27,6 +27,7 @@
 
 #include <cstdlib>
 
+#include "ma_async.cuh"
 #include "ma_device.cuh"
 #include "ma_internal.h"
 
@@ -36,6 +37,10 @@ namespace {
 using namespace dev;
 
 constexpr int kChunk = 4096;     // elements per CTA in G2/G3/G4
+#ifndef MA_RQ8_UNROLL
+#define MA_RQ8_UNROLL 1  // A/B: 2 = both 2048-element halves of a chunk in flight
+#endif
+constexpr int kRq8Unroll = MA_RQ8_UNROLL;
 constexpr int kThreads = 256;
 constexpr int kPer = kChunk / kThreads;  // 16 elements per thread (strided by 256)
 
@@ -330,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 4) g_requant8(GlobalArgs p) {
         bd[blockIdx.x] = cs.x;
         if (blockIdx.x == nch - 1) bd[nch] = static_cast<int32_t>(p.k);
     }
-#pragma unroll 1
+#pragma unroll kRq8Unroll
     for (int h = 0; h < kChunk / (8 * kThreads); ++h) {
         const int64_t i0 = c0 + 8 * (int64_t(threadIdx.x) + int64_t(h) * kThreads);
         double a[8];
@@ -803,11 +808,19 @@ __global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, cons
     const int psz = p.p_dtype == F64 ? 8 : (p.p_dtype == F32 ? 4 : 2);
     const int n = static_cast<int>(p.dim - c0 < kChunk ? p.dim - c0 : kChunk);
     const bool vec = n == kChunk && (reinterpret_cast<uintptr_t>(p.params) & 15u) == 0;
-    const int nv16 = kChunk * psz / 16;
-    if (vec) {
-        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(p.params) + c0 * psz);
-        for (int t = threadIdx.x; t < nv16; t += kThreads) s_th4[t] = src[t];
+    // θ of the chunk: one bulk copy (TMA) in flight while the window entries load
+    __shared__ __align__(8) uint64_t s_bar;
+    if (vec && threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&s_bar, kChunk * psz);
+        bulk_g2s(s_th4, static_cast<const unsigned char*>(p.params) + c0 * psz, kChunk * psz, &s_bar);
     }
+    auto theta_landed = [&] {
+        if (vec)
+            while (!mbar_try_wait(&s_bar, 0)) {
+            }
+    };
     for (int t = threadIdx.x; t < kChunk / 32; t += kThreads) {
         s_seen[t] = 0;
         s_dup[t] = 0;
@@ -816,6 +829,7 @@ __global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, cons
     const int total = chunk_rows(p, c, filled, s_j0, s_off);  // (synchronises)
     if (total > kStage) {
         if (threadIdx.x == 0) p.ovf_list[atomicAdd(p.ovf_n, 1u)] = static_cast<int>(c);
+        theta_landed();  // no bulk copy may still target this CTA's shared memory
         return;
     }
     for (int e = threadIdx.x; e < total; e += kThreads) {
@@ -838,10 +852,12 @@ __global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, cons
     const int nd = s_nd;
     if (nd > kDupList) {
         if (threadIdx.x == 0) p.ovf_list[atomicAdd(p.ovf_n, 1u)] = static_cast<int>(c);
+        theta_landed();
         return;
     }
     __syncthreads();
     if (threadIdx.x == 0) s_nd = 0;
+    theta_landed();
     __syncthreads();
     double nnz = 0.0;
     void* th = s_th4;
@@ -898,12 +914,15 @@ __global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, cons
             }
         }
     }
-    if (vec) {
+    if (vec) {  // θ back by one bulk copy once every update landed in shared memory
         __syncthreads();
-        uint4* dst = reinterpret_cast<uint4*>(static_cast<unsigned char*>(p.params) + c0 * psz);
-        for (int t = threadIdx.x; t < nv16; t += kThreads) dst[t] = s_th4[t];
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_s2g(static_cast<unsigned char*>(p.params) + c0 * psz, s_th4, kChunk * psz);
+        }
     }
     g_nnz_partial(p, c, nnz, s_red);
+    if (vec && threadIdx.x == 0) bulk_wait_read();
 }
 
 // Chunks with more window entries than kStage: dense accumulators in shared
