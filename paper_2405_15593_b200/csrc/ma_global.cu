@@ -1032,22 +1032,48 @@ __global__ void __launch_bounds__(256, 6) g_bracket(GlobalArgs p, int pass) {
     unsigned above_t = 0;
     const int lane = threadIdx.x & 31;
     const int64_t ngroups = (p.dim + 7) / 8;
+    // fp32 screen (bf16 gradients, a bucket holds each 8-group): groups whose
+    // 8 keys are certainly below the bracket skip the fp64 decode. a32 =
+    // rn(g + rn(c lv32 + lo32)) is within 2^-23 (15|lv| + |lo|) + |a32| 2^-24
+    // (x 1.01) of the fp64 a (quantize.cpp:164-178 + optim.cpp:166-168:
+    // lv32, lo32, the FFMA and the FADD each round once); a group passes when
+    // some |a32| (1 + 2^-22) + 2 (15|lv32| + |lo32|) 2^-22 + 2^-126 >= the
+    // bracket's lower end rounded down to fp32, or is NaN.
+    const bool scr = p.g_dtype == BF16 && !p.dense && p.bucket_shift >= 3 &&
+                     (reinterpret_cast<uintptr_t>(p.grads) & 15u) == 0 && lo32 > 0;
+    const float t32 = __double2float_rd(__longlong_as_double(static_cast<long long>(uint64_t(lo32) << 32)));
     for (int64_t gi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; gi < ngroups;
          gi += int64_t(gridDim.x) * blockDim.x) {
-        double a[8];
-        const int nv = g_a8(p, gi * 8, a);
         const unsigned act = __activemask();
+        uint32_t hit = 0xFFu;  // elements the fp64 decode must see
+        if (scr && gi * 8 + 8 <= p.dim) {
+            const int64_t i0 = gi * 8, q = i0 >> p.bucket_shift;
+            const float lo32f = __double2float_rn(p.meta[q].x), lv32 = __double2float_rn(p.level[q]);
+            const float eb = __fmaf_ru(__fmaf_ru(15.0f, fabsf(lv32), fabsf(lo32f)), 0x1p-21f, 0x1p-126f);
+            const float thr = __fsub_rd(t32, eb);
+            const uint4 v = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(p.grads) + i0);
+            const uint32_t cw = *reinterpret_cast<const uint32_t*>(p.codes + (i0 >> 1));
+            const uint32_t ce = cw & 0x0F0F0F0Fu, co = (cw >> 4) & 0x0F0F0F0Fu;
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            const float2 lv2 = make_float2(lv32, lv32), lo2 = make_float2(lo32f, lo32f);
+            const float2 m23 = make_float2(-8388608.0f, -8388608.0f);
+            hit = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float2 c2 = make_float2(__uint_as_float(__byte_perm(ce, 0x4B000000u, 0x7540u | k)),
+                                        __uint_as_float(__byte_perm(co, 0x4B000000u, 0x7540u | k)));
+                c2 = __fadd2_rn(c2, m23);
+                const float2 a2 = __fadd2_rn(make_float2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xFFFF0000u)),
+                                             __ffma2_rn(c2, lv2, lo2));
+                hit |= static_cast<uint32_t>(!(__fmul_ru(fabsf(a2.x), 1.0f + 0x1p-22f) < thr)) << (2 * k);
+                hit |= static_cast<uint32_t>(!(__fmul_ru(fabsf(a2.y), 1.0f + 0x1p-22f) < thr)) << (2 * k + 1);
+            }
+        }
+        double a[8];
         uint32_t inm = 0;
         int above = 0;
-        if (nv == 8) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const uint32_t h = static_cast<uint32_t>(__double2hiint(a[e])) & 0x7FFFFFFFu;
-                mx = max(mx, h);
-                above += h > hi32;
-                inm |= static_cast<uint32_t>(h - lo32 <= span) << e;
-            }
-        } else {
+        if (hit == 0xFFu) {  // not screened (or every element hit): the 8-group decode
+            const int nv = g_a8(p, gi * 8, a);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const uint32_t h = static_cast<uint32_t>(__double2hiint(a[e])) & 0x7FFFFFFFu;
@@ -1056,6 +1082,15 @@ __global__ void __launch_bounds__(256, 6) g_bracket(GlobalArgs p, int pass) {
                     above += h > hi32;
                     inm |= static_cast<uint32_t>(h - lo32 <= span) << e;
                 }
+            }
+        } else {
+            for (uint32_t m = hit; m; m &= m - 1) {  // the few screen hits, one at a time
+                const int e = __ffs(m) - 1;
+                a[e] = g_a(p, gi * 8 + e);
+                const uint32_t h = static_cast<uint32_t>(__double2hiint(a[e])) & 0x7FFFFFFFu;
+                mx = max(mx, h);
+                above += h > hi32;
+                inm |= static_cast<uint32_t>(h - lo32 <= span) << e;
             }
         }
         // keys above the bracket are above K*: count them per chunk (a warp's
