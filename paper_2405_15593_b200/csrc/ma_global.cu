@@ -690,7 +690,7 @@ __device__ __forceinline__ void g_nnz_partial(const GlobalArgs& p, int64_t c, do
     __syncthreads();
     if (threadIdx.x == 0) {
         double sum = 0.0;
-        for (int w2 = 0; w2 < kThreads / 32; ++w2) sum += s_red[w2];
+        for (int w2 = 0; w2 < static_cast<int>(blockDim.x / 32); ++w2) sum += s_red[w2];
         p.partials[c * kReportFields + 4] = sum;
     }
     __syncthreads();
@@ -793,10 +793,15 @@ __global__ void g_stats_update(GlobalArgs p, const __grid_constant__ GWeights w,
 // than kStage entries go to the overflow list (g_stats_update_dense) before
 // anything is written.
 constexpr int kDupList = 64;
-__global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, const __grid_constant__ GWeights w,
+#ifndef MA_STATS_NT
+#define MA_STATS_NT 256
+#endif
+constexpr int kStatsThreads = MA_STATS_NT;  // threads per chunk of g_stats_sparse
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 7 : 12) g_stats_sparse(GlobalArgs p, const __grid_constant__ GWeights w,
                                                            int filled) {
     extern __shared__ uint4 s_th4[];  // the chunk's θ, staged with 16-byte loads
-    __shared__ double s_red[kThreads / 32];
+    __shared__ double s_red[NT / 32];
     __shared__ int s_j0[kMaxWindowGlobal], s_off[kMaxWindowGlobal + 1];
     __shared__ int16_t s_ei[kStage];
     __shared__ uint8_t s_er[kStage];
@@ -821,7 +826,7 @@ __global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, cons
             while (!mbar_try_wait(&s_bar, 0)) {
             }
     };
-    for (int t = threadIdx.x; t < kChunk / 32; t += kThreads) {
+    for (int t = threadIdx.x; t < kChunk / 32; t += NT) {
         s_seen[t] = 0;
         s_dup[t] = 0;
     }
@@ -832,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, cons
         theta_landed();  // no bulk copy may still target this CTA's shared memory
         return;
     }
-    for (int e = threadIdx.x; e < total; e += kThreads) {
+    for (int e = threadIdx.x; e < total; e += NT) {
         int r = 0;
         while (s_off[r + 1] <= e) ++r;
         const int64_t q = int64_t(r) * p.row_stride + s_j0[r] + (e - s_off[r]);
@@ -845,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, cons
     }
     __syncthreads();
     int nd_t = 0;
-    for (int e = threadIdx.x; e < total; e += kThreads) nd_t += (s_dup[s_ei[e] >> 5] >> (s_ei[e] & 31)) & 1u;
+    for (int e = threadIdx.x; e < total; e += NT) nd_t += (s_dup[s_ei[e] >> 5] >> (s_ei[e] & 31)) & 1u;
     nd_t = __reduce_add_sync(0xFFFFFFFFu, nd_t);
     if ((threadIdx.x & 31) == 0 && nd_t) atomicAdd(&s_nd, nd_t);
     __syncthreads();
@@ -861,7 +866,7 @@ __global__ void __launch_bounds__(kThreads, 7) g_stats_sparse(GlobalArgs p, cons
     __syncthreads();
     double nnz = 0.0;
     void* th = s_th4;
-    for (int e = threadIdx.x; e < total; e += kThreads) {
+    for (int e = threadIdx.x; e < total; e += NT) {
         const int i = s_ei[e];
         if ((s_dup[i >> 5] >> (i & 31)) & 1u) {
             s_dl[atomicAdd(&s_nd, 1)] = static_cast<int16_t>(e);
@@ -1538,9 +1543,9 @@ cudaError_t g_launch_stats_update(const GlobalArgs& a, const GWeights& w, int fi
         return !(v && v[0] == '0');
     }();
     if (sparse) {
-        e = cudaFuncSetAttribute(g_stats_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, int(th_smem));
+        e = cudaFuncSetAttribute(g_stats_sparse<kStatsThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(th_smem));
         if (e != cudaSuccess) return e;
-        g_stats_sparse<<<static_cast<unsigned>(global_chunks(a.dim)), kThreads, th_smem, s>>>(a, w, filled);
+        g_stats_sparse<kStatsThreads><<<static_cast<unsigned>(global_chunks(a.dim)), kStatsThreads, th_smem, s>>>(a, w, filled);
     } else {
         e = cudaFuncSetAttribute(g_stats_update, cudaFuncAttributeMaxDynamicSharedMemorySize, int(th_smem));
         if (e != cudaSuccess) return e;
