@@ -2161,17 +2161,21 @@ cudaError_t launch_kl(const StepArgs& a, cudaStream_t s) {
     X(BF16, BF16, F32)
 #endif
 
-// k_b <= 64: 4 candidate slots per lane; up to 256 (densities to 6.25%): 16.
+// Candidate slots per lane: k_b <= 64: 4; up to 128 (densities to 3.1%): 8
+// (half the shared memory of 16: 8 CTAs per SM instead of 6); up to 256
+// (densities to 6.25%): 16.
 constexpr int kWideKb = 32 * 16 / 2;
+__host__ __device__ constexpr int lean_capl(int kb) { return kb <= 32 * 4 / 2 ? kLCapL : (kb <= 32 * 8 / 2 ? 8 : 16); }
 
 template <int LPB>
 cudaError_t launch_ldt(const StepArgs& a, cudaStream_t s) {
-    const bool wide = a.per_block_k > kCap / 2;
+    const int capl = lean_capl(static_cast<int>(a.per_block_k));
     switch (dtype_key_w(a.g_dtype, a.p_dtype, a.v_dtype)) {
 #define MA_CASE(G_, P_, V_)                                                              \
         case dtype_key_w(G_, P_, V_):                                                    \
-            return wide ? launch_kl<KW<LPB, G_, P_, V_, false, 16>>(a, s)                \
-                        : launch_kl<KW<LPB, G_, P_, V_, false>>(a, s);
+            return capl == 16  ? launch_kl<KW<LPB, G_, P_, V_, false, 16>>(a, s)         \
+                   : capl == 8 ? launch_kl<KW<LPB, G_, P_, V_, false, 8>>(a, s)          \
+                               : launch_kl<KW<LPB, G_, P_, V_, false>>(a, s);
         MA_LEAN_DTYPES(MA_CASE)
 #undef MA_CASE
         default: return cudaErrorInvalidConfiguration;
@@ -2181,7 +2185,7 @@ cudaError_t launch_ldt(const StepArgs& a, cudaStream_t s) {
 // Shared memory of the fused lean kernel: per warp the LLayout area plus the
 // block's staged window rows (indices + values).
 size_t lean_smem_bytes(const StepArgs& a) {
-    const int capl = a.per_block_k > kCap / 2 ? 16 : kLCapL;
+    const int capl = lean_capl(static_cast<int>(a.per_block_k));
     const size_t vsz = a.v_dtype == F64 ? 8 : (a.v_dtype == F32 ? 4 : 2);
     const size_t rows = lean_stage_rows(a.m, a.kb_stride, int(vsz))
                             ? align_up(size_t(a.m) * a.kb_stride * 2, 16) + align_up(size_t(a.m) * a.kb_stride * vsz, 16)

@@ -127,13 +127,16 @@ def test_duplicate_coordinates_chunked(per_block, pdt):
     run_parity(d, dict(lr=1e-2, window=12), gdt="bf16", pdt=pdt, vdt="bf16", steps=16, grad_fn=g)
 
 
-@pytest.mark.parametrize("density,dt", [(0.02, "bf16"), (0.05, "bf16"), (0.0625, "f32")])
+@pytest.mark.parametrize("density,dt", [(0.02, "bf16"), (0.03, "f32"), (0.03125, "bf16"), (0.05, "bf16"),
+                                        (0.0625, "f32")])
 def test_wide_kb_lean_variant(density, dt):
-    # k_b in (64, 256] (densities 1.6%-6.25%): the 16-slot lean variant
+    # k_b in (64, 128] (densities 1.6%-3.1%): the 8-slot lean variant (k_b = 128
+    # at 3.125%); k_b in (128, 256] (to 6.25%): the 16-slot one
     run_parity(4096 * 6 + 900, dict(lr=1e-2, density=density, window=6), gdt=dt, pdt=dt, vdt="bf16",
                steps=10)
 
 
-def test_wide_kb_tie_heavy():
-    run_parity(4096 * 4, dict(lr=1e-2, density=0.04, window=4), gdt="f32", pdt="f32", vdt="bf16",
+@pytest.mark.parametrize("density", [0.025, 0.04])
+def test_wide_kb_tie_heavy(density):
+    run_parity(4096 * 4, dict(lr=1e-2, density=density, window=4), gdt="f32", pdt="f32", vdt="bf16",
                steps=8, levels=True)
