@@ -31,7 +31,7 @@ $(LIBDIR)/%.o: $(CSRC)/%.cpp $(HDRS)
 $(LIB): $(LIBDIR)/ma_nccl.o $(LIBDIR)/ma_bigblock.o $(LIBDIR)/ma_kernels.o $(LIBDIR)/ma_fast.o $(LIBDIR)/ma_warp.o $(LIBDIR)/ma_tile.o $(LIBDIR)/ma_global.o $(LIBDIR)/ma_capi.o $(LIBDIR)/microadam_b200.o
 	$(NVCC) $(NVFLAGS) -shared -o $@ $^ -ldl
 
-oracle:
+oracle: lib  # the adapter links the product library
 	$(MAKE) -s -C oracle $(if $(wildcard /root/reference/proj/src),all,oracle)
 
 sass: $(LIB)
