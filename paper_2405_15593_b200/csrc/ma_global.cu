@@ -317,23 +317,24 @@ __global__ void g_emit(GlobalArgs p) {
 // within) and written to the window row at the chunk's row offset, exactly as
 // g_emit writes it.
 template <int LPB, bool EMIT>
-__global__ void __launch_bounds__(kThreads, 4) g_requant8(GlobalArgs p) {
+__global__ void __launch_bounds__(kThreads, 4) g_requant8(GlobalArgs p, int64_t chunk0) {
     __shared__ double s_red[kThreads / 32][4];
     __shared__ int s_tmp[33];
-    const int64_t c0 = int64_t(blockIdx.x) * kChunk;
+    const int64_t cb = chunk0 + blockIdx.x;  // this CTA's chunk
+    const int64_t c0 = cb * kChunk;
     double rep[4] = {0.0, 0.0, 0.0, 0.0};
     int2 cs = make_int2(0, 0);
     uint64_t kstar = 0;
     if constexpr (EMIT) {
-        cs = p.sel_info[blockIdx.x];  // (row offset, ties to take in this chunk)
+        cs = p.sel_info[cb];  // (row offset, ties to take in this chunk)
         kstar = p.sel_state[0];
     }
     int64_t* ri = p.win_idx + int64_t(p.slot) * p.row_stride;
     if (EMIT && threadIdx.x == 0) {  // the new row's chunk bounds (what g_bounds would find)
         const int64_t nch = global_chunks_d(p.dim);
         int32_t* bd = p.bounds + int64_t(p.slot) * (nch + 1);
-        bd[blockIdx.x] = cs.x;
-        if (blockIdx.x == nch - 1) bd[nch] = static_cast<int32_t>(p.k);
+        bd[cb] = cs.x;
+        if (cb == nch - 1) bd[nch] = static_cast<int32_t>(p.k);
     }
 #pragma unroll kRq8Unroll
     for (int h = 0; h < kChunk / (8 * kThreads); ++h) {
@@ -477,8 +478,225 @@ __global__ void __launch_bounds__(kThreads, 4) g_requant8(GlobalArgs p) {
         if (threadIdx.x < 4) {
             double sum = 0.0;
             for (int w2 = 0; w2 < kThreads / 32; ++w2) sum += s_red[w2][threadIdx.x];
-            p.partials[int64_t(blockIdx.x) * kReportFields + threadIdx.x] = sum;
+            p.partials[cb * kReportFields + threadIdx.x] = sum;
         }
+    }
+}
+
+// g_requant8<L, true> in fp32 with exact fallbacks, for whole chunks of bf16
+// gradients (no StepReport): the blockwise lean kernel's pass-2 argument
+// (ma_warp.cu, above exact_bucket16) on this kernel's layout (thread t owns
+// the 8-groups t and t + 256, a bucket spans LPB threads).
+//   a32 = rn(g + fma(c, rn(level), rn(lo))) is within E_q + |a32| 2^-23 of
+//   the fp64 a (E_q = M 2^-21 + 2^-120, M = max(|lo|, |hi|) of the bucket's
+//   previous grid; M >= 2^100: E_q = inf, the bucket goes exact).
+//   * Selection: |a| >= K* implies |a32| >= Tf = rd((K* - E_q)(1 - 2^-22));
+//     only those elements are decoded in fp64 and compared with K* exactly.
+//   * Residual min / max, 4-bit codes: y = rn(r32 k2 + c2) = 257 + 2T + [0, 2G]
+//     (T = 15 (r - lo') / (hi' - lo')); byte 2 of y is the code unless y's
+//     fraction is below 2G: N = 1 / 31 mark the candidates of the exact
+//     minimum / maximum, even N a code boundary (IEEE quotient, quantize.cpp:
+//     51-53). Buckets the bound cannot settle take the fp64 path of
+//     g_requant8 (same operation order, so the same ties and codes).
+// one element's a in the reference's arithmetic, out of line (rare calls)
+__device__ __noinline__ double g_a1(const GlobalArgs* p, int64_t i) { return g_a(*p, i); }
+
+template <int LPB>
+__global__ void __launch_bounds__(kThreads, 4) g_requant8f(GlobalArgs p) {
+    __shared__ int s_tmp[33];
+    const int64_t cb = blockIdx.x, c0 = cb * kChunk;
+    int2 cs = p.sel_info[cb];  // (row offset, ties to take in this chunk)
+    const uint64_t kstar = p.sel_state[0];
+    const double kd = __longlong_as_double(static_cast<long long>(kstar));
+    int64_t* ri = p.win_idx + int64_t(p.slot) * p.row_stride;
+    if (threadIdx.x == 0) {  // the new row's chunk bounds (what g_bounds would find)
+        const int64_t nch = global_chunks_d(p.dim);
+        int32_t* bd = p.bounds + int64_t(p.slot) * (nch + 1);
+        bd[cb] = cs.x;
+        if (cb == nch - 1) bd[nch] = static_cast<int32_t>(p.k);
+    }
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned bm = LPB >= 32 ? 0xFFFFFFFFu : (((1u << LPB) - 1u) << (lane & ~(LPB - 1u)));  // the bucket's lanes
+#pragma unroll 1
+    for (int h = 0; h < kChunk / (8 * kThreads); ++h) {
+        const int64_t i0 = c0 + 8 * (int64_t(threadIdx.x) + int64_t(h) * kThreads);
+        const int64_t q = i0 >> p.bucket_shift;
+        const double2 mt = p.meta[q];
+        const double lv = p.level[q];
+        const uint4 v = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(p.grads) + i0);
+        const uint32_t cw = *reinterpret_cast<const uint32_t*>(p.codes + (i0 >> 1));
+        // one element's exact a from the registers (g_a: optim.cpp:166-168, quantize.cpp:164-178)
+        auto exact_a = [&](int e) -> double {
+            const int wi = e >> 1;
+            const uint32_t wv = wi == 0 ? v.x : (wi == 1 ? v.y : (wi == 2 ? v.z : v.w));
+            const float g = __uint_as_float((e & 1) ? (wv & 0xFFFF0000u) : (wv << 16));
+            const double c = static_cast<double>((cw >> (4 * e)) & 15u);
+            return __dadd_rn(static_cast<double>(g), __dadd_rn(__dmul_rn(c, lv), mt.x));
+        };
+        const double M = fmax(fabs(mt.x), fabs(mt.y));
+        float E = __double2float_ru(__dadd_ru(__dmul_ru(M, 0x1p-21), 0x1p-120));
+        if (!(M < 0x1p100)) E = CUDART_INF_F;
+        // a32 of the 8 elements
+        float a32[8];
+        {
+            const float2 lv2 = make_float2(__double2float_rn(lv), __double2float_rn(lv));
+            const float2 lo2 = make_float2(__double2float_rn(mt.x), __double2float_rn(mt.x));
+            const float2 m23 = make_float2(-8388608.0f, -8388608.0f);
+            const uint32_t ce = cw & 0x0F0F0F0Fu, co = (cw >> 4) & 0x0F0F0F0Fu;
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float2 c2 = make_float2(__uint_as_float(__byte_perm(ce, 0x4B000000u, 0x7540u | k)),
+                                        __uint_as_float(__byte_perm(co, 0x4B000000u, 0x7540u | k)));
+                c2 = __fadd2_rn(c2, m23);
+                const float2 a2 = __fadd2_rn(make_float2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xFFFF0000u)),
+                                             __ffma2_rn(c2, lv2, lo2));
+                a32[2 * k] = a2.x;
+                a32[2 * k + 1] = a2.y;
+            }
+        }
+        // ---- selection (compress.cpp:39-53 over the whole vector) + emit ----
+        float tf = __double2float_rd(__dmul_rd(__dsub_rd(kd, static_cast<double>(E)), 1.0 - 0x1p-22));
+        if (!(tf > 0.0f)) tf = 0.0f;
+        uint32_t maybe = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) maybe |= static_cast<uint32_t>(!(fabsf(a32[e]) < tf)) << e;
+        uint32_t gtm = 0, eqm = 0;
+        for (uint32_t m = maybe; m; m &= m - 1) {
+            const int e = __ffs(m) - 1;
+            const uint64_t k = key_of(exact_a(e));
+            gtm |= static_cast<uint32_t>(k > kstar) << e;
+            eqm |= static_cast<uint32_t>(k == kstar) << e;
+        }
+        int both;
+        const int pre = cta_excl_scan(__popc(gtm) | (__popc(eqm) << 16), s_tmp, both);
+        const int te = both >> 16;
+        uint32_t sw = gtm;
+        int tot = both & 0xFFFF;
+        int pos = cs.x + (pre & 0xFFFF);
+        if (te) {
+            int tie_before = pre >> 16;
+            for (uint32_t m = eqm; m; m &= m - 1) {
+                if (tie_before < cs.y) sw |= m & (0u - m);
+                ++tie_before;
+            }
+            pos = cs.x + cta_excl_scan(__popc(sw), s_tmp, tot);
+        }
+        for (uint32_t m = sw; m; m &= m - 1) {
+            const int e = __ffs(m) - 1;
+            ri[pos] = i0 + e;
+            st_val(p.win_val, p.v_dtype, int64_t(p.slot) * p.row_stride + pos, exact_a(e));
+            ++pos;
+        }
+        cs.x += tot;
+        cs.y -= te;
+        // ---- residual (compress.cpp:95-102) + re-quantization (quantize.cpp:15-24, 42-55) ----
+        float r32[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r32[e] = ((sw >> e) & 1u) ? 0.0f : a32[e];
+        float mn = fminf(fminf(fminf(r32[0], r32[1]), fminf(r32[2], r32[3])), fminf(fminf(r32[4], r32[5]), fminf(r32[6], r32[7])));
+        float mx = fmaxf(fmaxf(fmaxf(r32[0], r32[1]), fmaxf(r32[2], r32[3])), fmaxf(fmaxf(r32[4], r32[5]), fmaxf(r32[6], r32[7])));
+#pragma unroll
+        for (int off = 1; off < LPB; off <<= 1) {
+            mn = fminf(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, off));
+            mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+        }
+        const float eps = __fmaf_ru(fmaxf(fabsf(mn), fabsf(mx)), 0x1p-23f, E);
+        const float R = __fsub_rd(mx, mn);
+        const float den = __fsub_rd(R, 2.0f * eps);
+        const float k2 = __fdividef(30.0f, R);
+        const float cmag = 258.0f + fabsf(mn * k2);
+        const float G = __fmaf_ru(128.0f, __fdividef(eps, den), __fmaf_ru(cmag, 0x1p-23f, 0x1p-13f));
+        const bool fast = R >= 0x1p-100f && R <= 0x1p100f && den > 0.0f && G <= 0.0625f;  // bucket-uniform
+        uint32_t word = 0, bnd = 0;
+        bool bad = false;
+        double lmin = CUDART_INF, lmax = -CUDART_INF;
+        if (fast) {
+            const float c2 = __fmaf_rn(-mn, k2, 257.0f + G);
+            const uint32_t Gu = static_cast<uint32_t>(__fmaf_ru(2.0f, G, 0x1p-13f) * 32768.0f) + 1u;
+            uint32_t yb[8];
+            const float2 k22 = make_float2(k2, k2), c22 = make_float2(c2, c2);
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+                const float2 y = __ffma2_rn(make_float2(r32[e], r32[e + 1]), k22, c22);
+                yb[e] = __float_as_uint(y.x);
+                yb[e + 1] = __float_as_uint(y.y);
+            }
+            {
+                const uint32_t ev = __byte_perm(__byte_perm(yb[0], yb[2], 0x0062u), __byte_perm(yb[4], yb[6], 0x0062u), 0x5410u);
+                const uint32_t od = __byte_perm(__byte_perm(yb[1], yb[3], 0x0062u), __byte_perm(yb[5], yb[7], 0x0062u), 0x5410u);
+                word = (ev & 0x0F0F0F0Fu) | ((od << 4) & 0xF0F0F0F0u);
+            }
+            uint32_t fl = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) fl |= static_cast<uint32_t>((yb[e] & 0x7FFFu) < Gu) << e;
+            for (uint32_t m = fl; m; m &= m - 1) {  // min / max candidates and code boundaries (~2 per bucket)
+                const int e = __ffs(m) - 1;
+                uint32_t ye = yb[0];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) ye = k == e ? yb[k] : ye;
+                const uint32_t N = (ye >> 15) & 0xFFu;
+                const double rx = ((sw >> e) & 1u) ? 0.0 : exact_a(e);
+                bad |= N == 0u || N > 31u;
+                lmin = (N == 1u && rx < lmin) ? rx : lmin;
+                lmax = (N == 31u && rx > lmax) ? rx : lmax;
+                bnd |= static_cast<uint32_t>((N & 1u) == 0u && N - 1u < 31u) << e;
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < LPB; off <<= 1) {  // the bucket's exact extremes
+            const double ol = __shfl_xor_sync(0xFFFFFFFFu, lmin, off), oh = __shfl_xor_sync(0xFFFFFFFFu, lmax, off);
+            lmin = ol < lmin ? ol : lmin;
+            lmax = oh > lmax ? oh : lmax;
+            bad |= __shfl_xor_sync(0xFFFFFFFFu, static_cast<int>(bad), off) != 0;
+        }
+        bad = bad || !fast || !(lmin < CUDART_INF) || !(lmax > -CUDART_INF);  // bucket-uniform
+        double lo = lmin, hi = lmax;
+        if (bad) {  // the fp64 path of g_requant8 for this bucket (its lanes: bm)
+            double a[8];
+            g_a8(p, i0, a);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) a[e] = ((sw >> e) & 1u) ? 0.0 : a[e];
+            lo = CUDART_INF;
+            hi = -CUDART_INF;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                lo = a[e] < lo ? a[e] : lo;
+                hi = a[e] > hi ? a[e] : hi;
+            }
+#pragma unroll
+            for (int off = 1; off < LPB; off <<= 1) {
+                const double ol = __shfl_xor_sync(bm, lo, off);
+                const double oh = __shfl_xor_sync(bm, hi, off);
+                lo = ol < lo ? ol : lo;
+                hi = oh > hi ? oh : hi;
+            }
+            const double rng = __dsub_rn(hi, lo);
+            word = 0;
+            if (rng != 0.0) {
+                const double level = __ddiv_rn(rng, 15.0);
+#pragma unroll
+                for (int e = 7; e >= 0; --e) {
+                    double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(a[e], lo), level), 0.5));
+                    f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+                    word = (word << 4) | static_cast<uint32_t>(f);
+                }
+            }
+        } else if (bnd) {  // rare: quotients within the guard band of a code boundary
+            const double level = __ddiv_rn(__dsub_rn(hi, lo), 15.0);
+            for (uint32_t m = bnd; m; m &= m - 1) {
+                const int e = __ffs(m) - 1;
+                const double rx = ((sw >> e) & 1u) ? 0.0 : exact_a(e);
+                double f = floor(__dadd_rn(__ddiv_rn(__dsub_rn(rx, lo), level), 0.5));
+                f = f < 0.0 ? 0.0 : (f > 15.0 ? 15.0 : f);
+                word = (word & ~(15u << (4 * e))) | (static_cast<uint32_t>(f) << (4 * e));
+            }
+        }
+        // every lane of the bucket is done reading the previous grid (g_a) before
+        // its first lane overwrites it
+        __syncwarp();
+        *reinterpret_cast<uint32_t*>(p.codes + (i0 >> 1)) = word;
+        if ((threadIdx.x & (LPB - 1)) == 0) p.meta[q] = make_double2(lo, hi);
     }
 }
 
@@ -1509,9 +1727,21 @@ cudaError_t g_launch_requant(const GlobalArgs& a, cudaStream_t s) {
         return cudaGetLastError();
     }
     const bool emit = g_fused_emit(a);  // g_launch_emit left G3 to this kernel
+    // the fp32 form (g_requant8f) for whole chunks of bf16 gradients without a
+    // StepReport; the partial last chunk (and everything else) in fp64
+    const unsigned nfull = static_cast<unsigned>(a.dim / kChunk);
+    const char* f32_env = std::getenv("MA_GLOBAL_RQ_FP32");  // A/B: 0 = the fp64 kernel everywhere
+    const bool fp32 = !(f32_env && f32_env[0] == '0') && a.g_dtype == BF16 && !a.partials &&
+                      (reinterpret_cast<uintptr_t>(a.grads) & 15u) == 0;
 #define MA_RQ8(L)                                                                   \
-    if (emit) g_requant8<L, true><<<nch, kThreads, 0, s>>>(a);                     \
-    else g_requant8<L, false><<<nch, kThreads, 0, s>>>(a);                         \
+    if (emit && fp32) {                                                             \
+        if (nfull) g_requant8f<L><<<nfull, kThreads, 0, s>>>(a);                    \
+        if (nfull < nch) g_requant8<L, true><<<nch - nfull, kThreads, 0, s>>>(a, nfull); \
+    } else if (emit) {                                                              \
+        g_requant8<L, true><<<nch, kThreads, 0, s>>>(a, 0);                          \
+    } else {                                                                        \
+        g_requant8<L, false><<<nch, kThreads, 0, s>>>(a, 0);                         \
+    }                                                                               \
     return cudaGetLastError();
     switch (a.bucket) {  // the register path for 8 <= B_q <= 256
         case 8: MA_RQ8(1)

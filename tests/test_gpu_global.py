@@ -194,3 +194,29 @@ def test_global_tiled_allocation_scan(monkeypatch):
         slot = (eng.counters()[1] + hp["window"] - 1) % hp["window"]
         assert np.array_equal(eng.window().indices[slot], so.win_idx[slot]), f"selection @ {s}"
         assert np.array_equal(_bits(_host(p)), _bits(so.params)), f"θ @ {s}"
+
+
+@pytest.mark.parametrize("bucket,levels", [(8, False), (16, True), (64, True), (256, False)])
+def test_global_fp32_requant_buckets(bucket, levels):
+    # g_requant8f (bf16 gradients, whole chunks) for every register bucket
+    # width (B_q = 8 .. 256: 1 .. 32 threads per bucket), tie-heavy gradients
+    # (constant / two-valued buckets send whole buckets to the fp64 path);
+    # d leaves a partial last chunk for the fp64 kernel
+    d = 4096 * 6 + 1000
+    hp = dict(lr=1e-2, window=3, density=0.02, bucket=bucket)
+    torch = _torch()
+    th0 = _host(_dev(oracle.synth(1, 0, 0, d, "bf16"), "bf16"))
+    orc = oracle.Oracle(th0, dict(hp, block=d), param_dtype="bf16", value_dtype="bf16")
+    eng = _global_engine(d, hp, "bf16", "bf16")
+    p = _dev(th0, "bf16")
+    for s in range(1, 7):
+        g = _host(_dev(oracle.synth(11, s, 0, d, "bf16", levels=levels) * (2.0 ** (3 * (s % 3))), "bf16"))
+        orc.step(g, hp["lr"])
+        eng.step(p, _dev(g, "bf16"), hp["lr"])
+        torch.cuda.synchronize()
+        so = orc.state()
+        eb = eng.error_buffer()
+        assert np.array_equal(eb.codes, so.codes), f"codes @ {s}"
+        assert np.array_equal(_bits(eb.lo), _bits(so.lo)), f"lo @ {s}"
+        assert np.array_equal(_bits(eb.hi), _bits(so.hi)), f"hi @ {s}"
+        assert np.array_equal(_bits(_host(p)), _bits(so.params)), f"θ @ {s}"
