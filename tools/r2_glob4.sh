@@ -7,4 +7,4 @@ echo "== fp32 $(timeout 600 python tools/bench_global.py 1.3e9 2>&1 | cut -c1-50
 echo "== fp64 $(MA_GLOBAL_RQ_FP32=0 timeout 600 python tools/bench_global.py 1.3e9 2>&1 | cut -c1-50)"
 done
 timeout 600 python tools/bench_global.py 6.738415616e9 2>&1 | cut -c1-200
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:g_requant -c 30 --csv --log-file gpurun_out/${tag}_launches.csv python tools/bench_global.py 1.3e9 > /dev/null 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:g_stats -c 30 --csv --log-file gpurun_out/${tag}_launches.csv python tools/bench_global.py 1.3e9 > /dev/null 2>&1
