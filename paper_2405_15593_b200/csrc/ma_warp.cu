@@ -918,6 +918,20 @@ __device__ __forceinline__ uint32_t prmt_imm(uint32_t a, uint32_t b, int k) {
     }
     return d;
 }
+// 0x4B000000 read back from shared memory (a volatile load ptxas cannot fold):
+// with a literal, ptxas under register pressure encodes the constant as PRMT's
+// immediate and moves each selector from a uniform register instead (one extra
+// IMAD.U32 per decoded element in passes 1 and 2).
+__device__ __forceinline__ uint32_t opaque_kmag(const int* s_word) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.b32 %0, [%1];"
+                 : "=r"(v)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(s_word))));
+    return v;
+}
+#ifndef MA_LEAN_PFLAG
+#define MA_LEAN_PFLAG 1  // lean pass 2: code-boundary flags computed two elements per word
+#endif
 #ifndef MA_LEAN_CAPL
 #define MA_LEAN_CAPL 4  // lean kernel: exact-stage candidate slots per lane
 #endif
@@ -1481,6 +1495,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         s_sel[lane * 4 + k] = 0;
         s_dup[lane * 4 + k] = 0;
     }
+    if (lane == 0) s_misc[8] = 0x4B000000;  // opaque_kmag's word
     __syncwarp();
 
 #if MA_LEAN_PROF
@@ -1498,11 +1513,11 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         const unsigned char* gp = static_cast<const unsigned char*>(p.grads) + (base + lane * 8) * gsz;
         const uint32_t* cp = reinterpret_cast<const uint32_t*>(p.codes + ((base + lane * 8) >> 1));
         const float4* lf = s_llf + (lane * 8) / BUCKET;
-        uint32_t kmag;  // 0x4B000000 held in a register: the permutes below take immediate selectors
-        asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(kmag));
         const float2 m23 = make_float2(-kTwo23, -kTwo23);
 #pragma unroll 1
         for (int w = 0; w < 4; ++w) {
+            // 0x4B000000 in a register: the permutes below take immediate selectors
+            const uint32_t kmag = opaque_kmag(s_misc + 8);
             uint32_t acc = 0;
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
@@ -1829,12 +1844,11 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         // (re-zeroed below before ADAM_STATS uses them)
         unsigned char* s_scr = ws + L.wpref;
         const unsigned char* gp = static_cast<const unsigned char*>(p.grads) + base * gsz;
-        uint32_t kmag;
-        asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(kmag));
         const float2 m23 = make_float2(-kTwo23, -kTwo23);
 #pragma unroll 1
         for (int j = 0; j < kBlk / 512; ++j) {
             const int e0 = j * 512 + lane * 16;
+            const uint32_t kmag = opaque_kmag(s_misc + 8);
             if ((PH & 2) && j == 4 && lane == 0)
                 prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
             const Raw16<KT::GDT> raw = load_raw16<KT::GDT, !KT::RS>(gp + size_t(e0) * gsz);
@@ -1898,9 +1912,22 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                 }
                 w0 = pack_codes8(yb);
                 w1 = pack_codes8(yb + 8);
+#if MA_LEAN_PFLAG
+                // Flags two elements per word: the low halves of y_2k, y_2k+1
+                // (15 fraction bits each) + (0x8000 - Gu) set bit 15 / 31 exactly
+                // when the fraction is >= Gu (Gu <= 4097: no carry between the
+                // halves); the NOT-flagged bits land at 15 - k / 31 - k.
+                const uint32_t Cg = (0x8000u - Gu) * 0x10001u;
+                uint32_t nf = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    nf |= (((__byte_perm(yb[2 * k], yb[2 * k + 1], 0x5410u) & 0x7FFF7FFFu) + Cg) & 0x80008000u) >> k;
+                uint32_t fl = ~nf & 0xFF00FF00u;  // bit b -> element 30 - 2 (b & 15) + (b >> 4)
+#else
                 uint32_t fl = 0;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) fl |= static_cast<uint32_t>((yb[i] & 0x7FFFu) < Gu) << i;
+#endif
                 if (fl) {  // min / max candidates and code boundaries (~2 per bucket)
                     // this lane's raw gradients -> its 64-byte scratch slot (dead
                     // candidate / bitmap area) so flagged elements index them
@@ -1910,7 +1937,12 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                     const double2 q = s_ll[e0 / BUCKET];
                     const uint64_t cw64 = (static_cast<uint64_t>(cw.y) << 32) | cw.x;
                     do {  // branch-free body: every flagged element takes the same path
+#if MA_LEAN_PFLAG
+                        const int fb = __ffs(fl) - 1;
+                        const int i = 30 - 2 * (fb & 15) + (fb >> 4);
+#else
                         const int i = __ffs(fl) - 1;
+#endif
                         fl &= fl - 1;
                         const bool s = (sel16 >> i) & 1u;
                         const uint32_t c = static_cast<uint32_t>(cw64 >> (4 * i)) & 15u;
