@@ -283,5 +283,19 @@ __device__ uint32_t block_topk(const double (&a)[EPT], uint32_t valid, int kb, u
     return sel;
 }
 
+// 0x4B000000 (2^23 as fp32 bits, the nibble -> float decode constant) read back
+// from shared memory by a volatile load ptxas cannot fold: with a literal, ptxas
+// under register pressure encodes the constant as PRMT's immediate and moves
+// every selector from a uniform register instead (one extra IMAD.U32 per
+// decoded element). The word is written by the reading thread itself (or by
+// the warp before a __syncwarp).
+__device__ __forceinline__ uint32_t opaque_kmag(const int* s_word) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.b32 %0, [%1];"
+                 : "=r"(v)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(s_word))));
+    return v;
+}
+
 }  // namespace dev
 }  // namespace ma

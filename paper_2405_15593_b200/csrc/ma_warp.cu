@@ -918,17 +918,13 @@ __device__ __forceinline__ uint32_t prmt_imm(uint32_t a, uint32_t b, int k) {
     }
     return d;
 }
-// 0x4B000000 read back from shared memory (a volatile load ptxas cannot fold):
-// with a literal, ptxas under register pressure encodes the constant as PRMT's
-// immediate and moves each selector from a uniform register instead (one extra
-// IMAD.U32 per decoded element in passes 1 and 2).
-__device__ __forceinline__ uint32_t opaque_kmag(const int* s_word) {
-    uint32_t v;
-    asm volatile("ld.volatile.shared.b32 %0, [%1];"
-                 : "=r"(v)
-                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(s_word))));
-    return v;
-}
+#ifndef MA_LEAN_THPF_LOOP
+// θ prefetch for ADAM_STATS (A/B at 7B, same box): 0 = one bulk prefetch before
+// the pass-2 loop (19.03 ms), 1 = bulk prefetch at iteration 4 (18.68 ms, kept
+// although its uniform-address sequence runs predicated on every iteration),
+// 2 = per-lane line prefetches at iteration 4 (18.71 ms)
+#define MA_LEAN_THPF_LOOP 1
+#endif
 #ifndef MA_LEAN_PFLAG
 #define MA_LEAN_PFLAG 1  // lean pass 2: code-boundary flags computed two elements per word
 #endif
@@ -1845,12 +1841,26 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         unsigned char* s_scr = ws + L.wpref;
         const unsigned char* gp = static_cast<const unsigned char*>(p.grads) + base * gsz;
         const float2 m23 = make_float2(-kTwo23, -kTwo23);
+#if MA_LEAN_THPF_LOOP == 0
+        if ((PH & 2) && lane == 0) prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
+#endif
 #pragma unroll 1
         for (int j = 0; j < kBlk / 512; ++j) {
             const int e0 = j * 512 + lane * 16;
             const uint32_t kmag = opaque_kmag(s_misc + 8);
+#if MA_LEAN_THPF_LOOP == 1
             if ((PH & 2) && j == 4 && lane == 0)
                 prefetch_l2(static_cast<const unsigned char*>(p.params) + base * psz, kBlk * psz);
+#elif MA_LEAN_THPF_LOOP == 2
+            if ((PH & 2) && j == 4) {
+                // per-lane L2 prefetch of the block's θ lines (no uniform-address
+                // sequence for a bulk prefetch, which ran predicated every iteration)
+                const unsigned char* th = static_cast<const unsigned char*>(p.params) + base * psz;
+#pragma unroll
+                for (int q = lane * 128; q < kBlk * psz; q += 32 * 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(th + q));
+            }
+#endif
             const Raw16<KT::GDT> raw = load_raw16<KT::GDT, !KT::RS>(gp + size_t(e0) * gsz);
             const uint2 cw = *reinterpret_cast<const uint2*>(p.codes + ((base + e0) >> 1));
             const float4 f = s_llf[e0 / BUCKET];
