@@ -925,6 +925,9 @@ __device__ __forceinline__ uint32_t prmt_imm(uint32_t a, uint32_t b, int k) {
 // 2 = per-lane line prefetches at iteration 4 (18.71 ms)
 #define MA_LEAN_THPF_LOOP 1
 #endif
+#ifndef MA_LEAN_SIGNCOUNT
+#define MA_LEAN_SIGNCOUNT 1  // lean select: candidate counts as sums of sign bits
+#endif
 #ifndef MA_LEAN_PFLAG
 #define MA_LEAN_PFLAG 1  // lean pass 2: code-boundary flags computed two elements per word
 #endif
@@ -1634,10 +1637,22 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
         }
     };
     auto count_ge = [&](uint32_t v) {
+#if MA_LEAN_SIGNCOUNT
+        // keys kh < 2^31 and 0 <= v <= 2^31: kh >= v <=> (v - 1 - kh) < 0 as a
+        // 32-bit signed value, so the count is a sum of sign bits (IADD3 + LEA.HI
+        // per slot instead of a compare and a select); v above 2^31 (a carried
+        // threshold near the inf / NaN keys) counts nothing, as v = 2^31 does
+        const uint32_t vm1 = min(v, 0x80000000u) - 1u;
+        uint32_t c = 0;
+#pragma unroll
+        for (int s = 0; s < KT::CAPL; ++s) c += (vm1 - kh[s]) >> 31;
+        return __reduce_add_sync(0xFFFFFFFFu, static_cast<int>(c));
+#else
         int c = 0;
 #pragma unroll
         for (int s = 0; s < KT::CAPL; ++s) c += kh[s] >= v;
         return __reduce_add_sync(0xFFFFFFFFu, c);
+#endif
     };
     load_keys();
     int clo = ncand < 0 ? 0 : count_ge(base16 << 16);
