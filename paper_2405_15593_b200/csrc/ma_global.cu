@@ -504,8 +504,8 @@ __device__ __noinline__ double g_a1(const GlobalArgs* p, int64_t i) { return g_a
 template <int LPB>
 __global__ void __launch_bounds__(kThreads, 4) g_requant8f(GlobalArgs p) {
     __shared__ int s_tmp[33];
-    __shared__ int s_kmag;
-    s_kmag = 0x4B000000;  // opaque_kmag's word (every thread writes the same value)
+    __shared__ int s_kmag[kThreads / 32];
+    s_kmag[threadIdx.x >> 5] = 0x4B000000;  // opaque_kmag's word, one per warp (each lane reads its own store)
     const int64_t cb = blockIdx.x, c0 = cb * kChunk;
     int2 cs = p.sel_info[cb];  // (row offset, ties to take in this chunk)
     const uint64_t kstar = p.sel_state[0];
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 4) g_requant8f(GlobalArgs p) {
             const float2 m23 = make_float2(-8388608.0f, -8388608.0f);
             const uint32_t ce = cw & 0x0F0F0F0Fu, co = (cw >> 4) & 0x0F0F0F0Fu;
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-            const uint32_t kmag = opaque_kmag(&s_kmag);
+            const uint32_t kmag = opaque_kmag(&s_kmag[threadIdx.x >> 5]);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 float2 c2 = make_float2(__uint_as_float(__byte_perm(ce, kmag, 0x7540u | k)),
@@ -1239,8 +1239,8 @@ __global__ void g_count_cand(GlobalArgs p) {
 __global__ void __launch_bounds__(256, 6) g_bracket(GlobalArgs p, int pass) {
     __shared__ unsigned long long s_above;
     __shared__ unsigned s_cn;  // keys collected into this CTA's segment
-    __shared__ int s_kmag;
-    s_kmag = 0x4B000000;  // opaque_kmag's word (every thread writes the same value)
+    __shared__ int s_kmag[8];
+    s_kmag[threadIdx.x >> 5] = 0x4B000000;  // opaque_kmag's word, one per warp (each lane reads its own store)
     if (pass == 0 ? p.sel_state[6] == 0 : p.sel_state[11] == 0) return;  // no bracket yet / no retry
     // [lo, hi] widened to whole 2^32 steps of the key: the tests below read
     // only the high word of |a| (keys >= lo32 << 32 and <= hi32 << 32 | ~0u)
@@ -1285,7 +1285,7 @@ __global__ void __launch_bounds__(256, 6) g_bracket(GlobalArgs p, int pass) {
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
             const float2 lv2 = make_float2(lv32, lv32), lo2 = make_float2(lo32f, lo32f);
             const float2 m23 = make_float2(-8388608.0f, -8388608.0f);
-            const uint32_t kmag = opaque_kmag(&s_kmag);
+            const uint32_t kmag = opaque_kmag(&s_kmag[threadIdx.x >> 5]);
             hit = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
