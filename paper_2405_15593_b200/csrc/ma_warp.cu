@@ -925,6 +925,19 @@ __device__ __forceinline__ uint32_t prmt_imm(uint32_t a, uint32_t b, int k) {
 // 2 = per-lane line prefetches at iteration 4 (18.71 ms)
 #define MA_LEAN_THPF_LOOP 1
 #endif
+#ifndef MA_LEAN_BADENC
+#define MA_LEAN_BADENC 0  // A/B: per-lane `bad` carried in the lmin shuffle as -inf (18.73 vs 18.42 ms at 7B: rejected)
+#endif
+#ifndef MA_LEAN_SIGNREP
+#define MA_LEAN_SIGNREP 1  // lean pass 1: hit-mask bytes by sign-replicating permutes
+#endif
+// bytes 0 / 1 = the sign of a / b replicated (prmt generic mode: a selector
+// nibble with bit 3 set copies the msb of the selected byte to all 8 bits)
+__device__ __forceinline__ uint32_t prmt_sr(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, 0x00FB;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
 #ifndef MA_LEAN_SIGNCOUNT
 #define MA_LEAN_SIGNCOUNT 1  // lean select: candidate counts as sums of sign bits
 #endif
@@ -1539,11 +1552,20 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                     sg[2 * k] = __float_as_uint(d.x);
                     sg[2 * k + 1] = __float_as_uint(d.y);
                 }
+#if MA_LEAN_SIGNREP
+                // sign-replicated top bytes (prmt selector nibbles 0xB / 0xF: byte 3 of
+                // each operand, msb replicated): byte k of w0 / w1 is 0xFF when
+                // element k / k + 4 misses, so no shifts are needed below
+                const uint32_t w0 = __byte_perm(prmt_sr(sg[0], sg[1]), prmt_sr(sg[2], sg[3]), 0x5410u);
+                const uint32_t w1 = __byte_perm(prmt_sr(sg[4], sg[5]), prmt_sr(sg[6], sg[7]), 0x5410u);
+                const uint32_t b = (w0 & 0x01010101u) | (w1 & 0x02020202u);
+#else
                 // top (sign) bytes of elements 0..3 and 4..7
                 const uint32_t w0 = __byte_perm(__byte_perm(sg[0], sg[1], 0x0073u), __byte_perm(sg[2], sg[3], 0x0073u), 0x5410u);
                 const uint32_t w1 = __byte_perm(__byte_perm(sg[4], sg[5], 0x0073u), __byte_perm(sg[6], sg[7], 0x0073u), 0x5410u);
                 // byte k: bit 0 = sign of element k, bit 1 = sign of element k + 4
                 const uint32_t b = ((w0 >> 7) & 0x01010101u) | ((w1 >> 6) & 0x02020202u);
+#endif
                 acc = (acc << 2) | b;
             }
             cm0 = cm1;
@@ -1986,6 +2008,17 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                     } while (fl);
                 }
             }
+#if MA_LEAN_BADENC
+            // a lane's `bad` travels as lmin = -inf (a fast-path candidate is finite)
+            if (bad) lmin = -CUDART_INF;
+#pragma unroll
+            for (int off = 1; off < LP2; off <<= 1) {  // the bucket's exact extremes (all lanes)
+                const double ol = __shfl_xor_sync(0xFFFFFFFFu, lmin, off), oh = __shfl_xor_sync(0xFFFFFFFFu, lmax, off);
+                lmin = ol < lmin ? ol : lmin;
+                lmax = oh > lmax ? oh : lmax;
+            }
+            bad = !fast || !(lmin > -CUDART_INF && lmin < CUDART_INF) || !(lmax > -CUDART_INF);  // bucket-uniform
+#else
 #pragma unroll
             for (int off = 1; off < LP2; off <<= 1) {  // the bucket's exact extremes (all lanes)
                 const double ol = __shfl_xor_sync(0xFFFFFFFFu, lmin, off), oh = __shfl_xor_sync(0xFFFFFFFFu, lmax, off);
@@ -1994,6 +2027,7 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                 bad |= __shfl_xor_sync(0xFFFFFFFFu, bad, off);
             }
             bad = bad || !fast || !(lmin < CUDART_INF) || !(lmax > -CUDART_INF);  // bucket-uniform
+#endif
             double lo_n = lmin, hi_n = lmax;
             if (bad) {
                 const Bucket16 o = exact_bucket16<KT>(&p, base, e0, sel16, s_ll[e0 / BUCKET], bm, LP2);
