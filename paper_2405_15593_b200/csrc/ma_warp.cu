@@ -925,6 +925,12 @@ __device__ __forceinline__ uint32_t prmt_imm(uint32_t a, uint32_t b, int k) {
 // 2 = per-lane line prefetches at iteration 4 (18.71 ms)
 #define MA_LEAN_THPF_LOOP 1
 #endif
+#ifndef MA_LEAN_MIXADD
+#define MA_LEAN_MIXADD 0  // A/B: a = g + e by mixed bf16 + fp32 adds (FHADD.BF16) in pass 1 (7B 18.64 ms) / both passes (18.47) vs 18.41: off
+#endif
+#ifndef MA_LEAN_MIXADD2
+#define MA_LEAN_MIXADD2 MA_LEAN_MIXADD  // the same in pass 2
+#endif
 #ifndef MA_LEAN_BADENC
 #define MA_LEAN_BADENC 0  // A/B: per-lane `bad` carried in the lmin shuffle as -inf (18.73 vs 18.42 ms at 7B: rejected)
 #endif
@@ -1086,6 +1092,23 @@ __device__ __forceinline__ float g32_of(const Raw16<DT>& r, int i) {  // i: comp
         const int k = i & 3;
         return __uint_as_float(k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w)));
     }
+}
+
+// rn(bf16 + fp32) of the two bf16 halves of w (element 2k in the low half)
+// and x: the mixed-precision add (FHADD.BF16) reads each half in place, so
+// the gradient needs no unpacking (bit-identical to widening, then __fadd_rn)
+__device__ __forceinline__ float2 add_bf16x2_f32(uint32_t w, float2 x) {
+    float r0, r1;
+    asm("{ .reg .b16 lo, hi; mov.b32 {lo, hi}, %2; add.rn.f32.bf16 %0, lo, %3; add.rn.f32.bf16 %1, hi, %4; }"
+        : "=f"(r0), "=f"(r1)
+        : "r"(w), "f"(x.x), "f"(x.y));
+    return make_float2(r0, r1);
+}
+template <int DT>
+__device__ __forceinline__ uint32_t raw16_word(const Raw16<DT>& r, int j) {  // j: compile-time after unrolling
+    const uint4 v = r.v[j >> 2];
+    const int k = j & 3;
+    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
 }
 
 // a32 of one block element, recomputed exactly as the packed decode does it.
@@ -1547,7 +1570,17 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                     float2 c = make_float2(__uint_as_float(prmt_imm<0x7540u>(ce, kmag, k)),
                                            __uint_as_float(prmt_imm<0x7540u>(co, kmag, k)));
                     c = __fadd2_rn(c, m23);
+#if MA_LEAN_MIXADD
+                    float2 a;
+                    if constexpr (KT::GDT == BF16) {
+                        const uint32_t wk = k == 0 ? r.v[0].x : (k == 1 ? r.v[0].y : (k == 2 ? r.v[0].z : r.v[0].w));
+                        a = add_bf16x2_f32(wk, __ffma2_rn(c, lv2, lo2));
+                    } else {
+                        a = __fadd2_rn(make_float2(g[2 * k], g[2 * k + 1]), __ffma2_rn(c, lv2, lo2));
+                    }
+#else
                     const float2 a = __fadd2_rn(make_float2(g[2 * k], g[2 * k + 1]), __ffma2_rn(c, lv2, lo2));
+#endif
                     const float2 d = __ffma2_rn(a, a, t2);
                     sg[2 * k] = __float_as_uint(d.x);
                     sg[2 * k + 1] = __float_as_uint(d.y);
@@ -1915,8 +1948,17 @@ __global__ void __launch_bounds__(32 * kWarps, MA_LEAN_MINB) microadam_step_lean
                                                 __uint_as_float(prmt_imm<0x7540u>(co, kmag, k)));
                         cc = __fadd2_rn(cc, m23);
                         const int i = 8 * h + 2 * k;
+#if MA_LEAN_MIXADD2
+                        float2 a;
+                        if constexpr (KT::GDT == BF16)
+                            a = add_bf16x2_f32(raw16_word<KT::GDT>(raw, i >> 1), __ffma2_rn(cc, lv2, lo2));
+                        else
+                            a = __fadd2_rn(make_float2(g32_of<KT::GDT>(raw, i), g32_of<KT::GDT>(raw, i + 1)),
+                                           __ffma2_rn(cc, lv2, lo2));
+#else
                         const float2 a = __fadd2_rn(make_float2(g32_of<KT::GDT>(raw, i), g32_of<KT::GDT>(raw, i + 1)),
                                                     __ffma2_rn(cc, lv2, lo2));
+#endif
                         r[i] = a.x;
                         r[i + 1] = a.y;
                     }
